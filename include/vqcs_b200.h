@@ -1,0 +1,237 @@
+/*
+ * vqcs_b200.h — C-ABI of the B200-native state-vector / density-matrix core.
+ *
+ * This is the drop-in boundary for the data-parallel path of the C++
+ * reference `vqcs` (/root/reference/proj/include/vqcs). The reference has no
+ * FFI: its "operator API" is a header-only C++ template API. Every entry point
+ * below replaces one function of that API (cited per function) with plain C
+ * types, so a maintainer can bind it from the reference's C++ (see
+ * include/vqcs_b200.hpp and INTEGRATION.md) or from ctypes.
+ *
+ * Conventions (identical to the reference):
+ *   - complex128 amplitudes, interleaved (re, im) doubles;
+ *   - qubit j (1-based) <-> bit j-1 of the flat amplitude index
+ *     (state.hpp:17-22);
+ *   - a density matrix of n qubits is stored as 4^n entries,
+ *     entry(row, col) at row + col * 2^n, i.e. a 2n-qubit pseudo state with
+ *     ket qubits 1..n and bra qubits n+1..2n (state.hpp:259-327);
+ *   - gate matrices are column-major 2^m x 2^m, first listed position = local
+ *     LSB (gates.hpp:18-22).
+ *
+ * Error handling: every function returns a vqb_status. Nonzero codes 1..11
+ * map 1:1 onto the reference exception classes (errors.hpp:23-96); CUDA and
+ * NCCL failures get their own codes. vqb_last_error() returns a thread-local
+ * message for the last failure on the calling thread.
+ *
+ * Calls are synchronous at the API (the reference's calls are synchronous,
+ * threading.hpp:54-70): a function returns after its device work completed.
+ * One CUDA stream per state handle; callers need exclusive access to a state
+ * during a call.
+ */
+#ifndef VQCS_B200_H
+#define VQCS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define VQB_API __attribute__((visibility("default")))
+#else
+#define VQB_API
+#endif
+
+/* ---- status codes: errors.hpp:23-96, in declaration order ---- */
+typedef enum vqb_status {
+    VQB_OK = 0,
+    VQB_ERR_SIZE = 1,           /* SizeError            errors.hpp:29 */
+    VQB_ERR_SHAPE = 2,          /* ShapeError           errors.hpp:35 */
+    VQB_ERR_VALIDITY = 3,       /* ValidityError        errors.hpp:42 */
+    VQB_ERR_DOMAIN = 4,         /* DomainError          errors.hpp:48 */
+    VQB_ERR_INDEX = 5,          /* IndexError           errors.hpp:54 */
+    VQB_ERR_TYPE = 6,           /* TypeError            errors.hpp:61 */
+    VQB_ERR_UNSUPPORTED = 7,    /* UnsupportedError     errors.hpp:68 */
+    VQB_ERR_DEGENERATE = 8,     /* DegenerateStateError errors.hpp:75 */
+    VQB_ERR_NONINVERTIBLE = 9,  /* NonInvertibleChannelError errors.hpp:81 */
+    VQB_ERR_IO = 10,            /* IoError              errors.hpp:87 */
+    VQB_ERR_USAGE = 11,         /* UsageError           errors.hpp:93 */
+    VQB_ERR_CUDA = 20,          /* CUDA runtime failure (no reference analogue) */
+    VQB_ERR_NCCL = 21,          /* NCCL failure (no reference analogue) */
+    VQB_ERR_INTERNAL = 22
+} vqb_status;
+
+/* ---- GateKind, same numbering as gates.hpp:38-61 ---- */
+typedef enum vqb_gate_kind {
+    VQB_GATE_GENERIC = 0,
+    VQB_GATE_X, VQB_GATE_Y, VQB_GATE_Z, VQB_GATE_H, VQB_GATE_S, VQB_GATE_T,
+    VQB_GATE_SQRTX, VQB_GATE_SQRTY, VQB_GATE_SWAP, VQB_GATE_ISWAP, VQB_GATE_CZ,
+    VQB_GATE_CNOT, VQB_GATE_TOFFOLI, VQB_GATE_FREDKIN, VQB_GATE_RX, VQB_GATE_RY,
+    VQB_GATE_RZ, VQB_GATE_CRX, VQB_GATE_CRY, VQB_GATE_CRZ, VQB_GATE_FSIM
+} vqb_gate_kind;
+
+/* ---- ChannelKind, same numbering as gates.hpp:63-68 ---- */
+typedef enum vqb_channel_kind {
+    VQB_CHANNEL_GENERIC = 0,
+    VQB_CHANNEL_AMPLITUDE_DAMPING = 1,
+    VQB_CHANNEL_PHASE_DAMPING = 2,
+    VQB_CHANNEL_DEPOLARIZING = 3
+} vqb_channel_kind;
+
+enum { VQB_ELEM_GATE = 0, VQB_ELEM_CHANNEL = 1 };
+enum { VQB_MAX_POSITIONS = 6, VQB_MAX_PARAMS = 5 };
+
+typedef struct vqb_c128 {
+    double re;
+    double im;
+} vqb_c128;
+
+/*
+ * One circuit element: a GateOp (gates.hpp:106-130) or a ChannelOp
+ * (gates.hpp:133-141). Nested circuits (circuit.hpp:40) are passed flattened
+ * in depth-first order, which is the reference's traversal order
+ * (circuit.hpp:69-102).
+ */
+typedef struct vqb_op {
+    int32_t elem;                        /* VQB_ELEM_GATE | VQB_ELEM_CHANNEL */
+    int32_t kind;                        /* vqb_gate_kind | vqb_channel_kind */
+    int32_t num_positions;               /* m >= 1 */
+    int32_t positions[VQB_MAX_POSITIONS];/* 1-based; first = local LSB */
+    int32_t num_params;                  /* 0, 1 (rotations) or 5 (FSIM) */
+    double params[VQB_MAX_PARAMS];
+    int32_t is_param[VQB_MAX_PARAMS];    /* nonzero = variational */
+    /* Gate: column-major 2^m x 2^m matrix, or NULL to build it from kind and
+     * params exactly as standard_gate/parametric_gate do (gates.hpp:439-533). */
+    const vqb_c128 *matrix;
+    /* Channel: num_kraus column-major 2^m x 2^m Kraus operators back to back,
+     * or NULL for a named channel built from params[0] as standard_channel
+     * does (gates.hpp:657-704). */
+    int32_t num_kraus;
+    const vqb_c128 *kraus;
+} vqb_op;
+
+/* One Pauli string (observables.hpp:38-65): product of (qubit, label) factors
+ * with distinct 1-based qubits and labels 'x'|'y'|'z' (either case); an empty
+ * factor list is the identity term. */
+typedef struct vqb_pauli_term {
+    vqb_c128 coeff;
+    int32_t num_factors;
+    const int32_t *qubits;
+    const char *labels;
+} vqb_pauli_term;
+
+/* Opaque device-resident state (PureState<double> state.hpp:175-256 or
+ * MixedState<double> state.hpp:259-349). */
+typedef struct vqb_state vqb_state;
+
+/* ---- errors / build info ---- */
+VQB_API const char *vqb_last_error(void);
+VQB_API const char *vqb_build_info(void);
+/* Number of native kernel launches issued by this process so far (evidence
+ * counter for benchmarks; incremented on every launch of our kernels). */
+VQB_API int64_t vqb_kernel_launch_count(void);
+
+/* ---- device state: replaces PureState / MixedState storage ---- */
+/* PureState(n) (state.hpp:182-185) when mixed == 0, MixedState(n)
+ * (state.hpp:264-268) when mixed != 0; initialised to |0...0> (<0...0|). */
+VQB_API int vqb_state_create(int32_t num_qubits, int32_t mixed, vqb_state **out);
+/* Non-owning handle over caller-owned device memory holding 2^num_qubits
+ * amplitudes (mixed: 4^num_qubits). `global_offset` is the flat index of the
+ * buffer's first amplitude inside a larger, sharded state (0 when
+ * unsharded); diagonal and controlled operations use it to resolve qubits
+ * that live above the buffer (global qubits). */
+VQB_API int vqb_state_wrap(void *device_ptr, int32_t num_qubits, int32_t mixed,
+                           uint64_t global_offset, int32_t global_qubits,
+                           vqb_state **out);
+VQB_API int vqb_state_destroy(vqb_state *st);
+VQB_API int vqb_state_info(const vqb_state *st, int32_t *num_qubits, int32_t *mixed,
+                           uint64_t *num_amplitudes);
+VQB_API int vqb_state_device_ptr(const vqb_state *st, void **ptr);
+VQB_API int vqb_state_set_zero(vqb_state *st); /* back to |0...0> */
+/* Host <-> device. `count` must equal the number of amplitudes. The host
+ * buffer may be pageable or pinned. */
+VQB_API int vqb_state_upload(vqb_state *st, const vqb_c128 *host, uint64_t count);
+VQB_API int vqb_state_download(const vqb_state *st, vqb_c128 *host, uint64_t count);
+VQB_API int vqb_state_copy(vqb_state *dst, const vqb_state *src);
+
+/* ---- gate / channel application: kernels.hpp, circuit.hpp ---- */
+/* apply_gate_fast (kernels.hpp:365-430) on a pure state; apply_gate_mixed
+ * (kernels.hpp:434-449) on a mixed state. */
+VQB_API int vqb_apply_gate(vqb_state *st, const vqb_op *gate);
+/* apply_channel (kernels.hpp:453-461); mixed states only. */
+VQB_API int vqb_apply_channel(vqb_state *st, const vqb_op *channel);
+/* apply_matrix (kernels.hpp:327-361): arbitrary (not necessarily unitary)
+ * m-qubit matrix on the given positions of the (pseudo) state. */
+VQB_API int vqb_apply_matrix(vqb_state *st, const int32_t *positions, int32_t m,
+                             const vqb_c128 *matrix);
+/* apply_circuit (circuit.hpp:110-129) over a flattened element list. Gates
+ * are scheduled into fused shared-memory tile passes; results match the
+ * reference within 1e-12 max-abs. */
+VQB_API int vqb_apply_circuit(vqb_state *st, const vqb_op *ops, int64_t count);
+/* Same, gate by gate (one kernel per element, the unfused path). */
+VQB_API int vqb_apply_circuit_unfused(vqb_state *st, const vqb_op *ops, int64_t count);
+
+/* ---- reductions: state.hpp, observables.hpp ---- */
+VQB_API int vqb_norm(const vqb_state *st, double *out);       /* state.hpp:236-242 */
+VQB_API int vqb_trace(const vqb_state *st, vqb_c128 *out);    /* state.hpp:329-336 */
+/* expectation (observables.hpp:176-213), pure or mixed. */
+VQB_API int vqb_expectation(const vqb_state *st, const vqb_pauli_term *terms,
+                            int64_t num_terms, vqb_c128 *out);
+/* apply_operator (observables.hpp:216-237): dst <- H src. dst must have the
+ * same shape as src. */
+VQB_API int vqb_apply_operator(const vqb_state *src, vqb_state *dst,
+                               const vqb_pauli_term *terms, int64_t num_terms);
+/* bilinear_gate_form (kernels.hpp:466-503): <bra| L |ket>. */
+VQB_API int vqb_bilinear_form(const vqb_state *bra, const vqb_state *ket,
+                              const int32_t *positions, int32_t m,
+                              const vqb_c128 *local, vqb_c128 *out);
+/* reverse_sweep_step (kernels.hpp:659-697): phi <- inv phi;
+ * out[p] = <psi| dmats[p] |phi>; psi <- inv psi. dmats holds np matrices
+ * back to back. */
+VQB_API int vqb_reverse_step(vqb_state *phi, vqb_state *psi, const int32_t *positions,
+                             int32_t m, const vqb_c128 *inv, const vqb_c128 *dmats,
+                             int32_t np, vqb_c128 *out);
+
+/* ---- losses and gradients: autodiff.hpp ---- */
+/* loss_pure (autodiff.hpp:80-89). s0 is not mutated. */
+VQB_API int vqb_loss_pure(const vqb_op *ops, int64_t count, const vqb_pauli_term *terms,
+                          int64_t num_terms, const vqb_state *s0, double *loss);
+/* gradient_pure (autodiff.hpp:95-156): Algorithm 2 with two working states.
+ * grads receives one value per active parameter in traversal order;
+ * *num_grads is set to that count (an error if it exceeds capacity).
+ * reverse_residual (nullable) = max |phi_end - s0| (autodiff.hpp:151-154). */
+VQB_API int vqb_gradient_pure(const vqb_op *ops, int64_t count,
+                              const vqb_pauli_term *terms, int64_t num_terms,
+                              const vqb_state *s0, double *loss, double *grads,
+                              int64_t capacity, int64_t *num_grads,
+                              double *reverse_residual);
+/* loss_mixed (autodiff.hpp:160-167). */
+VQB_API int vqb_loss_mixed(const vqb_op *ops, int64_t count, const vqb_pauli_term *terms,
+                           int64_t num_terms, const vqb_state *dm0, double *loss);
+/* gradient_mixed (autodiff.hpp:184-329): noisy reverse sweep on vec(rho);
+ * channels are inverted on the host (LU, condition limit 1e12,
+ * autodiff.hpp:51,263-276) and a non-invertible one returns
+ * VQB_ERR_NONINVERTIBLE. */
+VQB_API int vqb_gradient_mixed(const vqb_op *ops, int64_t count,
+                               const vqb_pauli_term *terms, int64_t num_terms,
+                               const vqb_state *dm0, double *loss, double *grads,
+                               int64_t capacity, int64_t *num_grads,
+                               double *reverse_residual);
+
+/* ---- host-side gate algebra (gates.hpp), exported for bindings ---- */
+/* Matrix of a gate descriptor: the caller's matrix if given, else built from
+ * kind/params (gates.hpp:188-259,309-373). out: 4^m entries. */
+VQB_API int vqb_gate_matrix(const vqb_op *gate, vqb_c128 *out);
+/* gate_derivative (gates.hpp:543-577). */
+VQB_API int vqb_gate_derivative(const vqb_op *gate, int32_t param_index, vqb_c128 *out);
+/* gate_inverse (gates.hpp:581-619): matrix of the inverse gate. */
+VQB_API int vqb_gate_inverse(const vqb_op *gate, vqb_c128 *out);
+/* channel_superoperator (gates.hpp:708-732). out: 16^m entries. */
+VQB_API int vqb_channel_superop(const vqb_op *channel, vqb_c128 *out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VQCS_B200_H */

@@ -1,0 +1,70 @@
+"""TEST INFRASTRUCTURE ONLY — the CPU checkers for the CUDA path.
+
+Two implementations of the include/vqcs_b200.h C-ABI on the CPU:
+
+* ``reference()`` — the unmodified reference library (header-only C++,
+  /root/reference/proj/include/vqcs) compiled by oracle/Makefile from the
+  reference sources into oracle/_ref/libvqcs_ref.so via ref_shim.cpp;
+* ``restatement()`` — the plain-C restatement oracle/vqcs_oracle.c
+  (oracle/_ref/libvqcs_oracle.so), pinned against the former and the golden
+  vectors in tests/golden/.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` legs may import this package, and only as the checker or
+the CPU baseline. The product (paper_2406_19212_b200) never imports it.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import os
+import subprocess
+
+from paper_2406_19212_b200.engine import Engine
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_SO = os.path.join(HERE, "_ref", "libvqcs_ref.so")
+ORC_SO = os.path.join(HERE, "_ref", "libvqcs_oracle.so")
+
+_cache: dict = {}
+
+
+def build(quiet: bool = True) -> None:
+    """Compile the checkers (reference shim only where /root/reference exists)."""
+    out = subprocess.run(["make", "-C", HERE, "all"], capture_output=True, text=True)
+    if out.returncode != 0:
+        raise RuntimeError("oracle build failed:\n" + out.stdout + out.stderr)
+    if not quiet:
+        print(out.stdout)
+
+
+def _load(path: str, prefix: str, name: str) -> Engine:
+    if name not in _cache:
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} not built; run `make -C oracle`")
+        lib = ct.CDLL(path)
+        _cache[name] = Engine(lib, prefix, name)
+    return _cache[name]
+
+
+def reference_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def reference() -> Engine:
+    """The reference vqcs library itself (multi-threaded per VQCS_NUM_THREADS
+    or set_num_threads)."""
+    return _load(REF_SO, "vqcsref_", "reference")
+
+
+def restatement() -> Engine:
+    return _load(ORC_SO, "vqcsorc_", "restatement")
+
+
+def checker() -> Engine:
+    """The strongest available checker: the reference itself if built, else
+    the restatement."""
+    return reference() if reference_available() else restatement()
+
+
+def set_reference_threads(t: int) -> None:
+    reference().lib.vqcsref_set_num_threads(int(t))

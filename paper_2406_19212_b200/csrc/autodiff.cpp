@@ -1,0 +1,209 @@
+// Losses and adjoint gradients on the device (autodiff.hpp:80-329).
+//
+// Algorithm 2 of the paper: forward to |Phi_M>, |Psi> = H|Phi_M>,
+// then per element in reverse pull both states back through the inverse and
+// accumulate <Psi| dU |Phi> for every active parameter. Only two full-size
+// working states are held. Gradient partials are reduced on the device and
+// written straight into a device gradient vector; the host reads it once at
+// the end (no per-gate synchronisation).
+#include "autodiff.hpp"
+
+#include "engine.hpp"
+
+namespace vqb {
+
+namespace {
+
+struct DevBuf {
+    void *p = nullptr;
+    explicit DevBuf(size_t bytes) { VQB_CUDA(cudaMalloc(&p, bytes)); }
+    ~DevBuf() { cudaFree(p); }
+    template <typename T> T *as() { return static_cast<T *>(p); }
+};
+
+struct StateGuard {
+    DeviceState *s;
+    ~StateGuard() { state_destroy(s); }
+};
+
+DeviceState *clone(const DeviceState *src) {
+    DeviceState *d = state_create(src->n, src->mixed);
+    VQB_CUDA(cudaStreamSynchronize(src->stream));
+    VQB_CUDA(cudaMemcpyAsync(d->amps, src->amps, sizeof(double2) * src->size,
+                             cudaMemcpyDeviceToDevice, d->stream));
+    return d;
+}
+
+void check_operator(const PauliPack &op, int n, const char *what) {
+    if (op.max_qubit > n)
+        raise(VQB_ERR_INDEX, std::string(what) + ": operator acts on qubit " +
+                                 std::to_string(op.max_qubit) + " but the state has " +
+                                 std::to_string(n) + " qubits");
+}
+
+void reject_channels(const vqb_op *ops, int64_t count, const char *what) {
+    for (int64_t i = 0; i < count; ++i)
+        if (ops[i].elem == VQB_ELEM_CHANNEL)
+            raise(VQB_ERR_TYPE, std::string(what) +
+                                    ": circuit contains quantum channels; use the mixed-state variant");
+}
+
+} // namespace
+
+double loss_pure(const vqb_op *ops, int64_t count, const vqb_pauli_term *terms, int64_t nterms,
+                 DeviceState *s0, bool fused) {
+    if (s0->mixed) raise(VQB_ERR_TYPE, "loss_pure: pure initial state required");
+    reject_channels(ops, count, "loss_pure");
+    const PauliPack op = pack_operator(terms, nterms, false);
+    const auto es = build_elements(ops, count);
+    std::vector<Gate> prog;
+    for (const auto &e : es) {
+        check_fit(e.gate.pos, e.gate.m, s0->n);
+        prog.push_back(e.gate);
+    }
+    check_operator(op, s0->n, "loss_pure");
+    DeviceState *s = clone(s0);
+    StateGuard g{s};
+    run_program(s, prog, fused);
+    return expectation(s, op).real();
+}
+
+double loss_mixed(const vqb_op *ops, int64_t count, const vqb_pauli_term *terms, int64_t nterms,
+                  DeviceState *dm0, bool fused) {
+    if (!dm0->mixed) raise(VQB_ERR_TYPE, "loss_mixed: mixed initial state required");
+    const PauliPack op = pack_operator(terms, nterms, false);
+    check_operator(op, dm0->n, "loss_mixed");
+    const auto es = build_elements(ops, count);
+    for (const auto &e : es) {
+        if (e.channel) check_fit(e.chan.pos, e.chan.m, dm0->n);
+        else check_fit(e.gate.pos, e.gate.m, dm0->n);
+    }
+    DeviceState *s = clone(dm0);
+    StateGuard g{s};
+    run_program(s, mixed_forward_program(es, dm0->n), fused);
+    return expectation(s, op).real();
+}
+
+GradientOut gradient_pure(const vqb_op *ops, int64_t count, const vqb_pauli_term *terms,
+                          int64_t nterms, DeviceState *s0, bool want_residual, bool fused) {
+    if (s0->mixed) raise(VQB_ERR_TYPE, "gradient_pure: pure initial state required");
+    reject_channels(ops, count, "gradient_pure");
+    const int n = s0->n;
+    const PauliPack op = pack_operator(terms, nterms, false);
+    check_operator(op, n, "gradient_pure");
+    const auto es = build_elements(ops, count);
+    std::vector<int64_t> base(count);
+    int64_t total = 0;
+    std::vector<Gate> fwd;
+    for (int64_t i = 0; i < count; ++i) {
+        base[i] = total;
+        total += es[i].gate.num_active();
+        check_fit(es[i].gate.pos, es[i].gate.m, n);
+        fwd.push_back(es[i].gate);
+    }
+
+    DeviceState *phi = clone(s0);
+    StateGuard gphi{phi};
+    run_program(phi, fwd, fused);
+
+    GradientOut out;
+    out.grads.assign(total, 0.0);
+    if (total == 0) {
+        out.loss = expectation(phi, op).real();
+        return out;
+    }
+    DeviceState *psi = state_create(n, 0);
+    StateGuard gpsi{psi};
+    VQB_CUDA(cudaStreamSynchronize(psi->stream));
+    apply_operator(phi, psi->amps, op, false);
+    const size_t gbytes = sizeof(double2) * ((total + 1) / 2); // keep dloss 16-B aligned
+    DevBuf dbuf(gbytes + sizeof(double2));
+    double *dgrads = dbuf.as<double>();
+    double2 *dloss = reinterpret_cast<double2 *>(dbuf.as<char>() + gbytes);
+    dot_async(phi, phi->amps, psi->amps, dloss); // loss = Re <phi|H phi>
+
+    run_reverse(phi, psi, pure_reverse_program(es, base), dgrads, fused);
+
+    double2 hl;
+    VQB_CUDA(cudaMemcpyAsync(out.grads.data(), dgrads, sizeof(double) * total,
+                             cudaMemcpyDeviceToHost, phi->stream));
+    VQB_CUDA(cudaMemcpyAsync(&hl, dloss, sizeof(double2), cudaMemcpyDeviceToHost, phi->stream));
+    VQB_CUDA(cudaStreamSynchronize(phi->stream));
+    out.loss = hl.x;
+    if (want_residual) out.residual = max_abs_diff(phi, phi->amps, s0->amps);
+    return out;
+}
+
+GradientOut gradient_mixed(const vqb_op *ops, int64_t count, const vqb_pauli_term *terms,
+                           int64_t nterms, DeviceState *dm0, bool want_residual, bool fused) {
+    if (!dm0->mixed) raise(VQB_ERR_TYPE, "gradient_mixed: mixed initial state required");
+    const int n = dm0->n;
+    const PauliPack op = pack_operator(terms, nterms, true); // op.conjugated() (autodiff.hpp:247)
+    check_operator(op, n, "gradient_mixed");
+    const auto es = build_elements(ops, count);
+    std::vector<int64_t> base(count);
+    int64_t total = 0;
+    for (int64_t i = 0; i < count; ++i) {
+        base[i] = total;
+        if (es[i].channel) {
+            check_fit(es[i].chan.pos, es[i].chan.m, n);
+        } else {
+            total += es[i].gate.num_active();
+            check_fit(es[i].gate.pos, es[i].gate.m, n);
+        }
+    }
+    // Channel inverses on the host first (LU, condition limit;
+    // autodiff.hpp:263-276), so a non-invertible channel fails before any
+    // device work.
+    std::vector<cvec> chan_inv(count), chan_adj(count);
+    if (total > 0) {
+        for (int64_t i = count; i-- > 0;) {
+            if (!es[i].channel) continue;
+            const Channel &ch = es[i].chan;
+            const cvec s = channel_superop(ch);
+            const int d = 1 << (2 * ch.m);
+            const Inverse lu = lu_inverse(s, d);
+            if (lu.singular || lu.condition > kChannelConditionLimit) {
+                static const char *names[] = {"Generic", "AmplitudeDamping", "PhaseDamping",
+                                              "Depolarizing"};
+                raise(VQB_ERR_NONINVERTIBLE,
+                      std::string("gradient_mixed: the superoperator of channel '") +
+                          names[ch.kind & 3] + "' on qubit " + std::to_string(ch.pos[0]) +
+                          " (element " + std::to_string(i + 1) +
+                          ") is singular or too ill-conditioned to invert");
+            }
+            chan_inv[i] = lu.inv;
+            chan_adj[i] = adjoint(s, d);
+        }
+    }
+
+    DeviceState *phi = clone(dm0);
+    StateGuard gphi{phi};
+    run_program(phi, mixed_forward_program(es, n), fused);
+
+    DeviceState *psi = state_create(n, 1);
+    StateGuard gpsi{psi};
+    identity_costate(psi, op); // <<Psi| = <<I| H (autodiff.hpp:241-248)
+    VQB_CUDA(cudaStreamSynchronize(psi->stream));
+
+    GradientOut out;
+    out.grads.assign(total, 0.0);
+    const size_t gbytes = sizeof(double2) * ((std::max<int64_t>(total, 1) + 1) / 2);
+    DevBuf dbuf(gbytes + sizeof(double2));
+    double *dgrads = dbuf.as<double>();
+    double2 *dloss = reinterpret_cast<double2 *>(dbuf.as<char>() + gbytes);
+    dot_async(phi, psi->amps, phi->amps, dloss); // loss = Re <<psi|phi>>
+    if (total > 0) {
+        run_reverse(phi, psi, mixed_reverse_program(es, n, base, chan_inv, chan_adj), dgrads, fused);
+        VQB_CUDA(cudaMemcpyAsync(out.grads.data(), dgrads, sizeof(double) * total,
+                                 cudaMemcpyDeviceToHost, phi->stream));
+    }
+    double2 hl;
+    VQB_CUDA(cudaMemcpyAsync(&hl, dloss, sizeof(double2), cudaMemcpyDeviceToHost, phi->stream));
+    VQB_CUDA(cudaStreamSynchronize(phi->stream));
+    out.loss = hl.x;
+    if (want_residual && total > 0) out.residual = max_abs_diff(phi, phi->amps, dm0->amps);
+    return out;
+}
+
+} // namespace vqb

@@ -1,0 +1,401 @@
+// extern "C" boundary (include/vqcs_b200.h). Every entry point catches all
+// exceptions and returns a vqb_status; messages go to a thread-local buffer.
+#include <cstring>
+#include <string>
+
+#include "autodiff.hpp"
+#include "engine.hpp"
+
+using namespace vqb;
+
+struct vqb_state : DeviceState {};
+
+namespace vqb {
+int64_t launch_count();
+}
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F> int guard(F &&f) {
+    try {
+        f();
+        return VQB_OK;
+    } catch (const vqb::Error &e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc &) {
+        g_err = "host allocation failed";
+        return VQB_ERR_SIZE;
+    } catch (const std::exception &e) {
+        g_err = e.what();
+        return VQB_ERR_INTERNAL;
+    }
+}
+
+DeviceState *ds(vqb_state *s) {
+    if (!s) raise(VQB_ERR_USAGE, "null state handle");
+    return static_cast<DeviceState *>(s);
+}
+DeviceState *ds(const vqb_state *s) { return ds(const_cast<vqb_state *>(s)); }
+
+void need(const void *p, const char *what) {
+    if (!p) raise(VQB_ERR_USAGE, std::string("null argument: ") + what);
+}
+
+void check_count(const DeviceState *s, uint64_t count, const char *what) {
+    if (count != s->size)
+        raise(VQB_ERR_SHAPE, std::string(what) + ": count " + std::to_string(count) +
+                                 " does not match the state's " + std::to_string(s->size) +
+                                 " amplitudes");
+}
+
+void write_grads(const GradientOut &r, double *loss, double *grads, int64_t cap, int64_t *ng,
+                 double *res) {
+    if ((int64_t)r.grads.size() > cap)
+        raise(VQB_ERR_SHAPE, "gradient buffer too small: need " + std::to_string(r.grads.size()));
+    *loss = r.loss;
+    if (!r.grads.empty()) std::memcpy(grads, r.grads.data(), sizeof(double) * r.grads.size());
+    *ng = (int64_t)r.grads.size();
+    if (res) *res = r.residual;
+}
+
+} // namespace
+
+extern "C" {
+
+VQB_API const char *vqb_last_error(void) { return g_err.c_str(); }
+
+VQB_API const char *vqb_build_info(void) {
+    return "libvqcs_b200: sm_100a complex128 state-vector/density-matrix core (CUDA "
+#ifdef __CUDACC_VER_MAJOR__
+        "nvcc"
+#endif
+        ")";
+}
+
+VQB_API int64_t vqb_kernel_launch_count(void) { return vqb::launch_count(); }
+
+VQB_API int vqb_state_create(int32_t n, int32_t mixed, vqb_state **out) {
+    return guard([&] {
+        need(out, "out");
+        *out = static_cast<vqb_state *>(state_create(n, mixed));
+    });
+}
+
+VQB_API int vqb_state_wrap(void *ptr, int32_t n, int32_t mixed, uint64_t goff, int32_t gq,
+                           vqb_state **out) {
+    return guard([&] {
+        need(ptr, "device_ptr");
+        need(out, "out");
+        *out = static_cast<vqb_state *>(state_wrap(ptr, n, mixed, goff, gq));
+    });
+}
+
+VQB_API int vqb_state_destroy(vqb_state *s) {
+    return guard([&] { state_destroy(static_cast<DeviceState *>(s)); });
+}
+
+VQB_API int vqb_state_info(const vqb_state *s, int32_t *n, int32_t *mixed, uint64_t *count) {
+    return guard([&] {
+        const DeviceState *d = ds(s);
+        if (n) *n = d->n;
+        if (mixed) *mixed = d->mixed;
+        if (count) *count = d->size;
+    });
+}
+
+VQB_API int vqb_state_device_ptr(const vqb_state *s, void **ptr) {
+    return guard([&] { *ptr = ds(s)->amps; });
+}
+
+VQB_API int vqb_state_set_zero(vqb_state *s) { return guard([&] { state_set_zero(ds(s)); }); }
+
+VQB_API int vqb_state_upload(vqb_state *s, const vqb_c128 *host, uint64_t count) {
+    return guard([&] {
+        DeviceState *d = ds(s);
+        need(host, "host");
+        check_count(d, count, "state_upload");
+        VQB_CUDA(cudaMemcpyAsync(d->amps, host, sizeof(double2) * count, cudaMemcpyHostToDevice,
+                                 d->stream));
+        sync(d);
+    });
+}
+
+VQB_API int vqb_state_download(const vqb_state *s, vqb_c128 *host, uint64_t count) {
+    return guard([&] {
+        DeviceState *d = ds(s);
+        need(host, "host");
+        check_count(d, count, "state_download");
+        VQB_CUDA(cudaMemcpyAsync(host, d->amps, sizeof(double2) * count, cudaMemcpyDeviceToHost,
+                                 d->stream));
+        sync(d);
+    });
+}
+
+VQB_API int vqb_state_copy(vqb_state *dst, const vqb_state *src) {
+    return guard([&] {
+        DeviceState *a = ds(dst), *b = ds(src);
+        if (a->size != b->size) raise(VQB_ERR_SHAPE, "state_copy: shape mismatch");
+        sync(b);
+        VQB_CUDA(cudaMemcpyAsync(a->amps, b->amps, sizeof(double2) * b->size,
+                                 cudaMemcpyDeviceToDevice, a->stream));
+        sync(a);
+    });
+}
+
+VQB_API int vqb_apply_gate(vqb_state *s, const vqb_op *op) {
+    return guard([&] {
+        DeviceState *d = ds(s);
+        need(op, "gate");
+        const Gate g = gate_from_op(*op);
+        check_fit(g.pos, g.m, d->n);
+        if (d->mixed) apply_gate_both_sides(d, g);
+        else apply_gate_fast(d->amps, d->pn, g, d->stream);
+        sync(d);
+    });
+}
+
+VQB_API int vqb_apply_channel(vqb_state *s, const vqb_op *op) {
+    return guard([&] {
+        DeviceState *d = ds(s);
+        need(op, "channel");
+        if (!d->mixed)
+            raise(VQB_ERR_TYPE, "apply_channel: a quantum channel cannot act on a pure state");
+        const Channel c = channel_from_op(*op);
+        check_fit(c.pos, c.m, d->n);
+        apply_superop(d, c);
+        sync(d);
+    });
+}
+
+VQB_API int vqb_apply_matrix(vqb_state *s, const int32_t *pos, int32_t m, const vqb_c128 *mat) {
+    return guard([&] {
+        DeviceState *d = ds(s);
+        need(pos, "positions");
+        need(mat, "matrix");
+        if (m < 1 || m > VQB_MAX_POSITIONS) raise(VQB_ERR_UNSUPPORTED, "apply_matrix: 1..6 positions");
+        check_fit(pos, m, d->pn);
+        const size_t dd = size_t(1) << (2 * m);
+        cvec M(dd);
+        for (size_t i = 0; i < dd; ++i) M[i] = cplx(mat[i].re, mat[i].im);
+        int bits[VQB_MAX_POSITIONS];
+        for (int k = 0; k < m; ++k) bits[k] = pos[k] - 1;
+        launch_dense(d->amps, d->pn, bits, m, M, d->stream);
+        sync(d);
+    });
+}
+
+static void apply_circuit_impl(vqb_state *s, const vqb_op *ops, int64_t count, bool fused) {
+    DeviceState *d = ds(s);
+    if (count > 0) need(ops, "ops");
+    const auto es = build_elements(ops, count);
+    for (const auto &e : es) {
+        if (e.channel) {
+            if (!d->mixed)
+                raise(VQB_ERR_TYPE,
+                      "apply_circuit: a quantum channel cannot act on a pure state; use a MixedState");
+            check_fit(e.chan.pos, e.chan.m, d->n);
+        } else {
+            check_fit(e.gate.pos, e.gate.m, d->n);
+        }
+    }
+    if (d->mixed) {
+        run_program(d, mixed_forward_program(es, d->n), fused);
+    } else {
+        std::vector<Gate> prog;
+        prog.reserve(es.size());
+        for (const auto &e : es) prog.push_back(e.gate);
+        run_program(d, prog, fused);
+    }
+    sync(d);
+}
+
+VQB_API int vqb_apply_circuit(vqb_state *s, const vqb_op *ops, int64_t count) {
+    return guard([&] { apply_circuit_impl(s, ops, count, true); });
+}
+
+VQB_API int vqb_apply_circuit_unfused(vqb_state *s, const vqb_op *ops, int64_t count) {
+    return guard([&] { apply_circuit_impl(s, ops, count, false); });
+}
+
+VQB_API int vqb_norm(const vqb_state *s, double *out) {
+    return guard([&] {
+        DeviceState *d = ds(s);
+        need(out, "out");
+        if (d->mixed) raise(VQB_ERR_TYPE, "norm: pure states only (use trace)");
+        *out = std::sqrt(norm_sq(d));
+    });
+}
+
+VQB_API int vqb_trace(const vqb_state *s, vqb_c128 *out) {
+    return guard([&] {
+        DeviceState *d = ds(s);
+        need(out, "out");
+        if (!d->mixed) raise(VQB_ERR_TYPE, "trace: mixed states only");
+        const cplx t = trace(d);
+        out->re = t.real();
+        out->im = t.imag();
+    });
+}
+
+VQB_API int vqb_expectation(const vqb_state *s, const vqb_pauli_term *terms, int64_t nt,
+                            vqb_c128 *out) {
+    return guard([&] {
+        DeviceState *d = ds(s);
+        need(out, "out");
+        const PauliPack p = pack_operator(terms, nt, false);
+        if (p.max_qubit > d->n)
+            raise(VQB_ERR_INDEX, "expectation: operator acts on qubit " + std::to_string(p.max_qubit) +
+                                     " but the state has " + std::to_string(d->n) + " qubits");
+        const cplx e = expectation(d, p);
+        out->re = e.real();
+        out->im = e.imag();
+    });
+}
+
+VQB_API int vqb_apply_operator(const vqb_state *src, vqb_state *dst, const vqb_pauli_term *terms,
+                               int64_t nt) {
+    return guard([&] {
+        DeviceState *a = ds(src), *b = ds(dst);
+        if (a->mixed || b->mixed) raise(VQB_ERR_TYPE, "apply_operator: pure states only");
+        if (a->size != b->size) raise(VQB_ERR_SHAPE, "apply_operator: shape mismatch");
+        if (a == b) raise(VQB_ERR_USAGE, "apply_operator: src and dst must differ");
+        const PauliPack p = pack_operator(terms, nt, false);
+        if (p.max_qubit > a->n)
+            raise(VQB_ERR_INDEX, "apply_operator: operator acts on qubit " +
+                                     std::to_string(p.max_qubit) + " but the state has " +
+                                     std::to_string(a->n) + " qubits");
+        sync(b);
+        if (p.groups.empty()) {
+            VQB_CUDA(cudaMemsetAsync(b->amps, 0, sizeof(double2) * b->size, a->stream));
+        } else {
+            apply_operator(a, b->amps, p, false);
+        }
+        sync(a);
+    });
+}
+
+VQB_API int vqb_bilinear_form(const vqb_state *bra, const vqb_state *ket, const int32_t *pos,
+                              int32_t m, const vqb_c128 *local, vqb_c128 *out) {
+    return guard([&] {
+        DeviceState *a = ds(bra), *b = ds(ket);
+        need(pos, "positions");
+        need(local, "local");
+        need(out, "out");
+        if (a->size != b->size) raise(VQB_ERR_SHAPE, "bilinear_form: shape mismatch");
+        check_fit(pos, m, b->pn);
+        const size_t dd = size_t(1) << (2 * m);
+        cvec L(dd);
+        for (size_t i = 0; i < dd; ++i) L[i] = cplx(local[i].re, local[i].im);
+        const cplx r = bilinear_form(a, b, pos, m, L);
+        out->re = r.real();
+        out->im = r.imag();
+    });
+}
+
+VQB_API int vqb_reverse_step(vqb_state *phi, vqb_state *psi, const int32_t *pos, int32_t m,
+                             const vqb_c128 *inv, const vqb_c128 *dmats, int32_t np, vqb_c128 *out) {
+    return guard([&] {
+        DeviceState *a = ds(phi), *b = ds(psi);
+        need(pos, "positions");
+        need(inv, "inv");
+        if (np > 0) {
+            need(dmats, "dmats");
+            need(out, "out");
+        }
+        if (a->size != b->size) raise(VQB_ERR_SHAPE, "reverse_step: shape mismatch");
+        check_fit(pos, m, a->pn);
+        const size_t dd = size_t(1) << (2 * m);
+        cvec I(dd);
+        for (size_t i = 0; i < dd; ++i) I[i] = cplx(inv[i].re, inv[i].im);
+        sync(b);
+        if (np == 0) {
+            Gate g;
+            g.m = m;
+            for (int k = 0; k < m; ++k) g.pos[k] = pos[k];
+            g.mat = I;
+            apply_gate_fast(a->amps, a->pn, g, a->stream);
+            apply_gate_fast(b->amps, b->pn, g, a->stream);
+            sync(a);
+            return;
+        }
+        std::vector<cvec> D(np, cvec(dd));
+        for (int p = 0; p < np; ++p)
+            for (size_t i = 0; i < dd; ++i) D[p][i] = cplx(dmats[p * dd + i].re, dmats[p * dd + i].im);
+        reverse_step_async(a->amps, b->amps, a->pn, pos, m, I, D, a, a->ws.result, nullptr, 0.0);
+        VQB_CUDA(cudaMemcpyAsync(a->ws.host_result, a->ws.result, sizeof(double2) * np,
+                                 cudaMemcpyDeviceToHost, a->stream));
+        sync(a);
+        for (int p = 0; p < np; ++p) {
+            out[p].re = a->ws.host_result[p].x;
+            out[p].im = a->ws.host_result[p].y;
+        }
+    });
+}
+
+VQB_API int vqb_loss_pure(const vqb_op *ops, int64_t count, const vqb_pauli_term *terms, int64_t nt,
+                          const vqb_state *s0, double *loss) {
+    return guard([&] {
+        need(loss, "loss");
+        *loss = loss_pure(ops, count, terms, nt, ds(s0), true);
+    });
+}
+
+VQB_API int vqb_loss_mixed(const vqb_op *ops, int64_t count, const vqb_pauli_term *terms,
+                           int64_t nt, const vqb_state *dm0, double *loss) {
+    return guard([&] {
+        need(loss, "loss");
+        *loss = loss_mixed(ops, count, terms, nt, ds(dm0), true);
+    });
+}
+
+VQB_API int vqb_gradient_pure(const vqb_op *ops, int64_t count, const vqb_pauli_term *terms,
+                              int64_t nt, const vqb_state *s0, double *loss, double *grads,
+                              int64_t cap, int64_t *ng, double *res) {
+    return guard([&] {
+        need(loss, "loss");
+        need(ng, "num_grads");
+        const auto r = gradient_pure(ops, count, terms, nt, ds(s0), res != nullptr, true);
+        if (!r.grads.empty()) need(grads, "grads");
+        write_grads(r, loss, grads, cap, ng, res);
+    });
+}
+
+VQB_API int vqb_gradient_mixed(const vqb_op *ops, int64_t count, const vqb_pauli_term *terms,
+                               int64_t nt, const vqb_state *dm0, double *loss, double *grads,
+                               int64_t cap, int64_t *ng, double *res) {
+    return guard([&] {
+        need(loss, "loss");
+        need(ng, "num_grads");
+        const auto r = gradient_mixed(ops, count, terms, nt, ds(dm0), res != nullptr, true);
+        if (!r.grads.empty()) need(grads, "grads");
+        write_grads(r, loss, grads, cap, ng, res);
+    });
+}
+
+static void to_c128(const cvec &v, vqb_c128 *out) {
+    for (size_t i = 0; i < v.size(); ++i) {
+        out[i].re = v[i].real();
+        out[i].im = v[i].imag();
+    }
+}
+
+VQB_API int vqb_gate_matrix(const vqb_op *op, vqb_c128 *out) {
+    return guard([&] { to_c128(gate_from_op(*op).mat, out); });
+}
+
+VQB_API int vqb_gate_derivative(const vqb_op *op, int32_t p, vqb_c128 *out) {
+    return guard([&] { to_c128(gate_derivative(gate_from_op(*op), p), out); });
+}
+
+VQB_API int vqb_gate_inverse(const vqb_op *op, vqb_c128 *out) {
+    return guard([&] { to_c128(gate_inverse(gate_from_op(*op)).mat, out); });
+}
+
+VQB_API int vqb_channel_superop(const vqb_op *op, vqb_c128 *out) {
+    return guard([&] { to_c128(channel_superop(channel_from_op(*op)), out); });
+}
+
+} // extern "C"

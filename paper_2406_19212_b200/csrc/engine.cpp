@@ -1,0 +1,161 @@
+// Lowering of circuits to gate programs and the element-by-element executor.
+#include "engine.hpp"
+
+namespace vqb {
+
+std::vector<Element> build_elements(const vqb_op *ops, int64_t count) {
+    std::vector<Element> es(count);
+    for (int64_t i = 0; i < count; ++i) {
+        if (ops[i].elem == VQB_ELEM_CHANNEL) {
+            es[i].channel = true;
+            es[i].chan = channel_from_op(ops[i]);
+        } else {
+            es[i].gate = gate_from_op(ops[i]);
+        }
+    }
+    return es;
+}
+
+namespace {
+
+// The bra-side copy of a gate: conj(U) on positions + n, keeping the kind
+// only when conj(U) == U (kernels.hpp:441-448).
+Gate bra_side(const Gate &g, int n) {
+    Gate b = g;
+    for (int k = 0; k < g.m; ++k) b.pos[k] = g.pos[k] + n;
+    b.mat = conjugated(g.mat);
+    b.np = 0;
+    if (b.mat != g.mat) b.kind = VQB_GATE_GENERIC;
+    return b;
+}
+
+Gate dense_gate(const int *pos, int m, cvec mat) {
+    Gate g;
+    g.kind = VQB_GATE_GENERIC;
+    g.m = m;
+    for (int k = 0; k < m; ++k) g.pos[k] = pos[k];
+    g.mat = std::move(mat);
+    return g;
+}
+
+Gate superop_gate(const Channel &c, int n, cvec mat) {
+    int pos[6];
+    for (int k = 0; k < c.m; ++k) {
+        pos[k] = c.pos[k];
+        pos[k + c.m] = c.pos[k] + n;
+    }
+    return dense_gate(pos, 2 * c.m, std::move(mat));
+}
+
+} // namespace
+
+std::vector<Gate> mixed_forward_program(const std::vector<Element> &es, int n) {
+    std::vector<Gate> prog;
+    for (const auto &e : es) {
+        if (e.channel) {
+            prog.push_back(superop_gate(e.chan, n, channel_superop(e.chan)));
+        } else {
+            prog.push_back(e.gate);
+            prog.push_back(bra_side(e.gate, n));
+        }
+    }
+    return prog;
+}
+
+// gradient_pure reverse loop (autodiff.hpp:130-150)
+std::vector<RevOp> pure_reverse_program(const std::vector<Element> &es,
+                                        const std::vector<int64_t> &base) {
+    std::vector<RevOp> prog;
+    for (size_t i = es.size(); i-- > 0;) {
+        const Gate &g = es[i].gate;
+        RevOp r;
+        r.phi_op = gate_inverse(g);
+        r.psi_op = r.phi_op;
+        if (g.has_active()) {
+            for (int p = 0; p < g.np; ++p)
+                if (g.is_param[p]) r.dmats.push_back(gate_derivative(g, p));
+            r.grad_base = base[i];
+            r.scale = 2.0; // grads = 2 Re(acc) (autodiff.hpp:147-149)
+        }
+        prog.push_back(std::move(r));
+    }
+    return prog;
+}
+
+// gradient_mixed reverse loop (autodiff.hpp:263-323)
+std::vector<RevOp> mixed_reverse_program(const std::vector<Element> &es, int n,
+                                         const std::vector<int64_t> &base,
+                                         const std::vector<cvec> &chan_inv,
+                                         const std::vector<cvec> &chan_adj) {
+    std::vector<RevOp> prog;
+    for (size_t i = es.size(); i-- > 0;) {
+        if (es[i].channel) {
+            RevOp r;
+            r.phi_op = superop_gate(es[i].chan, n, chan_inv[i]); // S^-1 on phi
+            r.psi_op = superop_gate(es[i].chan, n, chan_adj[i]); // S^dag on psi
+            prog.push_back(std::move(r));
+            continue;
+        }
+        const Gate &g = es[i].gate;
+        const Gate inv = gate_inverse(g);
+        if (!g.has_active()) {
+            RevOp ket, bra;
+            ket.phi_op = ket.psi_op = inv;
+            bra.phi_op = bra.psi_op = bra_side(inv, n);
+            prog.push_back(std::move(ket));
+            prog.push_back(std::move(bra));
+            continue;
+        }
+        const int d = g.dim();
+        int pos[6];
+        for (int k = 0; k < g.m; ++k) {
+            pos[k] = g.pos[k];
+            pos[k + g.m] = g.pos[k] + n;
+        }
+        RevOp r;
+        // inv_local = kron(high = conj(U^-1) on bra, low = U^-1 on ket) (autodiff.hpp:297)
+        r.phi_op = dense_gate(pos, 2 * g.m, kron(conjugated(inv.mat), d, inv.mat, d));
+        r.psi_op = r.phi_op;
+        const cvec conj_u = conjugated(g.mat);
+        for (int p = 0; p < g.np; ++p) {
+            if (!g.is_param[p]) continue;
+            // dS = dU (x) conj(U) + U (x) conj(dU) (autodiff.hpp:303-311)
+            const cvec du = gate_derivative(g, p);
+            cvec ds = kron(conj_u, d, du, d);
+            const cvec second = kron(conjugated(du), d, g.mat, d);
+            for (size_t k = 0; k < ds.size(); ++k) ds[k] += second[k];
+            r.dmats.push_back(std::move(ds));
+        }
+        r.grad_base = base[i];
+        r.scale = 1.0; // grads = Re(acc) (autodiff.hpp:320-322)
+        prog.push_back(std::move(r));
+    }
+    return prog;
+}
+
+void run_program(DeviceState *s, const std::vector<Gate> &prog, bool fused) {
+    if (fused) {
+        run_program_fused(s, prog);
+        return;
+    }
+    for (const auto &g : prog) apply_gate_fast(s->amps, s->pn, g, s->stream);
+}
+
+void run_reverse(DeviceState *phi, DeviceState *psi, const std::vector<RevOp> &prog,
+                 double *dgrads, bool fused) {
+    if (fused) {
+        run_reverse_fused(phi, psi, prog, dgrads);
+        return;
+    }
+    for (const auto &r : prog) {
+        if (r.dmats.empty()) {
+            apply_gate_fast(phi->amps, phi->pn, r.phi_op, phi->stream);
+            apply_gate_fast(psi->amps, psi->pn, r.psi_op, phi->stream);
+        } else {
+            reverse_step_async(phi->amps, psi->amps, phi->pn, r.phi_op.pos, r.phi_op.m,
+                               r.phi_op.mat, r.dmats, phi, nullptr, dgrads + r.grad_base, r.scale);
+        }
+    }
+}
+
+} // namespace vqb

@@ -1,0 +1,228 @@
+"""Python binding over one implementation of the include/vqcs_b200.h C-ABI.
+
+`Engine(lib, prefix)` wraps a loaded library; the product binds
+``libvqcs_b200.so`` (prefix ``vqb_``), and the test-only ``oracle`` package
+binds the CPU checkers with the same class, so parity tests call both sides
+through identical Python code. Method names follow the reference API
+(apply_circuit, expectation, gradient_pure, ... in namespace vqcs).
+"""
+from __future__ import annotations
+
+import ctypes as ct
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import abi
+from .abi import Circuit, PauliOperator, c128, c128_p, pack_ops
+
+
+class State:
+    """A state handle: PureState<double> (mixed=False) or MixedState<double>."""
+
+    def __init__(self, engine: "Engine", handle: ct.c_void_p, n: int, mixed: bool):
+        self.engine = engine
+        self.handle = handle
+        self.n = n
+        self.mixed = mixed
+
+    @property
+    def num_qubits(self) -> int:
+        return self.n
+
+    @property
+    def size(self) -> int:
+        return 1 << (2 * self.n if self.mixed else self.n)
+
+    def amplitudes(self) -> np.ndarray:
+        return self.engine.download(self)
+
+    def free(self) -> None:
+        if self.handle:
+            self.engine._fn("state_destroy")(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class Engine:
+    def __init__(self, lib: ct.CDLL, prefix: str, name: str):
+        self.lib = lib
+        self.prefix = prefix
+        self.name = name
+        abi.bind_abi(lib, prefix)
+
+    # ---- plumbing ----
+    def _fn(self, name):
+        return getattr(self.lib, self.prefix + name)
+
+    def has(self, name: str) -> bool:
+        return hasattr(self.lib, self.prefix + name)
+
+    def check(self, rc: int) -> None:
+        if rc != 0:
+            msg = self._fn("last_error")()
+            msg = msg.decode() if msg else ""
+            raise abi.STATUS_TO_ERROR.get(rc, abi.InternalError)(f"[{self.name}] {msg}")
+
+    # ---- states ----
+    def create(self, n: int, mixed: bool = False) -> State:
+        h = ct.c_void_p()
+        self.check(self._fn("state_create")(n, 1 if mixed else 0, ct.byref(h)))
+        return State(self, h, n, mixed)
+
+    def pure_state(self, n: int) -> State:
+        return self.create(n, False)
+
+    def mixed_state(self, n: int) -> State:
+        return self.create(n, True)
+
+    def from_amplitudes(self, amps: np.ndarray, mixed: bool = False) -> State:
+        amps = np.ascontiguousarray(amps, dtype=np.complex128)
+        nb = int(amps.size).bit_length() - 1
+        n = nb // 2 if mixed else nb
+        s = self.create(n, mixed)
+        self.upload(s, amps)
+        return s
+
+    def upload(self, s: State, amps: np.ndarray) -> None:
+        amps = np.ascontiguousarray(amps, dtype=np.complex128)
+        self.check(self._fn("state_upload")(s.handle, amps.ctypes.data_as(c128_p),
+                                            ct.c_uint64(amps.size)))
+
+    def download(self, s: State, out: Optional[np.ndarray] = None) -> np.ndarray:
+        if out is None:
+            out = np.empty(s.size, dtype=np.complex128)
+        self.check(self._fn("state_download")(s.handle, out.ctypes.data_as(c128_p),
+                                              ct.c_uint64(out.size)))
+        return out
+
+    def copy(self, s: State) -> State:
+        d = self.create(s.n, s.mixed)
+        self.check(self._fn("state_copy")(d.handle, s.handle))
+        return d
+
+    # ---- application ----
+    def apply_gate(self, s: State, g) -> None:
+        p = pack_ops([g])
+        self.check(self._fn("apply_gate")(s.handle, p.arr))
+
+    def apply_gate_naive(self, s: State, g) -> None:
+        p = pack_ops([g])
+        self.check(self._fn("apply_gate_naive")(s.handle, p.arr))
+
+    def apply_channel(self, s: State, c) -> None:
+        p = pack_ops([c])
+        self.check(self._fn("apply_channel")(s.handle, p.arr))
+
+    def apply_matrix(self, s: State, positions: Sequence[int], matrix) -> None:
+        m = abi.as_c128_array(matrix)
+        pos = (ct.c_int32 * len(positions))(*positions)
+        self.check(self._fn("apply_matrix")(s.handle, pos, len(positions), abi.c128_ptr(m)))
+
+    def apply_circuit(self, c: Circuit, s: State, fused: bool = True) -> None:
+        p = c.pack() if isinstance(c, Circuit) else pack_ops(c)
+        name = "apply_circuit" if (fused or not self.has("apply_circuit_unfused")) \
+            else "apply_circuit_unfused"
+        self.check(self._fn(name)(s.handle, p.arr, p.count))
+
+    # ---- reductions ----
+    def norm(self, s: State) -> float:
+        v = ct.c_double()
+        self.check(self._fn("norm")(s.handle, ct.byref(v)))
+        return v.value
+
+    def trace(self, s: State) -> complex:
+        v = c128()
+        self.check(self._fn("trace")(s.handle, ct.byref(v)))
+        return complex(v.re, v.im)
+
+    def expectation(self, op: PauliOperator, s: State) -> complex:
+        arr, nt, _k = op.pack()
+        v = c128()
+        self.check(self._fn("expectation")(s.handle, arr, nt, ct.byref(v)))
+        return complex(v.re, v.im)
+
+    def apply_operator(self, op: PauliOperator, s: State) -> State:
+        arr, nt, _k = op.pack()
+        out = self.create(s.n, s.mixed)
+        self.check(self._fn("apply_operator")(s.handle, out.handle, arr, nt))
+        return out
+
+    def bilinear_form(self, bra: State, ket: State, positions, local) -> complex:
+        m = abi.as_c128_array(local)
+        pos = (ct.c_int32 * len(positions))(*positions)
+        v = c128()
+        self.check(self._fn("bilinear_form")(bra.handle, ket.handle, pos, len(positions),
+                                             abi.c128_ptr(m), ct.byref(v)))
+        return complex(v.re, v.im)
+
+    def reverse_step(self, phi: State, psi: State, positions, inv, dmats) -> list:
+        iv = abi.as_c128_array(inv)
+        dm = np.ascontiguousarray(np.concatenate([abi.as_c128_array(d) for d in dmats]))
+        pos = (ct.c_int32 * len(positions))(*positions)
+        out = (c128 * max(len(dmats), 1))()
+        self.check(self._fn("reverse_step")(phi.handle, psi.handle, pos, len(positions),
+                                            abi.c128_ptr(iv), abi.c128_ptr(dm), len(dmats),
+                                            out))
+        return [complex(out[i].re, out[i].im) for i in range(len(dmats))]
+
+    # ---- losses / gradients ----
+    def loss_pure(self, op: PauliOperator, c: Circuit, s0: State) -> float:
+        p = c.pack()
+        arr, nt, _k = op.pack()
+        v = ct.c_double()
+        self.check(self._fn("loss_pure")(p.arr, p.count, arr, nt, s0.handle, ct.byref(v)))
+        return v.value
+
+    def loss_mixed(self, op: PauliOperator, c: Circuit, dm0: State) -> float:
+        p = c.pack()
+        arr, nt, _k = op.pack()
+        v = ct.c_double()
+        self.check(self._fn("loss_mixed")(p.arr, p.count, arr, nt, dm0.handle, ct.byref(v)))
+        return v.value
+
+    def _gradient(self, fn, op, c, s0, with_residual):
+        p = c.pack()
+        arr, nt, _k = op.pack()
+        cap = max(c.num_active_params(), 1)
+        grads = np.zeros(cap, dtype=np.float64)
+        loss = ct.c_double()
+        ng = ct.c_int64()
+        res = ct.c_double()
+        self.check(self._fn(fn)(p.arr, p.count, arr, nt, s0.handle, ct.byref(loss),
+                                grads.ctypes.data_as(ct.POINTER(ct.c_double)), cap,
+                                ct.byref(ng), ct.byref(res) if with_residual else None))
+        g = grads[: ng.value].copy()
+        if with_residual:
+            return loss.value, g, res.value
+        return loss.value, g
+
+    def gradient_pure(self, op, c, s0, with_residual=False):
+        return self._gradient("gradient_pure", op, c, s0, with_residual)
+
+    def gradient_mixed(self, op, c, dm0, with_residual=False):
+        return self._gradient("gradient_mixed", op, c, dm0, with_residual)
+
+    # ---- gate algebra ----
+    def _mat_call(self, fn, op, dim, *extra):
+        out = np.zeros(dim * dim, dtype=np.complex128)
+        p = pack_ops([op])
+        self.check(self._fn(fn)(p.arr, *extra, out.ctypes.data_as(c128_p)))
+        return out
+
+    def gate_matrix(self, g) -> np.ndarray:
+        return self._mat_call("gate_matrix", g, 1 << len(g.positions))
+
+    def gate_derivative(self, g, p: int) -> np.ndarray:
+        return self._mat_call("gate_derivative", g, 1 << len(g.positions), p)
+
+    def gate_inverse(self, g) -> np.ndarray:
+        return self._mat_call("gate_inverse", g, 1 << len(g.positions))
+
+    def channel_superop(self, c) -> np.ndarray:
+        return self._mat_call("channel_superop", c, 1 << (2 * len(c.positions)))
