@@ -1,0 +1,438 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path against BASELINE.json's configurations.
+
+Default (N=1): config 1 — the 28-qubit random circuit (4x7 grid, 20 cycles,
+785 gates, complex128) — through ``vqb_apply_circuit``; metric gates/s.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                  [--config rqc28|hea20|qaoa30|noisy15] [--unfused]
+
+A step = reset the device state to |0...0> and run the whole circuit (or one
+full adjoint gradient evaluation for hea20/qaoa30/noisy15). `value` is timed
+with CUDA events on the state's stream over exactly K steps after W warm-up
+steps, max over ranks; `e2e` is the same metric through the C-ABI with the
+state round-tripping through pinned HOST memory every step (upload before,
+download after, inside the timed region). Under torchrun (N>1) each rank runs
+an independent replica (config 1 does not shard: "replicas", weak scaling).
+
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref/libvqcs_ref.so, compiled from /root/reference) on all host
+cores, each step a bounded prefix sample of the same workload; only rank 0
+runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from paper_2406_19212_b200 import circuits  # noqa: E402
+from paper_2406_19212_b200.abi import Circuit, GateOp  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "traffic.json")
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_PATH) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+# ------------------------------------------------------------------ workloads
+class Workload:
+    """metric unit per step and the per-step call."""
+
+    def __init__(self, name, args):
+        self.name = name
+        self.fused = not args.unfused
+        if name == "rqc28":
+            self.w = circuits.config1()
+            self.kind = "apply"
+        elif name == "hea20":
+            self.w = circuits.config0()
+            self.kind = "grad_pure"
+        elif name == "qaoa30":
+            self.w = circuits.config2()
+            self.kind = "grad_pure"
+        elif name == "noisy15":
+            self.w = circuits.config3()
+            self.kind = "grad_mixed"
+        else:
+            raise SystemExit(f"unknown config {name}")
+        self.n = self.w.num_qubits
+        self.mixed = self.w.mixed
+        self.gates = len(self.w.circuit)
+        if self.kind == "apply":
+            self.metric, self.unit = "gates/s", "gates/s"
+            self.units_per_step = self.gates
+        else:
+            self.metric, self.unit = "gradient evals/s", "evals/s"
+            self.units_per_step = 1
+
+    def step(self, eng, state):
+        if self.kind == "apply":
+            eng.apply_circuit(self.w.circuit, state, fused=self.fused)
+        elif self.kind == "grad_pure":
+            eng.gradient_pure(self.w.observable, self.w.circuit, state)
+        else:
+            eng.gradient_mixed(self.w.observable, self.w.circuit, state)
+
+    def algorithmic_bytes(self) -> float:
+        """SURVEY.md §8(d) touched-amplitude rule over the reference schedule."""
+        pn = 2 * self.n if self.mixed else self.n
+        unit = 32.0 * (1 << pn)
+        fwd = sum(circuits.touched_fraction(e) for e in self.w.circuit.elements)
+        if self.kind == "apply":
+            return fwd * unit
+        rev = 2 * fwd  # reverse steps touch two states
+        return (fwd + 1 + rev) * unit
+
+
+# ------------------------------------------------------------------ clocks sampler
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ distributed plumbing
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as td
+        torch.cuda.set_device(local)
+        backend = "nccl" if args.impl == "b200" else "gloo"
+        td.init_process_group(backend, init_method="env://")
+        dist = td
+    return world, rank, local, dist
+
+
+def barrier(dist, local):
+    if dist is not None:
+        import torch
+        if dist.get_backend() == "nccl":
+            dist.barrier(device_ids=[local])
+        else:
+            dist.barrier()
+
+
+def max_over_ranks(dist, v: float) -> float:
+    if dist is None:
+        return v
+    import torch
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ reference arm
+def reference_engine():
+    import oracle
+    if not oracle.reference_available():
+        return None, "oracle/_ref/libvqcs_ref.so not built"
+    eng = oracle.reference()
+    threads = os.cpu_count() or 1
+    oracle.set_reference_threads(threads)
+    return eng, threads
+
+
+def reference_sample(wl: Workload, full: bool = False):
+    """A bounded prefix of the workload for the CPU reference (10-30 s)."""
+    if wl.kind == "apply":
+        k = 160 if full else 80
+        return Circuit(wl.w.circuit.elements[:k]), k, f"first {k} of {wl.gates} gates at n={wl.n}"
+    if wl.name == "hea20":
+        return wl.w.circuit, 1, "one full gradient evaluation (20q, 600 params)"
+    # 30q QAOA / 15q noisy gradient: one layer-sized prefix at reduced size
+    return None, 0, "n/a"
+
+
+def run_reference_arm(args, wl, world, rank):
+    if rank != 0:
+        return 0
+    eng, threads = reference_engine()
+    line = {"impl": "reference", "metric": wl.metric, "unit": wl.unit, "higher_is_better": True,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "data": "synthetic",
+            "dtype": "c128", "scaling": "weak", "vs_baseline": None,
+            "config": {"workload": wl.w.name, "qubits": wl.n}}
+    if eng is None:
+        line["unavailable"] = threads
+        print(json.dumps(line))
+        return 0
+    circ, units, sample = reference_sample(wl)
+    if circ is None:
+        line["unavailable"] = f"no bounded reference sample defined for {wl.name}"
+        print(json.dumps(line))
+        return 0
+    st = eng.create(wl.n, wl.mixed)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        if wl.kind == "apply":
+            eng.apply_circuit(circ, st)
+        else:
+            eng.gradient_pure(wl.w.observable, circ, st)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    total = sum(times)
+    value = units * len(times) / total
+    line.update({"value": value, "ms_per_step": 1e3 * total / len(times),
+                 "cpu_baseline": {"value": value, "unit": wl.unit, "cores": threads,
+                                  "kind": "reference", "sample": sample},
+                 "e2e": {"value": value, "unit": wl.unit, "h2d_bytes_per_step": 0,
+                         "d2h_bytes_per_step": 0}})
+    print(json.dumps(line))
+    return 0
+
+
+def cpu_baseline(wl: Workload):
+    eng, threads = reference_engine()
+    if eng is None:
+        return None
+    circ, units, sample = reference_sample(wl, full=True)
+    if circ is None:
+        return None
+    st = eng.create(wl.n, wl.mixed)
+    t0 = time.perf_counter()
+    if wl.kind == "apply":
+        eng.apply_circuit(circ, st)
+    else:
+        eng.gradient_pure(wl.w.observable, circ, st)
+    dt = time.perf_counter() - t0
+    st.free()
+    return {"value": units / dt, "unit": wl.unit, "cores": threads, "kind": "reference",
+            "sample": sample + f"; {dt:.2f} s on the GPU box host"}
+
+
+# ------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="rqc28", choices=["rqc28", "hea20", "qaoa30", "noisy15"])
+    ap.add_argument("--unfused", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world, rank, local, dist = dist_setup(args)
+    wl = Workload(args.config, args)
+    if args.impl == "reference":
+        return run_reference_arm(args, wl, world, rank)
+
+    import torch
+    import paper_2406_19212_b200 as vqb
+    torch.cuda.set_device(local)
+    eng = vqb.device()
+    state = eng.create(wl.n, wl.mixed)
+    stream = torch.cuda.ExternalStream(eng.stream_of(state), device=torch.device("cuda", local))
+
+    def reset():
+        eng.check(eng._fn("state_set_zero")(state.handle))
+
+    # warm-up
+    for _ in range(args.warmup):
+        reset()
+        wl.step(eng, state)
+    torch.cuda.synchronize()
+
+    # timed region
+    barrier(dist, local)
+    torch.cuda.synchronize()
+    l0 = eng.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            reset()
+            wl.step(eng, state)
+        ev1.record(stream)
+        ev1.synchronize()
+    torch.cuda.synchronize()
+    barrier(dist, local)
+    launches = eng.launch_count() - l0
+    ms = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(dist, ms)
+    ms_per_step = ms / args.steps
+    value = world * wl.units_per_step * args.steps / (ms / 1e3)
+
+    # sanity of the result
+    check = {}
+    if wl.kind == "apply" and not wl.mixed:
+        check["norm"] = eng.norm(state)
+
+    # roofline: per-kernel CUDA-event timing of one more step (untimed)
+    reset()
+    eng.profile_begin()
+    wl.step(eng, state)
+    prof = eng.profile_end()
+    peak, peak_kind = hbm_peak()
+    roof = None
+    if prof:
+        top = max(prof.items(), key=lambda kv: kv[1][1])
+        name, (cnt, tot_ms) = top
+        pn = 2 * wl.n if wl.mixed else wl.n
+        bytes_per_launch = 32.0 * (1 << pn)  # one read + one write pass of the state
+        avg_s = tot_ms / cnt / 1e3
+        achieved = bytes_per_launch / avg_s / 1e9
+        traffic = None
+        try:
+            with open(TRAFFIC_PATH) as f:
+                traffic = json.load(f).get(wl.name, {}).get(name)
+        except Exception:
+            pass
+        step_ms = sum(v[1] for v in prof.values())
+        roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                "peak_source": peak_kind, "launches_per_step": cnt,
+                "avg_launch_us": 1e6 * avg_s, "share_of_step": tot_ms / step_ms if step_ms else None,
+                "algorithmic_bytes_per_launch": bytes_per_launch}
+    algo_gbs = wl.algorithmic_bytes() / (ms_per_step / 1e3) / 1e9
+
+    # end to end through the C-ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        nbytes = 16 * state.size
+        h_in = torch.zeros(2 * state.size, dtype=torch.float64, pin_memory=True)
+        h_in[0] = 1.0
+        h_out = torch.empty(2 * state.size, dtype=torch.float64, pin_memory=True)
+        import ctypes as ct
+        from paper_2406_19212_b200.abi import c128_p
+        pin = ct.cast(ct.c_void_p(h_in.data_ptr()), c128_p)
+        pout = ct.cast(ct.c_void_p(h_out.data_ptr()), c128_p)
+        up = eng._fn("state_upload")
+        down = eng._fn("state_download")
+
+        def e2e_step():
+            eng.check(up(state.handle, pin, ct.c_uint64(state.size)))
+            wl.step(eng, state)
+            eng.check(down(state.handle, pout, ct.c_uint64(state.size)))
+            return float(h_out[0])
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier(dist, local)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        e1.synchronize()
+        ems = max_over_ranks(dist, e0.elapsed_time(e1))
+        e2e = {"value": world * wl.units_per_step * args.steps / (ems / 1e3), "unit": wl.unit,
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+               "ms_per_step": ems / args.steps,
+               "path": "vqb_state_upload -> " + ("vqb_apply_circuit" if wl.kind == "apply"
+                                                   else "vqb_gradient_*") + " -> vqb_state_download"}
+        del h_in, h_out
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        state.free()
+        cpu = cpu_baseline(wl)
+
+    if rank == 0:
+        line = {
+            "metric": wl.metric, "value": value, "unit": wl.unit, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic (seeded SplitMix64 circuit, |0...0> start)",
+            "config": {"workload": wl.w.name, "qubits": wl.n, "mixed": wl.mixed,
+                       "elements": wl.gates, "seed": wl.w.seed, "fused": wl.fused,
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": (f"state {16 * (1 << (2 * wl.n if wl.mixed else wl.n)) / 2**30:.2f} GiB"
+                              " vs 126 MB L2: "
+                              + ("inputs larger than L2, no flush" if wl.n + (wl.n if wl.mixed else 0) >= 24
+                                 else "state L2-resident (reported as is)"))},
+            "roofline": roof,
+            "hbm_gbs_algorithmic": algo_gbs,
+            "hbm_frac_algorithmic": algo_gbs / peak,
+            "gpu_launches": launches,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "check": check,
+        }
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -131,6 +131,12 @@ VQB_API const char *vqb_build_info(void);
 /* Number of native kernel launches issued by this process so far (evidence
  * counter for benchmarks; incremented on every launch of our kernels). */
 VQB_API int64_t vqb_kernel_launch_count(void);
+/* Per-launch CUDA-event timing window for benchmarks (no reference analogue;
+ * the reference only wall-clocks whole calls, src/bench.cpp:76-87).
+ * vqb_profile_end synchronises the device and writes one line per kernel
+ * name: "<name> <launches> <total_ms>\n" (truncated to `cap` bytes). */
+VQB_API int vqb_profile_begin(void);
+VQB_API int vqb_profile_end(char *buf, int64_t cap);
 
 /* ---- device state: replaces PureState / MixedState storage ---- */
 /* PureState(n) (state.hpp:182-185) when mixed == 0, MixedState(n)
@@ -148,6 +154,8 @@ VQB_API int vqb_state_destroy(vqb_state *st);
 VQB_API int vqb_state_info(const vqb_state *st, int32_t *num_qubits, int32_t *mixed,
                            uint64_t *num_amplitudes);
 VQB_API int vqb_state_device_ptr(const vqb_state *st, void **ptr);
+/* The cudaStream_t all work on this state is issued to (for event timing). */
+VQB_API int vqb_state_stream(const vqb_state *st, void **stream);
 VQB_API int vqb_state_set_zero(vqb_state *st); /* back to |0...0> */
 /* Host <-> device. `count` must equal the number of amplitudes. The host
  * buffer may be pageable or pinned. */

@@ -12,6 +12,8 @@ struct vqb_state : DeviceState {};
 
 namespace vqb {
 int64_t launch_count();
+void prof_start();
+std::string prof_stop();
 }
 
 namespace {
@@ -76,6 +78,28 @@ VQB_API const char *vqb_build_info(void) {
 }
 
 VQB_API int64_t vqb_kernel_launch_count(void) { return vqb::launch_count(); }
+
+VQB_API int vqb_profile_begin(void) {
+    return guard([&] { prof_start(); });
+}
+
+VQB_API int vqb_profile_end(char *buf, int64_t cap) {
+    return guard([&] {
+        const std::string r = prof_stop();
+        if (buf && cap > 0) {
+            const size_t n = std::min<size_t>(r.size(), size_t(cap - 1));
+            std::memcpy(buf, r.data(), n);
+            buf[n] = 0;
+        }
+    });
+}
+
+VQB_API int vqb_state_stream(const vqb_state *s, void **stream) {
+    return guard([&] {
+        need(stream, "stream");
+        *stream = ds(s)->stream;
+    });
+}
 
 VQB_API int vqb_state_create(int32_t n, int32_t mixed, vqb_state **out) {
     return guard([&] {

@@ -34,9 +34,18 @@ struct Error : std::runtime_error {
 
 // Launch accounting (vqb_kernel_launch_count).
 void note_launch(int64_t n = 1);
-// Check the last launch and count it.
-void check_launch(const char *what);
 
 inline int popcount64(uint64_t x) { return __builtin_popcountll(x); }
 
+} // namespace vqb
+
+namespace vqb {
+// Optional per-launch CUDA-event profiling (vqb_profile_begin/end): a mark is
+// taken before a launch and closed by check_launch after it.
+struct ProfMark {
+    int slot = -1;
+    cudaStream_t st = nullptr;
+};
+ProfMark prof_begin(cudaStream_t st);
+void check_launch(const char *what, const ProfMark &m);
 } // namespace vqb

@@ -63,14 +63,6 @@ inline unsigned grid_for(uint64_t work, int threads = kThreads, unsigned cap = 1
 }
 
 // ------------------------------------------------------------------ launch accounting
-static std::atomic<int64_t> g_launches{0};
-void note_launch(int64_t n) { g_launches += n; }
-void check_launch(const char *what) {
-    note_launch(1);
-    const cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) raise(VQB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
-}
-int64_t launch_count() { return g_launches.load(); }
 
 // ------------------------------------------------------------------ dense m-qubit
 template <int M> struct DenseArgs {
@@ -142,8 +134,9 @@ static void launch_dense_m(double2 *a, int pn, const int *bits, const cvec &mat,
     }
     for (int i = 0; i < (1 << (2 * M)); ++i) A.mat[i] = make_double2(mat[i].real(), mat[i].imag());
     const uint64_t groups = 1ull << (pn - M);
+    const ProfMark pf_ = prof_begin(st);
     k_dense<M><<<grid_for(groups), kThreads, 0, st>>>(a, groups, A);
-    check_launch("k_dense");
+    check_launch("k_dense", pf_);
 }
 
 template <int M>
@@ -162,8 +155,9 @@ static void launch_dense_big(double2 *a, int pn, const int *bits, const cvec &ma
     VQB_CUDA(cudaMallocAsync((void **)&dm, bytes, st));
     VQB_CUDA(cudaMemcpyAsync(dm, mat.data(), bytes, cudaMemcpyHostToDevice, st));
     const uint64_t groups = 1ull << (pn - M);
+    const ProfMark pf_ = prof_begin(st);
     k_dense_big<M><<<grid_for(groups, 128), 128, 0, st>>>(a, groups, dm, A);
-    check_launch("k_dense_big");
+    check_launch("k_dense_big", pf_);
     VQB_CUDA(cudaFreeAsync(dm, st));
     VQB_CUDA(cudaStreamSynchronize(st)); // mat (host) must outlive the async copy
 }
@@ -223,11 +217,13 @@ static void launch_sparse(bool swap, double2 *a, int pn, const Gate &g, uint64_t
     A.phase = make_double2(phase.real(), phase.imag());
     const uint64_t groups = 1ull << (pn - g.m);
     if (swap) {
+        const ProfMark pf_ = prof_begin(st);
         k_swap<<<grid_for(groups), kThreads, 0, st>>>(a, groups, A);
-        check_launch("k_swap");
+        check_launch("k_swap", pf_);
     } else {
+        const ProfMark pf_ = prof_begin(st);
         k_phase<<<grid_for(groups), kThreads, 0, st>>>(a, groups, A);
-        check_launch("k_phase");
+        check_launch("k_phase", pf_);
     }
 }
 
@@ -418,26 +414,29 @@ static cplx fetch_result(DeviceState *s, int slot = 0) {
 
 double norm_sq(DeviceState *s) {
     const unsigned g = reduce_grid(s->size);
+    const ProfMark pf_ = prof_begin(s->stream);
     k_norm_sq<<<g, kThreads, 0, s->stream>>>(s->amps, s->size, s->ws.partials, s->ws.counter,
                                              ep_result(s));
-    check_launch("k_norm_sq");
+    check_launch("k_norm_sq", pf_);
     return fetch_result(s).real();
 }
 
 cplx trace(DeviceState *s) {
     const uint64_t dim = 1ull << s->n;
     const unsigned g = reduce_grid(dim);
+    const ProfMark pf_ = prof_begin(s->stream);
     k_trace<<<g, kThreads, 0, s->stream>>>(s->amps, dim, s->ws.partials, s->ws.counter,
                                            ep_result(s));
-    check_launch("k_trace");
+    check_launch("k_trace", pf_);
     return fetch_result(s);
 }
 
 void dot_async(DeviceState *s, const double2 *a, const double2 *b, double2 *out_dev) {
     const unsigned g = reduce_grid(s->size);
+    const ProfMark pf_ = prof_begin(s->stream);
     k_dot<<<g, kThreads, 0, s->stream>>>(a, b, s->size, s->ws.partials, s->ws.counter,
                                          Epilogue{out_dev, nullptr, 0.0});
-    check_launch("k_dot");
+    check_launch("k_dot", pf_);
 }
 
 cplx dot_async_result(DeviceState *s, const double2 *a, const double2 *b) {
@@ -448,8 +447,9 @@ cplx dot_async_result(DeviceState *s, const double2 *a, const double2 *b) {
 double max_abs_diff(DeviceState *s, const double2 *a, const double2 *b) {
     double *d = reinterpret_cast<double *>(s->ws.result);
     VQB_CUDA(cudaMemsetAsync(d, 0, sizeof(double), s->stream));
+    const ProfMark pf_ = prof_begin(s->stream);
     k_max_abs_diff<<<grid_for(s->size), kThreads, 0, s->stream>>>(a, b, s->size, d);
-    check_launch("k_max_abs_diff");
+    check_launch("k_max_abs_diff", pf_);
     VQB_CUDA(cudaMemcpyAsync(s->ws.host_result, d, sizeof(double), cudaMemcpyDeviceToHost,
                              s->stream));
     VQB_CUDA(cudaStreamSynchronize(s->stream));
@@ -590,13 +590,16 @@ void expectation_async(DeviceState *s, const PauliPack &p, double2 *out_dev) {
     }
     if (s->mixed) {
         const uint64_t dim = 1ull << s->n;
+        const ProfMark pf_ = prof_begin(s->stream);
         k_expect_mixed<<<reduce_grid(dim), kThreads, 0, s->stream>>>(s->amps, dim, groups, ng, terms,
                                                                      s->ws.partials, s->ws.counter, ep);
+        check_launch("k_expect_mixed", pf_);
     } else {
+        const ProfMark pf_ = prof_begin(s->stream);
         k_expect_pure<<<reduce_grid(s->size), kThreads, 0, s->stream>>>(
             s->amps, s->size, groups, ng, terms, s->ws.partials, s->ws.counter, ep);
+        check_launch("k_expect_pure", pf_);
     }
-    check_launch("k_expect");
 }
 
 cplx expectation(DeviceState *s, const PauliPack &p) {
@@ -627,9 +630,10 @@ void apply_operator(DeviceState *src, double2 *dst, const PauliPack &p, bool) {
     auto *groups = reinterpret_cast<const PauliGroupDev *>(src->ws.terms);
     auto *terms = reinterpret_cast<const PauliTermDev *>(
         reinterpret_cast<const char *>(src->ws.terms) + sizeof(PauliGroupDev) * p.groups.size());
+    const ProfMark pf_ = prof_begin(src->stream);
     k_apply_operator<<<grid_for(src->size), kThreads, 0, src->stream>>>(
         src->amps, dst, src->size, groups, (int)p.groups.size(), terms);
-    check_launch("k_apply_operator");
+    check_launch("k_apply_operator", pf_);
 }
 
 // <<I| H as a ket on vec(rho) (autodiff.hpp:241-248): entry (c^x) + c*dim gets
@@ -653,9 +657,10 @@ void identity_costate(DeviceState *s, const PauliPack &p) {
         reinterpret_cast<const char *>(s->ws.terms) + sizeof(PauliGroupDev) * p.groups.size());
     VQB_CUDA(cudaMemsetAsync(s->amps, 0, sizeof(double2) * s->size, s->stream));
     const uint64_t dim = 1ull << s->n;
+    const ProfMark pf_ = prof_begin(s->stream);
     k_identity_costate<<<grid_for(dim), kThreads, 0, s->stream>>>(s->amps, dim, groups,
                                                                   (int)p.groups.size(), terms);
-    check_launch("k_identity_costate");
+    check_launch("k_identity_costate", pf_);
 }
 
 // ------------------------------------------------------------------ bilinear form / reverse step
@@ -766,9 +771,10 @@ template <int M>
 static cplx bilinear_m(DeviceState *bra, DeviceState *ket, const int *pos1, const cvec &local) {
     const auto A = make_step_args<M>(pos1, {}, {local});
     const uint64_t groups = 1ull << (ket->pn - M);
+    const ProfMark pf_ = prof_begin(ket->stream);
     k_bilinear<M><<<reduce_grid(groups), kThreads, 0, ket->stream>>>(
         bra->amps, ket->amps, groups, A, ket->ws.partials, ket->ws.counter, ep_result(ket));
-    check_launch("k_bilinear");
+    check_launch("k_bilinear", pf_);
     return fetch_result(ket);
 }
 
@@ -789,9 +795,10 @@ static void reverse_m(double2 *phi, double2 *psi, int pn, const int *pos1, const
                       double scale) {
     const auto A = make_step_args<M>(pos1, inv, dm);
     const uint64_t groups = 1ull << (pn - M);
+    const ProfMark pf_ = prof_begin(w->stream);
     k_reverse_step<M><<<reduce_grid(groups), kThreads, 0, w->stream>>>(
         phi, psi, groups, A, w->ws.partials, w->ws.counter, Epilogue{out_c, out_r, scale});
-    check_launch("k_reverse_step");
+    check_launch("k_reverse_step", pf_);
 }
 
 void reverse_step_async(double2 *phi, double2 *psi, int pn, const int *pos1, int m, const cvec &inv,

@@ -69,6 +69,28 @@ class Engine:
             msg = msg.decode() if msg else ""
             raise abi.STATUS_TO_ERROR.get(rc, abi.InternalError)(f"[{self.name}] {msg}")
 
+    # ---- instrumentation (product library only) ----
+    def launch_count(self) -> int:
+        return int(self._fn("kernel_launch_count")())
+
+    def profile_begin(self) -> None:
+        self.check(self._fn("profile_begin")())
+
+    def profile_end(self) -> dict:
+        """-> {kernel name: (launches, total_ms)} for the window."""
+        buf = ct.create_string_buffer(1 << 16)
+        self.check(self._fn("profile_end")(buf, len(buf)))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, cnt, ms = line.split()
+            out[name] = (int(cnt), float(ms))
+        return out
+
+    def stream_of(self, s: "State") -> int:
+        v = ct.c_void_p()
+        self.check(self._fn("state_stream")(s.handle, ct.byref(v)))
+        return v.value or 0
+
     # ---- states ----
     def create(self, n: int, mixed: bool = False) -> State:
         h = ct.c_void_p()
