@@ -420,6 +420,7 @@ def main():
                               + ("inputs larger than L2, no flush" if wl.n + (wl.n if wl.mixed else 0) >= 24
                                  else "state L2-resident (reported as is)"))},
             "roofline": roof,
+            "kernels": {k: {"launches": v[0], "ms": round(v[1], 4)} for k, v in prof.items()},
             "hbm_gbs_algorithmic": algo_gbs,
             "hbm_frac_algorithmic": algo_gbs / peak,
             "gpu_launches": launches,

@@ -1,0 +1,60 @@
+// Stage planner for the fused tile executor.
+//
+// Every operation is analysed into
+//   * mixing bits    — bits whose values the matrix couples (must live in the
+//                      shared-memory tile), at most 4;
+//   * condition bits — bits in which the matrix is block diagonal (controls,
+//                      diagonal phases); they select one of 2^nc sub-matrices
+//                      and are read from the amplitude's global index, so they
+//                      may lie anywhere in the state.
+// Consecutive operations are greedily packed into stages whose mixing bits
+// fit a 2^k tile that always contains the lowest three bits (128-B runs);
+// a later operation may overtake a deferred one only if their supports are
+// disjoint (they commute), so the stage order reproduces the program exactly.
+#pragma once
+
+#include "engine.hpp"
+
+namespace vqb {
+
+constexpr int kMaxMix = 4;
+constexpr int kMaxCond = 6;
+constexpr int kLowBits = 3;
+constexpr int kMaxPlanOps = 96; // per stage, before block fusion (bounds shared memory)
+
+struct FusedOp {
+    int nt = 0, nc = 0, np = 0;
+    int mix[kMaxMix] = {};   // global bits, local sub-matrix order
+    int cnd[kMaxCond] = {};  // global bits, condition index order
+    cvec sub_phi;            // 2^nc blocks of (2^nt)^2, column-major
+    cvec sub_psi;            // pair ops only (phi and psi matrices differ)
+    cvec sub_d;              // np * 2^nc blocks (param ops)
+    bool pair = false;
+    int64_t grad_base = -1;
+    double scale = 1.0;
+    uint64_t support = 0;    // all bits touched (commutation test)
+    uint64_t mixmask = 0;
+    bool fusable = true;
+    Gate gate;               // original (fallback path)
+    const RevOp *rev = nullptr;
+};
+
+struct Stage {
+    bool fused = true;       // false: a single unfusable op, run unfused
+    int k = 0;
+    int bits[24] = {};       // tile bits, ascending (global positions)
+    std::vector<int> ops;    // indices into the op list, in execution order
+};
+
+FusedOp analyse_gate(const Gate &g);
+FusedOp analyse_rev(const RevOp &r);
+std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k);
+
+// Within one stage, multiply runs of non-parametric operations into dense
+// blocks on at most `max_support` qubits (an operation is moved only past
+// operations on disjoint qubits). Parametric reverse steps are kept as they
+// are. Returns the stage's new operation list (re-analysed).
+std::vector<FusedOp> fuse_blocks(const std::vector<FusedOp> &ops, const std::vector<int> &order,
+                                 int max_support);
+
+} // namespace vqb

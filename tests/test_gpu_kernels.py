@@ -265,3 +265,31 @@ def test_reverse_step(dev, ref):
     got = dev.reverse_step(dphi, dpsi, pos, inv, dmats)
     want = ref.reverse_step(rphi, rpsi, pos, inv, dmats)
     assert np.max(np.abs(np.array(got) - np.array(want))) <= 1e-12
+
+
+@pytest.mark.parametrize("tile_bits,fuse", [("8", "2"), ("10", "0"), ("12", "2"), ("7", "1")])
+def test_fused_planner_variants(dev, ref, monkeypatch, tile_bits, fuse):
+    """Stage planning / block fusion under several tile sizes against the
+    reference: random named, parametric and generic gates incl. controls on
+    bits outside the tile."""
+    monkeypatch.setenv("VQB_TILE_BITS", tile_bits)
+    monkeypatch.setenv("VQB_TILE_BITS_REV", tile_bits)
+    monkeypatch.setenv("VQB_FUSE_QUBITS", fuse)
+    rng = np.random.default_rng(int(tile_bits) * 7 + int(fuse))
+    n = 15
+    c = Circuit([random_gate(n, rng) for _ in range(300)])
+    amps = random_state(n, rng)
+    d, r = both(dev, ref, amps)
+    dev.apply_circuit(c, d)
+    ref.apply_circuit(c, r)
+    assert np.max(np.abs(dev.download(d) - ref.download(r))) <= TOL
+    w = circuits.config2(n=12, p=2)
+    loss, g = dev.gradient_pure(w.observable, w.circuit, dev.pure_state(12))
+    rloss, rg = ref.gradient_pure(w.observable, w.circuit, ref.pure_state(12))
+    assert abs(loss - rloss) <= 1e-10 * abs(rloss)
+    assert np.max(np.abs(g - rg)) <= 1e-10 * np.max(np.abs(rg))
+    w = circuits.config3(n=4, layers=1)
+    loss, g = dev.gradient_mixed(w.observable, w.circuit, dev.mixed_state(4))
+    rloss, rg = ref.gradient_mixed(w.observable, w.circuit, ref.mixed_state(4))
+    assert abs(loss - rloss) <= 1e-10 * abs(rloss)
+    assert np.max(np.abs(g - rg)) <= 1e-10 * np.max(np.abs(rg))
