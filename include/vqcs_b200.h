@@ -227,6 +227,20 @@ VQB_API int vqb_gradient_mixed(const vqb_op *ops, int64_t count,
                                int64_t capacity, int64_t *num_grads,
                                double *reverse_residual);
 
+/* ---- host-only planning (no device work; no reference analogue) ---- */
+/* Plans the fused execution of a circuit exactly as vqb_apply_circuit does
+ * (stage packing into 2^tile_bits tiles, then block fusion on at most
+ * max_support qubits) and exports the result as dense blocks in execution
+ * order: block b acts on num_positions[b] 1-based positions
+ * positions[6*b ...] of the (pseudo) state with the column-major matrix
+ * matrices[stride*b ...] (stride = 256, so blocks of at most 4 positions).
+ * mixed != 0 plans the density-matrix program of an n-qubit MixedState.
+ * With cap == 0 only *num_blocks and *num_stages are computed. */
+VQB_API int vqb_plan_blocks(const vqb_op *ops, int64_t count, int32_t num_qubits, int32_t mixed,
+                            int32_t tile_bits, int32_t max_support, int64_t cap,
+                            int64_t *num_blocks, int64_t *num_stages, int32_t *num_positions,
+                            int32_t *positions, vqb_c128 *matrices);
+
 /* ---- host-side gate algebra (gates.hpp), exported for bindings ---- */
 /* Matrix of a gate descriptor: the caller's matrix if given, else built from
  * kind/params (gates.hpp:188-259,309-373). out: 4^m entries. */

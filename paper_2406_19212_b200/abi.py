@@ -384,6 +384,8 @@ def bind_abi(lib: ct.CDLL, prefix: str) -> None:
         "profile_begin": (ct.c_int, []),
         "profile_end": (ct.c_int, [ct.c_char_p, i64]),
         "state_stream": (ct.c_int, [vp, ct.POINTER(vp)]),
+        "plan_blocks": (ct.c_int, [op_p, i64, i32, i32, i32, i32, i64, ct.POINTER(i64),
+                                   ct.POINTER(i64), ct.POINTER(i32), ct.POINTER(i32), c128_p]),
         # oracle-only
         "apply_gate_naive": (ct.c_int, [vp, op_p]),
         "set_num_threads": (None, [ct.c_int]),
@@ -405,5 +407,5 @@ ABI_FUNCTIONS = [
     "apply_circuit", "apply_circuit_unfused", "norm", "trace", "expectation",
     "apply_operator", "bilinear_form", "reverse_step", "loss_pure", "gradient_pure",
     "loss_mixed", "gradient_mixed", "gate_matrix", "gate_derivative", "gate_inverse",
-    "channel_superop",
+    "channel_superop", "plan_blocks",
 ]

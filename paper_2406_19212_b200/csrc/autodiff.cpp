@@ -21,13 +21,47 @@ struct DevBuf {
     template <typename T> T *as() { return static_cast<T *>(p); }
 };
 
+// Working states of the losses / gradients. States up to 2^26 amplitudes
+// (1 GiB) are cached per thread and reused across calls (allocation, stream
+// and workspace setup otherwise dominate small problems such as config 0);
+// larger ones are allocated per call so no large buffer outlives the call.
+constexpr uint64_t kCacheLimit = 1ull << 26;
+
+struct ScratchCache {
+    std::vector<DeviceState *> free_list;
+    ~ScratchCache() {
+        for (auto *s : free_list) state_destroy(s);
+    }
+};
+thread_local ScratchCache g_cache;
+
+DeviceState *scratch(int n, int mixed) {
+    const uint64_t size = 1ull << (mixed ? 2 * n : n);
+    if (size <= kCacheLimit)
+        for (size_t i = 0; i < g_cache.free_list.size(); ++i) {
+            DeviceState *s = g_cache.free_list[i];
+            if (s->n == n && s->mixed == mixed) {
+                g_cache.free_list.erase(g_cache.free_list.begin() + i);
+                return s;
+            }
+        }
+    return state_create(n, mixed);
+}
+
 struct StateGuard {
     DeviceState *s;
-    ~StateGuard() { state_destroy(s); }
+    ~StateGuard() {
+        if (s->size <= kCacheLimit && g_cache.free_list.size() < 8) {
+            cudaStreamSynchronize(s->stream);
+            g_cache.free_list.push_back(s);
+        } else {
+            state_destroy(s);
+        }
+    }
 };
 
 DeviceState *clone(const DeviceState *src) {
-    DeviceState *d = state_create(src->n, src->mixed);
+    DeviceState *d = scratch(src->n, src->mixed);
     VQB_CUDA(cudaStreamSynchronize(src->stream));
     VQB_CUDA(cudaMemcpyAsync(d->amps, src->amps, sizeof(double2) * src->size,
                              cudaMemcpyDeviceToDevice, d->stream));
@@ -112,7 +146,7 @@ GradientOut gradient_pure(const vqb_op *ops, int64_t count, const vqb_pauli_term
         out.loss = expectation(phi, op).real();
         return out;
     }
-    DeviceState *psi = state_create(n, 0);
+    DeviceState *psi = scratch(n, 0); // fully overwritten by apply_operator
     StateGuard gpsi{psi};
     VQB_CUDA(cudaStreamSynchronize(psi->stream));
     apply_operator(phi, psi->amps, op, false);
@@ -181,7 +215,7 @@ GradientOut gradient_mixed(const vqb_op *ops, int64_t count, const vqb_pauli_ter
     StateGuard gphi{phi};
     run_program(phi, mixed_forward_program(es, n), fused);
 
-    DeviceState *psi = state_create(n, 1);
+    DeviceState *psi = scratch(n, 1); // fully overwritten by identity_costate
     StateGuard gpsi{psi};
     identity_costate(psi, op); // <<Psi| = <<I| H (autodiff.hpp:241-248)
     VQB_CUDA(cudaStreamSynchronize(psi->stream));

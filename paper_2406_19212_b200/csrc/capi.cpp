@@ -5,6 +5,7 @@
 
 #include "autodiff.hpp"
 #include "engine.hpp"
+#include "plan.hpp"
 
 using namespace vqb;
 
@@ -396,6 +397,56 @@ VQB_API int vqb_gradient_mixed(const vqb_op *ops, int64_t count, const vqb_pauli
         const auto r = gradient_mixed(ops, count, terms, nt, ds(dm0), res != nullptr, true);
         if (!r.grads.empty()) need(grads, "grads");
         write_grads(r, loss, grads, cap, ng, res);
+    });
+}
+
+VQB_API int vqb_plan_blocks(const vqb_op *ops, int64_t count, int32_t n, int32_t mixed,
+                            int32_t tile_bits, int32_t max_support, int64_t cap,
+                            int64_t *num_blocks, int64_t *num_stages, int32_t *num_positions,
+                            int32_t *positions, vqb_c128 *matrices) {
+    return guard([&] {
+        need(num_blocks, "num_blocks");
+        need(num_stages, "num_stages");
+        if (count > 0) need(ops, "ops");
+        const auto es = build_elements(ops, count);
+        std::vector<Gate> prog;
+        if (mixed) {
+            prog = mixed_forward_program(es, n);
+        } else {
+            for (const auto &e : es) {
+                if (e.channel) raise(VQB_ERR_TYPE, "plan_blocks: channel in a pure-state program");
+                prog.push_back(e.gate);
+            }
+        }
+        const int pn = mixed ? 2 * n : n;
+        for (const auto &g : prog) check_fit(g.pos, g.m, pn);
+        std::vector<FusedOp> fops;
+        for (const auto &g : prog) fops.push_back(analyse_gate(g));
+        const auto stages = plan_stages(fops, pn, tile_bits);
+        int64_t nb = 0;
+        for (const auto &sg : stages) {
+            std::vector<FusedOp> blocks;
+            if (sg.fused && max_support > 0) {
+                blocks = fuse_blocks(fops, sg.ops, max_support);
+            } else {
+                for (int i : sg.ops) blocks.push_back(fops[i]);
+            }
+            for (const auto &b : blocks) {
+                if (nb < cap) {
+                    const Gate &g = b.gate;
+                    if (g.m > 4) raise(VQB_ERR_UNSUPPORTED, "plan_blocks: block wider than 4 positions");
+                    num_positions[nb] = g.m;
+                    for (int k = 0; k < g.m; ++k) positions[6 * nb + k] = g.pos[k];
+                    for (size_t i = 0; i < g.mat.size(); ++i) {
+                        matrices[256 * nb + i].re = g.mat[i].real();
+                        matrices[256 * nb + i].im = g.mat[i].imag();
+                    }
+                }
+                ++nb;
+            }
+        }
+        *num_blocks = nb;
+        *num_stages = (int64_t)stages.size();
     });
 }
 

@@ -818,12 +818,25 @@ void reverse_step_async(double2 *phi, double2 *psi, int pn, const int *pos1, int
 }
 
 // ------------------------------------------------------------------ state management
+// Pinned host staging for small results: one 1-KiB block per thread, shared
+// by the states that thread drives (API calls are synchronous per thread).
+// Deliberately never freed: a state may outlive the thread that created it.
+struct PinnedResults {
+    double2 *p = nullptr;
+};
+static thread_local PinnedResults g_pinned;
+
 static void alloc_workspace(DeviceState *s) {
-    VQB_CUDA(cudaMalloc(&s->ws.partials, sizeof(double2) * kMaxReduceBlocks * kMaxReduceSlots));
-    VQB_CUDA(cudaMalloc(&s->ws.counter, sizeof(unsigned) * 4));
-    VQB_CUDA(cudaMemset(s->ws.counter, 0, sizeof(unsigned) * 4));
-    VQB_CUDA(cudaMalloc(&s->ws.result, sizeof(double2) * 64));
-    VQB_CUDA(cudaMallocHost(&s->ws.host_result, sizeof(double2) * 64));
+    // one device allocation: partials | result | counter
+    const size_t pb = sizeof(double2) * kMaxReduceBlocks * kMaxReduceSlots;
+    char *base = nullptr;
+    VQB_CUDA(cudaMalloc(&base, pb + sizeof(double2) * 64 + 64));
+    s->ws.partials = reinterpret_cast<double2 *>(base);
+    s->ws.result = reinterpret_cast<double2 *>(base + pb);
+    s->ws.counter = reinterpret_cast<unsigned *>(base + pb + sizeof(double2) * 64);
+    VQB_CUDA(cudaMemsetAsync(s->ws.counter, 0, sizeof(unsigned) * 4, s->stream));
+    if (!g_pinned.p) VQB_CUDA(cudaMallocHost(&g_pinned.p, sizeof(double2) * 64));
+    s->ws.host_result = g_pinned.p;
 }
 
 DeviceState *state_create(int n, int mixed) {
@@ -879,10 +892,7 @@ void state_destroy(DeviceState *s) {
     if (!s) return;
     cudaStreamSynchronize(s->stream);
     if (s->owned && s->amps) cudaFree(s->amps);
-    cudaFree(s->ws.partials);
-    cudaFree(s->ws.counter);
-    cudaFree(s->ws.result);
-    cudaFreeHost(s->ws.host_result);
+    cudaFree(s->ws.partials); // partials | result | counter are one allocation
     if (s->ws.terms) cudaFree(s->ws.terms);
     cudaStreamDestroy(s->stream);
     delete s;

@@ -230,6 +230,30 @@ class Engine:
     def gradient_mixed(self, op, c, dm0, with_residual=False):
         return self._gradient("gradient_mixed", op, c, dm0, with_residual)
 
+    # ---- host-only planning (product library) ----
+    def plan_blocks(self, c: Circuit, n: int, mixed: bool = False, tile_bits: int = 12,
+                    max_support: int = 2):
+        """-> (blocks [(positions, column-major matrix)], num_stages) exactly as
+        the fused executor would run them; no device work."""
+        p = c.pack() if isinstance(c, Circuit) else pack_ops(c)
+        nb, ns = ct.c_int64(), ct.c_int64()
+        fn = self._fn("plan_blocks")
+        self.check(fn(p.arr, p.count, n, int(mixed), tile_bits, max_support, 0, ct.byref(nb),
+                      ct.byref(ns), None, None, None))
+        cap = nb.value
+        npos = np.zeros(max(cap, 1), dtype=np.int32)
+        pos = np.zeros(6 * max(cap, 1), dtype=np.int32)
+        mats = np.zeros(256 * max(cap, 1), dtype=np.complex128)
+        self.check(fn(p.arr, p.count, n, int(mixed), tile_bits, max_support, cap, ct.byref(nb),
+                      ct.byref(ns), npos.ctypes.data_as(ct.POINTER(ct.c_int32)),
+                      pos.ctypes.data_as(ct.POINTER(ct.c_int32)), mats.ctypes.data_as(c128_p)))
+        blocks = []
+        for b in range(nb.value):
+            m = int(npos[b])
+            d = 1 << m
+            blocks.append((list(pos[6 * b: 6 * b + m]), mats[256 * b: 256 * b + d * d].copy()))
+        return blocks, ns.value
+
     # ---- gate algebra ----
     def _mat_call(self, fn, op, dim, *extra):
         out = np.zeros(dim * dim, dtype=np.complex128)
