@@ -761,7 +761,25 @@ void execute(DeviceState *sphi, DeviceState *spsi, const std::vector<FusedOp> &f
 
 } // namespace
 
+bool regstage_available(int pn);
+void run_program_reg(DeviceState *s, const std::vector<Gate> &prog);
+
+// One stage through the shared-memory executor (used by the register
+// executor when a stage's program exceeds its parameter block).
+void run_program_fused_smem_stage(DeviceState *s, const std::vector<FusedOp> &fops,
+                                  const Stage &sg) {
+    execute<false>(s, nullptr, fops, std::vector<Stage>{sg}, s->pn, nullptr,
+                   [&](const FusedOp &f) { apply_gate_fast(s->amps, s->pn, f.gate, s->stream); });
+}
+
 void run_program_fused(DeviceState *s, const std::vector<Gate> &prog) {
+    // register-resident executor for states of >= 2^12 amplitudes
+    // (VQB_EXECUTOR=smem selects the shared-memory interpreter instead)
+    const char *ex = std::getenv("VQB_EXECUTOR");
+    if (regstage_available(s->pn) && !(ex && std::strcmp(ex, "smem") == 0)) {
+        run_program_reg(s, prog);
+        return;
+    }
     std::vector<FusedOp> fops;
     fops.reserve(prog.size());
     for (const auto &g : prog) fops.push_back(analyse_gate(g));
