@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -545,6 +546,14 @@ void run_program_reg(DeviceState *s, const std::vector<Gate> &prog) {
         if (!lower_stage_reg(sg, blocks, s->pn, P)) {
             run_program_fused_smem_stage(s, fops, sg);
             continue;
+        }
+        if (std::getenv("VQB_PLAN_STATS")) {
+            int nt_hist[5] = {0, 0, 0, 0, 0}, nops = 0;
+            for (int i = 0; i < P.nsubs; ++i) nops += P.subs[i].op_count;
+            for (int i = 0; i < nops; ++i) nt_hist[std::min(P.ops[i].nt, 4)]++;
+            std::fprintf(stderr, "[regstage] gates %zu blocks %zu subs %d ops nt0..4 %d %d %d %d %d\n",
+                         sg.ops.size(), blocks.size(), P.nsubs, nt_hist[0], nt_hist[1], nt_hist[2],
+                         nt_hist[3], nt_hist[4]);
         }
         const int grid = (int)std::min<unsigned long long>((unsigned long long)nsm * std::max(per_sm, 1),
                                                            (P.ntiles + G - 1) / G);
