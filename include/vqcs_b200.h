@@ -135,6 +135,10 @@ VQB_API int64_t vqb_kernel_launch_count(void);
  * the reference only wall-clocks whole calls, src/bench.cpp:76-87).
  * vqb_profile_end synchronises the device and writes one line per kernel
  * name: "<name> <launches> <total_ms>\n" (truncated to `cap` bytes). */
+/* Algorithmic FP64 flops issued by the fused executors so far (a dense
+ * complex 2^m x 2^m block costs 8 * 2^m flops per amplitude); the FP64
+ * roofline numerator for benchmarks. */
+VQB_API double vqb_flop_count(void);
 VQB_API int vqb_profile_begin(void);
 VQB_API int vqb_profile_end(char *buf, int64_t cap);
 

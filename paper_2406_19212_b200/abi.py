@@ -381,6 +381,7 @@ def bind_abi(lib: ct.CDLL, prefix: str) -> None:
         "apply_circuit_unfused": (ct.c_int, [vp, op_p, i64]),
         "build_info": (ct.c_char_p, []),
         "kernel_launch_count": (i64, []),
+        "flop_count": (ct.c_double, []),
         "profile_begin": (ct.c_int, []),
         "profile_end": (ct.c_int, [ct.c_char_p, i64]),
         "state_stream": (ct.c_int, [vp, ct.POINTER(vp)]),
@@ -400,7 +401,7 @@ def bind_abi(lib: ct.CDLL, prefix: str) -> None:
 
 
 ABI_FUNCTIONS = [
-    "last_error", "build_info", "kernel_launch_count", "profile_begin", "profile_end",
+    "last_error", "build_info", "kernel_launch_count", "flop_count", "profile_begin", "profile_end",
     "state_stream", "state_create", "state_wrap",
     "state_destroy", "state_info", "state_device_ptr", "state_set_zero", "state_upload",
     "state_download", "state_copy", "apply_gate", "apply_channel", "apply_matrix",

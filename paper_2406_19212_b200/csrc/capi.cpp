@@ -13,6 +13,7 @@ struct vqb_state : DeviceState {};
 
 namespace vqb {
 int64_t launch_count();
+double flop_count();
 void prof_start();
 std::string prof_stop();
 }
@@ -79,6 +80,8 @@ VQB_API const char *vqb_build_info(void) {
 }
 
 VQB_API int64_t vqb_kernel_launch_count(void) { return vqb::launch_count(); }
+
+VQB_API double vqb_flop_count(void) { return vqb::flop_count(); }
 
 VQB_API int vqb_profile_begin(void) {
     return guard([&] { prof_start(); });

@@ -790,8 +790,16 @@ void run_program_fused(DeviceState *s, const std::vector<Gate> &prog) {
     });
 }
 
+void run_reverse_reg(DeviceState *phi, DeviceState *psi, const std::vector<RevOp> &prog,
+                     double *dgrads);
+
 void run_reverse_fused(DeviceState *phi, DeviceState *psi, const std::vector<RevOp> &prog,
                        double *dgrads) {
+    const char *ex = std::getenv("VQB_EXECUTOR");
+    if (regstage_available(phi->pn) && !(ex && std::strcmp(ex, "smem") == 0)) {
+        run_reverse_reg(phi, psi, prog, dgrads);
+        return;
+    }
     std::vector<FusedOp> fops;
     fops.reserve(prog.size());
     for (const auto &r : prog) fops.push_back(analyse_rev(r));

@@ -45,6 +45,15 @@ cudaEvent_t take_event() {
 void note_launch(int64_t n) { g_launches += n; }
 int64_t launch_count() { return g_launches.load(); }
 
+// Algorithmic FP64 flops issued by the fused executors (complex MAC = 8 flops).
+static std::atomic<double> g_flops{0.0};
+void note_flops(double f) {
+    double cur = g_flops.load();
+    while (!g_flops.compare_exchange_weak(cur, cur + f)) {
+    }
+}
+double flop_count() { return g_flops.load(); }
+
 ProfMark prof_begin(cudaStream_t st) {
     ProfMark m;
     if (!g_prof.load(std::memory_order_relaxed)) return m;

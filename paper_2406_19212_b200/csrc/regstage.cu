@@ -1,22 +1,26 @@
-// Register-resident stage executor (forward programs).
+// Register-resident stage executor (forward programs and adjoint sweeps).
 //
-// A stage's tile (K = 12 tile bits = 4096 amplitudes) is split over 256
-// threads x 16 registers. A *layout* assigns 4 tile bits to the register
-// index and 8 to the thread index. Within a sub-stage every operation's
-// mixing bits are register bits, so the operation is pure register
-// arithmetic (FP64 FMA bound, no shared memory, no barrier). Between
-// sub-stages the tile is re-laid out once through shared memory, XOR-swizzled
-// so the three quarter-warp lane bits always hit distinct bank groups.
+// A stage's tile (K = 11 tile bits = 2048 amplitudes per state) is split over
+// 128 threads x 16 registers. A *layout* assigns 4 tile bits to the register
+// index and 7 to the thread index. Within a sub-stage every operation's
+// mixing bits are register bits, so the operation is pure register arithmetic
+// (FP64 FMA bound, no shared memory, no barrier). Between sub-stages the tile
+// is re-laid out once through shared memory, XOR-swizzled so the three
+// quarter-warp lane bits always hit distinct bank groups. The next tile is
+// prefetched with cp.async (LDGSTS) into a staging buffer while the current
+// one is computed; results are stored straight from registers. Two blocks run
+// per SM, so one block's relayout or load phase overlaps the other's FP64.
 //
-// The stage program (layouts, operations, sub-matrices) is passed as one
-// __grid_constant__ parameter block: every thread reads the same words, so
-// the matrices come through the constant cache (LDC) instead of occupying
-// registers, which keeps the kernel at <= 128 registers = 2 blocks (16 warps)
-// per SM; one block's HBM load overlaps the other's arithmetic.
+// The stage program (layouts, operations, sub-matrices) is one
+// __grid_constant__ parameter block (read through the constant cache);
+// programs that do not fit are split over several launches of the same tile
+// bits.
 //
-// Host side: sub-stage packing reuses the stage planner's rule (an op may
-// overtake a deferred one only if their supports are disjoint), with the
-// register-bit budget instead of the tile budget.
+// Adjoint mode (REV): each thread holds 16 amplitudes of Phi and of Psi; a
+// parametric step computes Phi <- inv Phi, Re <Psi| D_p |Phi>, Psi <- inv Psi
+// in registers (reverse_sweep_step kernels.hpp:659-697); contributions are
+// reduced per warp into shared-memory slots, per block into a partial row,
+// and over blocks in fixed order by k_grads (deterministic for a fixed grid).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -29,21 +33,25 @@
 namespace vqb {
 
 void apply_gate_fast(double2 *a, int pn, const Gate &g, cudaStream_t st);
+void note_flops(double f);
+void reverse_step_async(double2 *phi, double2 *psi, int pn, const int *pos1, int m,
+                        const cvec &inv, const std::vector<cvec> &dmats, DeviceState *w,
+                        double2 *out_c, double *out_r, double real_scale);
 
 namespace {
 
 constexpr int RB = 4;       // register bits
-constexpr int R = 1 << RB;  // amplitudes per thread
-constexpr int TB = 7;       // thread bits (per tile group)
-constexpr int TG = 1 << TB; // threads per tile group
-constexpr int G = 2;        // independent tile groups per block (named barriers)
-constexpr int T = TG * G;   // threads per block
+constexpr int R = 1 << RB;  // amplitudes per thread (per state)
+constexpr int TB = 7;       // thread bits
+constexpr int T = 1 << TB;  // threads per block (one tile per block at a time)
+constexpr int NW = T / 32;  // warps per block
 constexpr int K = RB + TB;  // tile bits
 constexpr int TS = 1 << K;  // tile size
 
-constexpr int kMaxSubs = 40;
-constexpr int kMaxOps = 64;
-constexpr int kMaxPool = 1024; // double2 entries
+constexpr int kMaxSubs = 32;
+constexpr int kMaxOps = 56;
+constexpr int kMaxSlots = 64;
+constexpr int kMaxPool = 1280; // double2 entries
 
 struct RLayout {
     int reg[RB]; // tile-local bit of register bit b
@@ -51,14 +59,15 @@ struct RLayout {
 };
 
 struct ROp {
-    int nt, nc;
+    int nt, nc, np;
     int code;             // nt = 1: p0; nt = 2: pair index; nt = 3: triple index
     int per_group;        // condition depends on register bits
+    int pair;             // psi has its own matrices (channel steps)
+    int slot;             // first gradient slot (param ops)
     int ck[kMaxCond];     // 0: outside tile, 1: thread bit, 2: register bit
     int cp[kMaxCond];     // global bit / thread bit / register bit
-    unsigned mat;         // pool offset of 2^nc sub-matrices (ascending register order)
-    unsigned nz;          // nt <= 2: union sparsity of the sub-matrices
-    unsigned long long ident;
+    unsigned mat, mat_psi, mat_d; // pool offsets (2^nc sub-matrices each, ascending order)
+    unsigned long long ident, ident_psi;
 };
 
 struct RSub {
@@ -69,11 +78,12 @@ struct RSub {
 struct RParams {
     int bits[K];                // tile bits ascending (global); local bit j <-> bits[j]
     unsigned long long ntiles;
-    int nsubs;
+    int nsubs, nslots, slot_begin, partial_ld;
     RSub subs[kMaxSubs];
     ROp ops[kMaxOps];
     double2 pool[kMaxPool];
 };
+static_assert(sizeof(RParams) <= 32000, "kernel parameter block too large");
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
@@ -81,15 +91,16 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
     return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
 }
+// Re(conj(a) * b)
+__device__ __forceinline__ double re_cj(double2 a, double2 b) { return fma(a.x, b.x, a.y * b.y); }
 
 // shared-memory slot of a tile-local index: low 3 bits XOR-folded with the
-// three higher 3-bit chunks (local bit l contributes to bank bit l mod 3).
+// higher 3-bit chunks (local bit l contributes to bank bit l mod 3).
 // XOR-linear: swz(a | b) = swz(a) ^ swz(b) for disjoint a, b.
 __host__ __device__ __forceinline__ int swz(int l) {
     return l ^ ((l >> 3) & 7) ^ ((l >> 6) & 7) ^ ((l >> 9) & 7);
 }
 
-// Per-thread addressing of one layout: slot(i) = st ^ XOR_{b in i} sw[b]
 struct Addr {
     int st;
     int sw[RB];
@@ -122,70 +133,123 @@ __device__ __forceinline__ int cond_of(const ROp &op, int cbase, int i) {
     return c;
 }
 
-// nt-bit operation on register positions P[0..NT) (ascending). Group-major:
-// each group's outputs are formed in a small temporary, entries of the
-// sub-matrix are read from the parameter block (constant cache).
-template <int NT, int P0, int P1 = 0, int P2 = 0, int P3 = 0>
-__device__ __forceinline__ void apply_r(double2 (&v)[R], const ROp &op, const double2 *pool,
-                                        int cbase) {
-    constexpr int D = 1 << NT;
-    constexpr int P[4] = {P0, P1, P2, P3};
-    constexpr int MASK = (NT > 0 ? 1 << P0 : 0) | (NT > 1 ? 1 << P1 : 0) | (NT > 2 ? 1 << P2 : 0) |
-                         (NT > 3 ? 1 << P3 : 0);
-    auto off = [&](int r) constexpr {
+template <int NT, int P0, int P1, int P2, int P3> struct Pos {
+    static constexpr int D = 1 << NT;
+    static constexpr int MASK = (NT > 0 ? 1 << P0 : 0) | (NT > 1 ? 1 << P1 : 0) |
+                                (NT > 2 ? 1 << P2 : 0) | (NT > 3 ? 1 << P3 : 0);
+    __host__ __device__ static constexpr int off(int r) {
         int o = 0;
-        for (int q = 0; q < NT; ++q)
-            if (r >> q & 1) o |= 1 << P[q];
+        if (NT > 0 && (r & 1)) o |= 1 << P0;
+        if (NT > 1 && (r & 2)) o |= 1 << P1;
+        if (NT > 2 && (r & 4)) o |= 1 << P2;
+        if (NT > 3 && (r & 8)) o |= 1 << P3;
         return o;
-    };
-    if (NT <= 2 && !op.per_group) {
-        // uniform sub-matrix: loaded once into registers, reused by every group
-        if ((op.ident >> cbase) & 1) return;
-        const double2 *M = pool + op.mat + cbase * D * D;
+    }
+};
+
+// out = M * v[group], written back in place; M read element by element.
+template <class PS>
+__device__ __forceinline__ void group_mv(double2 (&v)[R], int i, const double2 *M) {
+    constexpr int D = PS::D;
+    double2 out[D];
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+        double2 acc = cmul(M[r], v[i | PS::off(0)]);
+#pragma unroll
+        for (int s = 1; s < D; ++s) acc = cfma(M[r + s * D], v[i | PS::off(s)], acc);
+        out[r] = acc;
+    }
+#pragma unroll
+    for (int r = 0; r < D; ++r) v[i | PS::off(r)] = out[r];
+}
+
+// Apply an nt-bit operation (sub-matrices at `mat`) to one register state.
+// HOIST: a uniform sub-matrix of nt <= HOIST is loaded into registers once.
+template <int HOIST, int NT, int P0, int P1 = 0, int P2 = 0, int P3 = 0>
+__device__ __forceinline__ void apply_r(double2 (&v)[R], const ROp &op, const double2 *pool,
+                                        int cbase, unsigned mat, unsigned long long ident) {
+    using PS = Pos<NT, P0, P1, P2, P3>;
+    constexpr int D = PS::D;
+    if (NT <= HOIST && !op.per_group) {
+        if ((ident >> cbase) & 1) return;
+        const double2 *M = pool + mat + cbase * D * D;
         double2 m[D * D];
 #pragma unroll
         for (int e = 0; e < D * D; ++e) m[e] = M[e];
 #pragma unroll
+        for (int i = 0; i < R; ++i)
+            if (!(i & PS::MASK)) group_mv<PS>(v, i, m);
+        return;
+    }
+    if (!op.per_group && ((ident >> cbase) & 1)) return;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        if (i & PS::MASK) continue;
+        const int c = op.per_group ? cond_of(op, cbase, i) : cbase;
+        if (op.per_group && ((ident >> c) & 1)) continue;
+        group_mv<PS>(v, i, pool + mat + c * D * D);
+    }
+}
+
+// Reverse-sweep parametric step on (phi, psi) registers.
+template <int NT, int P0, int P1 = 0, int P2 = 0, int P3 = 0>
+__device__ __forceinline__ void param_r(double2 (&vf)[R], double2 (&vg)[R], const ROp &op,
+                                        const double2 *pool, int cbase, double (&acc)[VQB_MAX_PARAMS]) {
+    using PS = Pos<NT, P0, P1, P2, P3>;
+    constexpr int D = PS::D;
+    const int nsub = 1 << op.nc;
+    if (NT <= 1 && !op.per_group && op.np == 1) {
+        double2 m[D * D], d[D * D];
+#pragma unroll
+        for (int e = 0; e < D * D; ++e) {
+            m[e] = pool[op.mat + cbase * D * D + e];
+            d[e] = pool[op.mat_d + cbase * D * D + e];
+        }
+#pragma unroll
         for (int i = 0; i < R; ++i) {
-            if (i & MASK) continue;
-            double2 out[D];
+            if (i & PS::MASK) continue;
+            group_mv<PS>(vf, i, m);
+            double a = 0;
 #pragma unroll
             for (int r = 0; r < D; ++r) {
-                double2 acc = cmul(m[r], v[i | off(0)]);
+                double2 x = cmul(d[r], vf[i | PS::off(0)]);
 #pragma unroll
-                for (int s = 1; s < D; ++s) acc = cfma(m[r + s * D], v[i | off(s)], acc);
-                out[r] = acc;
+                for (int s = 1; s < D; ++s) x = cfma(d[r + s * D], vf[i | PS::off(s)], x);
+                a += re_cj(vg[i | PS::off(r)], x);
             }
-#pragma unroll
-            for (int r = 0; r < D; ++r) v[i | off(r)] = out[r];
+            acc[0] += a;
+            group_mv<PS>(vg, i, m);
         }
         return;
     }
-    if (!op.per_group && ((op.ident >> cbase) & 1)) return;
 #pragma unroll
     for (int i = 0; i < R; ++i) {
-        if (i & MASK) continue;
+        if (i & PS::MASK) continue;
         const int c = op.per_group ? cond_of(op, cbase, i) : cbase;
-        if (op.per_group && ((op.ident >> c) & 1)) continue;
-        const double2 *M = pool + op.mat + c * D * D;
-        double2 out[D];
+        group_mv<PS>(vf, i, pool + op.mat + c * D * D);
 #pragma unroll
-        for (int r = 0; r < D; ++r) {
-            double2 acc = cmul(M[r], v[i | off(0)]);
+        for (int p = 0; p < VQB_MAX_PARAMS; ++p) {
+            if (p >= op.np) break;
+            const double2 *Dm = pool + op.mat_d + (p * nsub + c) * D * D;
+            double a = 0;
 #pragma unroll
-            for (int s = 1; s < D; ++s) acc = cfma(M[r + s * D], v[i | off(s)], acc);
-            out[r] = acc;
+            for (int r = 0; r < D; ++r) {
+                double2 x = cmul(Dm[r], vf[i | PS::off(0)]);
+#pragma unroll
+                for (int s = 1; s < D; ++s) x = cfma(Dm[r + s * D], vf[i | PS::off(s)], x);
+                a += re_cj(vg[i | PS::off(r)], x);
+            }
+            acc[p] += a;
         }
-#pragma unroll
-        for (int r = 0; r < D; ++r) v[i | off(r)] = out[r];
+        group_mv<PS>(vg, i, pool + op.mat + c * D * D);
     }
 }
 
 __device__ __forceinline__ void apply_diag(double2 (&v)[R], const ROp &op, const double2 *pool,
-                                           int cbase) {
+                                           int cbase, unsigned mat, unsigned long long ident) {
     if (!op.per_group) {
-        if ((op.ident >> cbase) & 1) return;
-        const double2 ph = pool[op.mat + cbase];
+        if ((ident >> cbase) & 1) return;
+        const double2 ph = pool[mat + cbase];
 #pragma unroll
         for (int i = 0; i < R; ++i) v[i] = cmul(ph, v[i]);
         return;
@@ -193,54 +257,161 @@ __device__ __forceinline__ void apply_diag(double2 (&v)[R], const ROp &op, const
 #pragma unroll
     for (int i = 0; i < R; ++i) {
         const int c = cond_of(op, cbase, i);
-        if ((op.ident >> c) & 1) continue;
-        v[i] = cmul(pool[op.mat + c], v[i]);
+        if ((ident >> c) & 1) continue;
+        v[i] = cmul(pool[mat + c], v[i]);
     }
 }
 
+template <int HOIST, int MAXNT>
 __device__ __forceinline__ void dispatch(double2 (&v)[R], const ROp &op, const double2 *pool,
-                                         int cbase) {
+                                         int cbase, unsigned mat, unsigned long long ident) {
+    if (op.nt > MAXNT) return; // the caller routes wider ops elsewhere
     switch (op.nt) {
-    case 0: apply_diag(v, op, pool, cbase); return;
+    case 0: apply_diag(v, op, pool, cbase, mat, ident); return;
     case 1:
         switch (op.code) {
-        case 0: apply_r<1, 0>(v, op, pool, cbase); return;
-        case 1: apply_r<1, 1>(v, op, pool, cbase); return;
-        case 2: apply_r<1, 2>(v, op, pool, cbase); return;
-        default: apply_r<1, 3>(v, op, pool, cbase); return;
+        case 0: apply_r<HOIST, 1, 0>(v, op, pool, cbase, mat, ident); return;
+        case 1: apply_r<HOIST, 1, 1>(v, op, pool, cbase, mat, ident); return;
+        case 2: apply_r<HOIST, 1, 2>(v, op, pool, cbase, mat, ident); return;
+        default: apply_r<HOIST, 1, 3>(v, op, pool, cbase, mat, ident); return;
         }
     case 2:
         switch (op.code) {
-        case 0: apply_r<2, 0, 1>(v, op, pool, cbase); return;
-        case 1: apply_r<2, 0, 2>(v, op, pool, cbase); return;
-        case 2: apply_r<2, 0, 3>(v, op, pool, cbase); return;
-        case 3: apply_r<2, 1, 2>(v, op, pool, cbase); return;
-        case 4: apply_r<2, 1, 3>(v, op, pool, cbase); return;
-        default: apply_r<2, 2, 3>(v, op, pool, cbase); return;
+        case 0: apply_r<HOIST, 2, 0, 1>(v, op, pool, cbase, mat, ident); return;
+        case 1: apply_r<HOIST, 2, 0, 2>(v, op, pool, cbase, mat, ident); return;
+        case 2: apply_r<HOIST, 2, 0, 3>(v, op, pool, cbase, mat, ident); return;
+        case 3: apply_r<HOIST, 2, 1, 2>(v, op, pool, cbase, mat, ident); return;
+        case 4: apply_r<HOIST, 2, 1, 3>(v, op, pool, cbase, mat, ident); return;
+        default: apply_r<HOIST, 2, 2, 3>(v, op, pool, cbase, mat, ident); return;
         }
     case 3:
-        switch (op.code) {
-        case 0: apply_r<3, 0, 1, 2>(v, op, pool, cbase); return;
-        case 1: apply_r<3, 0, 1, 3>(v, op, pool, cbase); return;
-        case 2: apply_r<3, 0, 2, 3>(v, op, pool, cbase); return;
-        default: apply_r<3, 1, 2, 3>(v, op, pool, cbase); return;
+        if constexpr (MAXNT >= 3) {
+            switch (op.code) {
+            case 0: apply_r<HOIST, 3, 0, 1, 2>(v, op, pool, cbase, mat, ident); return;
+            case 1: apply_r<HOIST, 3, 0, 1, 3>(v, op, pool, cbase, mat, ident); return;
+            case 2: apply_r<HOIST, 3, 0, 2, 3>(v, op, pool, cbase, mat, ident); return;
+            default: apply_r<HOIST, 3, 1, 2, 3>(v, op, pool, cbase, mat, ident); return;
+            }
         }
-    default: apply_r<4, 0, 1, 2, 3>(v, op, pool, cbase); return;
+        return;
+    default:
+        if constexpr (MAXNT >= 4) apply_r<HOIST, 4, 0, 1, 2, 3>(v, op, pool, cbase, mat, ident);
+        return;
     }
 }
 
-// barrier over the 128 threads of one tile group
-__device__ __forceinline__ void group_sync(int grp) {
-    asm volatile("bar.sync %0, %1;\n" ::"r"(grp + 1), "r"(TG) : "memory");
+__device__ __forceinline__ void dispatch_param(double2 (&vf)[R], double2 (&vg)[R], const ROp &op,
+                                               const double2 *pool, int cbase,
+                                               double (&acc)[VQB_MAX_PARAMS]) {
+    switch (op.nt) {
+    case 0: param_r<0, 0>(vf, vg, op, pool, cbase, acc); return;
+    case 1:
+        switch (op.code) {
+        case 0: param_r<1, 0>(vf, vg, op, pool, cbase, acc); return;
+        case 1: param_r<1, 1>(vf, vg, op, pool, cbase, acc); return;
+        case 2: param_r<1, 2>(vf, vg, op, pool, cbase, acc); return;
+        default: param_r<1, 3>(vf, vg, op, pool, cbase, acc); return;
+        }
+    case 2:
+        switch (op.code) {
+        case 0: param_r<2, 0, 1>(vf, vg, op, pool, cbase, acc); return;
+        case 1: param_r<2, 0, 2>(vf, vg, op, pool, cbase, acc); return;
+        case 2: param_r<2, 0, 3>(vf, vg, op, pool, cbase, acc); return;
+        case 3: param_r<2, 1, 2>(vf, vg, op, pool, cbase, acc); return;
+        case 4: param_r<2, 1, 3>(vf, vg, op, pool, cbase, acc); return;
+        default: param_r<2, 2, 3>(vf, vg, op, pool, cbase, acc); return;
+        }
+    default: return; // wider parametric steps are planned as unfusable
+    }
 }
 
-__global__ void __launch_bounds__(T, 1)
-    k_regstage(double2 *__restrict__ amps, const __grid_constant__ RParams P) {
+// Wide (nt >= 3) operation on one state through the relayout buffer: the
+// registers go to shared memory in layout L, the operation runs over 2^(K-nt)
+// groups per tile with the outputs written straight back, and the registers
+// are reloaded. Used by the adjoint kernel, whose two register states leave
+// no room for 8- or 16-element groups.
+template <int NT>
+__device__ __forceinline__ void smem_op(double2 (&v)[R], const Addr &A, const RLayout &L,
+                                        double2 *xbuf, const ROp &op, const double2 *pool,
+                                        int cbase_uni, unsigned mat, unsigned long long ident,
+                                        int t) {
+    constexpr int D = 1 << NT;
+    // register positions of the mixing bits (ascending), then their local bits
+    int rp[4] = {0, 1, 2, 3};
+    if (NT == 3) {
+        const int missing = 3 - op.code; // triple_code inverse
+        for (int q = 0, k = 0; q < 4; ++q)
+            if (q != missing) rp[k++] = q;
+    }
+    int lb[NT], sorted[NT];
+#pragma unroll
+    for (int q = 0; q < NT; ++q) sorted[q] = lb[q] = L.reg[rp[q]];
+#pragma unroll
+    for (int a = 0; a < NT; ++a)
+#pragma unroll
+        for (int b = 0; b + 1 < NT - a; ++b)
+            if (sorted[b] > sorted[b + 1]) {
+                const int x = sorted[b];
+                sorted[b] = sorted[b + 1];
+                sorted[b + 1] = x;
+            }
+    int sw_off[D];
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+        int o = 0;
+#pragma unroll
+        for (int q = 0; q < NT; ++q)
+            if (r >> q & 1) o |= 1 << lb[q];
+        sw_off[r] = swz(o);
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) xbuf[slot(A, i)] = v[i];
+    __syncthreads();
+    for (int g = t; g < (TS >> NT); g += T) {
+        int b = g;
+#pragma unroll
+        for (int q = 0; q < NT; ++q) {
+            const int s = sorted[q];
+            b = ((b >> s) << (s + 1)) | (b & ((1 << s) - 1));
+        }
+        int c = cbase_uni;
+        for (int q = 0; q < op.nc; ++q) {
+            const int l = op.ck[q] == 1 ? L.thr[op.cp[q]] : (op.ck[q] == 2 ? L.reg[op.cp[q]] : -1);
+            if (l >= 0) c |= ((b >> l) & 1) << q;
+        }
+        if ((ident >> c) & 1) continue;
+        const double2 *M = pool + mat + c * D * D;
+        const int sb = swz(b);
+        double2 in[D];
+#pragma unroll
+        for (int r = 0; r < D; ++r) in[r] = xbuf[sb ^ sw_off[r]];
+#pragma unroll 1
+        for (int r = 0; r < D; ++r) {
+            double2 acc = cmul(M[r], in[0]);
+#pragma unroll
+            for (int s = 1; s < D; ++s) acc = cfma(M[r + s * D], in[s], acc);
+            xbuf[sb ^ sw_off[r]] = acc;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[i] = xbuf[slot(A, i)];
+    __syncthreads();
+}
+
+template <bool REV>
+__global__ void __launch_bounds__(T, 2)
+    k_regstage(double2 *__restrict__ phi, double2 *__restrict__ psi,
+               double *__restrict__ partial, const __grid_constant__ RParams P) {
+    constexpr int NS = REV ? 2 : 1; // states per tile
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int grp = threadIdx.x / TG;          // tile group: its own tiles, buffers, barrier
-    const int t = threadIdx.x % TG;
-    double2 *stage_buf = reinterpret_cast<double2 *>(smem_raw) + (size_t)grp * 2 * TS;
-    double2 *xbuf = stage_buf + TS;
+    double2 *stage_buf = reinterpret_cast<double2 *>(smem_raw); // NS tiles, cp.async target
+    double2 *xbuf = stage_buf + NS * TS;                          // relayout buffer (one tile)
+    double *pacc = reinterpret_cast<double *>(xbuf + TS);         // [nslots][NW]
+    const int t = threadIdx.x;
+    const int lane = t & 31, warp = t >> 5;
+    if (REV)
+        for (int i = t; i < P.nslots * NW; i += T) pacc[i] = 0;
 
     // natural tile order j = t + T*s: global offset glo | gh(s), slot swz(j)
     unsigned long long glo = 0;
@@ -253,7 +424,7 @@ __global__ void __launch_bounds__(T, 1)
     const int nat_st = swz(t);
     int nat_sw[RB];
 #pragma unroll
-    for (int b = 0; b < RB; ++b) nat_sw[b] = swz(TG << b);
+    for (int b = 0; b < RB; ++b) nat_sw[b] = swz(T << b);
     auto tile_base = [&](unsigned long long c) {
 #pragma unroll
         for (int i = 0; i < K; ++i) {
@@ -274,46 +445,87 @@ __global__ void __launch_bounds__(T, 1)
                     g |= gh[b];
                     sl ^= nat_sw[b];
                 }
-            const unsigned sa = (unsigned)__cvta_generic_to_shared(&stage_buf[sl]);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(&amps[g]));
+#pragma unroll
+            for (int q = 0; q < NS; ++q) {
+                const unsigned sa = (unsigned)__cvta_generic_to_shared(&stage_buf[q * TS + sl]);
+                const double2 *src = (q == 0 ? phi : psi) + g;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src));
+            }
         }
         asm volatile("cp.async.commit_group;\n" ::);
     };
+    auto relayout = [&](double2 (&v)[R], const Addr &A, const Addr &B) {
+#pragma unroll
+        for (int i = 0; i < R; ++i) xbuf[slot(A, i)] = v[i];
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < R; ++i) v[i] = xbuf[slot(B, i)];
+        __syncthreads();
+    };
 
-    const unsigned long long tstride = (unsigned long long)gridDim.x * G;
-    unsigned long long tile = (unsigned long long)blockIdx.x * G + grp;
+    unsigned long long tile = blockIdx.x;
     if (tile < P.ntiles) prefetch(tile);
-    for (; tile < P.ntiles; tile += tstride) {
+    for (; tile < P.ntiles; tile += gridDim.x) {
         const unsigned long long base = tile_base(tile);
         asm volatile("cp.async.wait_group 0;\n" ::);
-        group_sync(grp);
-        double2 v[R];
+        __syncthreads();
+        double2 vf[R], vg[REV ? R : 1];
         Addr A = layout_addr(P.subs[0].L, t);
 #pragma unroll
-        for (int i = 0; i < R; ++i) v[i] = stage_buf[slot(A, i)];
-        group_sync(grp); // staging consumed: refill it with the next tile
-        if (tile + tstride < P.ntiles) prefetch(tile + tstride);
+        for (int i = 0; i < R; ++i) vf[i] = stage_buf[slot(A, i)];
+        if constexpr (REV) {
+#pragma unroll
+            for (int i = 0; i < R; ++i) vg[i] = stage_buf[TS + slot(A, i)];
+        }
+        __syncthreads(); // staging consumed: refill it with the next tile
+        if (tile + gridDim.x < P.ntiles) prefetch(tile + gridDim.x);
         int cur = 0;
         for (int sub = 0; sub < P.nsubs; ++sub) {
             if (sub > 0) {
-#pragma unroll
-                for (int i = 0; i < R; ++i) xbuf[slot(A, i)] = v[i];
-                group_sync(grp);
-                A = layout_addr(P.subs[sub].L, t);
-#pragma unroll
-                for (int i = 0; i < R; ++i) v[i] = xbuf[slot(A, i)];
-                group_sync(grp); // xbuf free for the next relayout
+                const Addr B = layout_addr(P.subs[sub].L, t);
+                relayout(vf, A, B);
+                if constexpr (REV) relayout(vg, A, B);
+                A = B;
                 cur = sub;
             }
             const RSub &sb = P.subs[sub];
             for (int o = 0; o < sb.op_count; ++o) {
                 const ROp &op = P.ops[sb.op_begin + o];
-                int cbase = 0;
+                int cuni = 0, cthr = 0;
                 for (int q = 0; q < op.nc; ++q) {
-                    if (op.ck[q] == 0) cbase |= (int)((base >> op.cp[q]) & 1) << q;
-                    else if (op.ck[q] == 1) cbase |= ((t >> op.cp[q]) & 1) << q;
+                    if (op.ck[q] == 0) cuni |= (int)((base >> op.cp[q]) & 1) << q;
+                    else if (op.ck[q] == 1) cthr |= ((t >> op.cp[q]) & 1) << q;
                 }
-                dispatch(v, op, P.pool, cbase);
+                const int cbase = cuni | cthr;
+                if constexpr (!REV) {
+                    dispatch<2, 4>(vf, op, P.pool, cbase, op.mat, op.ident);
+                } else if (op.np == 0 && op.nt <= 2) {
+                    dispatch<1, 2>(vf, op, P.pool, cbase, op.mat, op.ident);
+                    dispatch<1, 2>(vg, op, P.pool, cbase, op.pair ? op.mat_psi : op.mat,
+                                   op.pair ? op.ident_psi : op.ident);
+                } else if (op.np == 0) {
+                    const RLayout &Lc = P.subs[sub].L;
+                    const unsigned mg = op.pair ? op.mat_psi : op.mat;
+                    const unsigned long long ig = op.pair ? op.ident_psi : op.ident;
+                    if (op.nt == 3) {
+                        smem_op<3>(vf, A, Lc, xbuf, op, P.pool, cuni, op.mat, op.ident, t);
+                        smem_op<3>(vg, A, Lc, xbuf, op, P.pool, cuni, mg, ig, t);
+                    } else {
+                        smem_op<4>(vf, A, Lc, xbuf, op, P.pool, cuni, op.mat, op.ident, t);
+                        smem_op<4>(vg, A, Lc, xbuf, op, P.pool, cuni, mg, ig, t);
+                    }
+                } else {
+                    double acc[VQB_MAX_PARAMS] = {0, 0, 0, 0, 0};
+                    dispatch_param(vf, vg, op, P.pool, cbase, acc);
+#pragma unroll
+                    for (int p = 0; p < VQB_MAX_PARAMS; ++p) {
+                        if (p >= op.np) break;
+                        double x = acc[p];
+#pragma unroll
+                        for (int sh = 16; sh > 0; sh >>= 1) x += __shfl_down_sync(0xffffffffu, x, sh);
+                        if (lane == 0) pacc[(op.slot + p) * NW + warp] += x;
+                    }
+                }
             }
         }
         // store from registers in the final layout
@@ -331,10 +543,30 @@ __global__ void __launch_bounds__(T, 1)
 #pragma unroll
             for (int b = 0; b < RB; ++b)
                 if ((i >> b) & 1) g |= gr[b];
-            amps[g] = v[i];
+            phi[g] = vf[i];
+            if constexpr (REV) psi[g] = vg[i];
         }
     }
     asm volatile("cp.async.wait_group 0;\n" ::);
+    if constexpr (REV) {
+        __syncthreads();
+        for (int s = t; s < P.nslots; s += T) {
+            double x = 0;
+            for (int w = 0; w < NW; ++w) x += pacc[s * NW + w];
+            partial[(size_t)blockIdx.x * P.partial_ld + P.slot_begin + s] = x;
+        }
+    }
+}
+
+// grads[dst[j]] = scale[j] * sum_b partial[b][j] (fixed block order)
+__global__ void k_grads(const double *__restrict__ partial, int nblocks, int ld,
+                        const double *__restrict__ scale, const long long *__restrict__ dst,
+                        int ncols, double *__restrict__ grads) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= ncols) return;
+    double v = 0;
+    for (int b = 0; b < nblocks; ++b) v += partial[(size_t)b * ld + j];
+    grads[dst[j]] = scale[j] * v;
 }
 
 // ---------------------------------------------------------------- host planning
@@ -343,8 +575,7 @@ int pair_code(int a, int b) { // a < b in [0,4)
     return code[a][b];
 }
 int triple_code(int a, int b, int c) {
-    const int missing = 6 - a - b - c; // {0,1,2}->0, {0,1,3}->1, {0,2,3}->2, {1,2,3}->3
-    return 3 - missing;
+    return 3 - (6 - a - b - c); // {0,1,2}->0, {0,1,3}->1, {0,2,3}->2, {1,2,3}->3
 }
 
 // reorder the local bits of a (2^nt x 2^nt) matrix: new bit q = old bit perm[q]
@@ -362,8 +593,8 @@ cvec permute_matrix(const cvec &m, int nt, const int *perm) {
     return out;
 }
 
-// Choose thread bits: thr[0..2] with distinct residues mod 3 (bank-conflict
-// free under swz), preferring local bits 0,1,2.
+// thr[0..2] get distinct residues mod 3 (bank-conflict free under swz),
+// preferring local bits 0,1,2 (coalesced stores).
 void choose_threads(RLayout &L, const std::vector<int> &fb) {
     int lanes[3] = {-1, -1, -1};
     auto used = [&](int b) { return lanes[0] == b || lanes[1] == b || lanes[2] == b; };
@@ -376,7 +607,7 @@ void choose_threads(RLayout &L, const std::vector<int> &fb) {
                     lanes[r] = b;
                     break;
                 }
-    for (int r = 0; r < 3; ++r) // fall back: any unused bit (bank conflicts possible)
+    for (int r = 0; r < 3; ++r)
         if (lanes[r] < 0)
             for (int b : fb)
                 if (!used(b)) {
@@ -389,41 +620,61 @@ void choose_threads(RLayout &L, const std::vector<int> &fb) {
         if (!used(b)) L.thr[k++] = b;
 }
 
-// Lower one stage into its parameter block; false if it does not fit.
-bool lower_stage_reg(const Stage &sg, const std::vector<FusedOp> &blocks, int pn, RParams &P) {
+struct SlotMap {
+    std::vector<double> scale;
+    std::vector<long long> dst;
+};
+
+// Lower as much of a stage's block list as fits one parameter block.
+// `remaining` (block indices, in a valid order) is consumed; what is left
+// must run in a following launch with the same tile bits.
+void lower_stage_reg(const Stage &sg, const std::vector<FusedOp> &blocks,
+                     std::vector<int> &remaining, int pn, bool rev, RParams &P, SlotMap &slots) {
     std::memset(&P, 0, sizeof P);
     for (int j = 0; j < K; ++j) P.bits[j] = sg.bits[j];
     P.ntiles = 1ull << (pn - K);
+    P.slot_begin = (int)slots.scale.size();
     auto local_of = [&](int g) {
         for (int j = 0; j < K; ++j)
             if (sg.bits[j] == g) return j;
         return -1;
     };
-    int nops = 0, npool = 0;
-    std::vector<int> remaining(blocks.size());
-    for (size_t i = 0; i < blocks.size(); ++i) remaining[i] = (int)i;
+    auto mixmask = [&](const FusedOp &f) {
+        unsigned mix = 0;
+        for (int q = 0; q < f.nt; ++q) mix |= 1u << local_of(f.mix[q]);
+        return mix;
+    };
+    auto pool_need = [&](const FusedOp &f) {
+        const int dd = (1 << (2 * f.nt)) << f.nc;
+        return dd * (1 + (f.pair ? 1 : 0) + (rev ? f.np : 0));
+    };
+    int nops = 0, npool = 0, nslots = 0;
     while (!remaining.empty()) {
-        if (P.nsubs >= kMaxSubs) return false;
+        if (P.nsubs >= kMaxSubs) break;
         unsigned rset = 0;
         uint64_t blocked = 0;
         std::vector<int> taken, deferred;
+        int pool_used = 0, ops_used = 0, slots_used = 0;
         for (int i : remaining) {
             const FusedOp &f = blocks[i];
-            unsigned mix = 0;
-            for (int q = 0; q < f.nt; ++q) mix |= 1u << local_of(f.mix[q]);
-            if ((f.support & blocked) || __builtin_popcount(rset | mix) > RB) {
+            const unsigned mix = mixmask(f);
+            const bool fits_res = nops + ops_used < kMaxOps &&
+                                  npool + pool_used + pool_need(f) <= kMaxPool &&
+                                  nslots + slots_used + (rev ? f.np : 0) <= kMaxSlots;
+            if ((f.support & blocked) || __builtin_popcount(rset | mix) > RB || !fits_res) {
                 deferred.push_back(i);
                 blocked |= f.support;
                 continue;
             }
             rset |= mix;
             taken.push_back(i);
+            pool_used += pool_need(f);
+            ++ops_used;
+            slots_used += rev ? f.np : 0;
         }
-        // pad the register set: bits the deferred ops need, then high bits
+        if (taken.empty()) break; // parameter block full: continue in the next launch
         for (int i : deferred) {
-            const FusedOp &f = blocks[i];
-            unsigned mix = 0;
-            for (int q = 0; q < f.nt; ++q) mix |= 1u << local_of(f.mix[q]);
+            const unsigned mix = mixmask(blocks[i]);
             if (__builtin_popcount(rset | mix) <= RB) rset |= mix;
         }
         for (int j = K - 1; j >= 0 && __builtin_popcount(rset) < RB; --j) rset |= 1u << j;
@@ -448,21 +699,19 @@ bool lower_stage_reg(const Stage &sg, const std::vector<FusedOp> &blocks, int pn
         sb.op_begin = nops;
         for (int i : taken) {
             const FusedOp &f = blocks[i];
-            if (nops >= kMaxOps) return false;
             ROp &o = P.ops[nops++];
             o.nt = f.nt;
             o.nc = f.nc;
+            o.np = rev ? f.np : 0;
+            o.pair = f.pair ? 1 : 0;
             int rp[kMaxMix], order[kMaxMix];
             for (int q = 0; q < f.nt; ++q) {
                 rp[q] = reg_of(local_of(f.mix[q]));
                 order[q] = q;
             }
             std::sort(order, order + f.nt, [&](int x, int y) { return rp[x] < rp[y]; });
-            int perm[kMaxMix], srp[kMaxMix];
-            for (int q = 0; q < f.nt; ++q) {
-                perm[q] = order[q];
-                srp[q] = rp[order[q]];
-            }
+            int srp[kMaxMix];
+            for (int q = 0; q < f.nt; ++q) srp[q] = rp[order[q]];
             if (f.nt == 1) o.code = srp[0];
             if (f.nt == 2) o.code = pair_code(srp[0], srp[1]);
             if (f.nt == 3) o.code = triple_code(srp[0], srp[1], srp[2]);
@@ -481,87 +730,190 @@ bool lower_stage_reg(const Stage &sg, const std::vector<FusedOp> &blocks, int pn
                 }
             }
             const int D = 1 << f.nt, dd = D * D;
-            if (npool + (dd << f.nc) > kMaxPool) return false;
-            o.mat = (unsigned)npool;
-            for (int c = 0; c < (1 << f.nc); ++c) {
-                const cvec sub(f.sub_phi.begin() + size_t(c) * dd,
-                               f.sub_phi.begin() + size_t(c + 1) * dd);
-                const cvec pm = f.nt > 1 ? permute_matrix(sub, f.nt, perm) : sub;
-                bool ident = true;
-                for (int r = 0; r < D; ++r)
-                    for (int s = 0; s < D; ++s) {
-                        const cplx x = pm[r + s * D];
-                        if (x != (r == s ? cplx(1) : cplx(0))) ident = false;
-                        if (f.nt <= 2 && x != cplx(0)) o.nz |= 1u << (r + s * D);
-                    }
-                if (ident) o.ident |= 1ull << c;
-                for (const auto &x : pm) P.pool[npool++] = make_double2(x.real(), x.imag());
+            // push 2^nc sub-matrices of `src` (permuted to ascending register
+            // order); returns the pool offset and the identity mask
+            auto push = [&](const cvec &src, size_t first_block, unsigned long long *ident) {
+                const unsigned off = (unsigned)npool;
+                for (int c = 0; c < (1 << f.nc); ++c) {
+                    const cvec sub(src.begin() + (first_block + c) * dd,
+                                   src.begin() + (first_block + c + 1) * dd);
+                    const cvec pm = f.nt > 1 ? permute_matrix(sub, f.nt, order) : sub;
+                    bool id = true;
+                    for (int r = 0; r < D; ++r)
+                        for (int s = 0; s < D; ++s)
+                            if (pm[r + s * D] != (r == s ? cplx(1) : cplx(0))) id = false;
+                    if (ident && id) *ident |= 1ull << c;
+                    for (const auto &x : pm) P.pool[npool++] = make_double2(x.real(), x.imag());
+                }
+                return off;
+            };
+            o.mat = push(f.sub_phi, 0, &o.ident);
+            if (f.pair) o.mat_psi = push(f.sub_psi, 0, &o.ident_psi);
+            if (o.np > 0) {
+                o.mat_d = (unsigned)npool;
+                for (int p = 0; p < f.np; ++p) push(f.sub_d, size_t(p) << f.nc, nullptr);
+                o.ident = 0;
+                o.slot = nslots;
+                for (int p = 0; p < f.np; ++p) {
+                    slots.scale.push_back(f.scale);
+                    slots.dst.push_back(f.grad_base + p);
+                }
+                nslots += f.np;
             }
         }
         sb.op_count = nops - sb.op_begin;
         remaining.swap(deferred);
     }
-    return true;
+    P.nslots = nslots;
 }
 
-} // namespace
-
-bool regstage_available(int pn) { return pn >= K; }
-
-void run_program_fused_smem_stage(DeviceState *s, const std::vector<FusedOp> &fops,
-                                  const Stage &sg);
-
-// Forward program on the register-resident executor. Unfusable ops go
-// through the element-by-element kernels; a stage whose program does not fit
-// the parameter block goes through the shared-memory executor.
-void run_program_reg(DeviceState *s, const std::vector<Gate> &prog) {
-    std::vector<FusedOp> fops;
-    fops.reserve(prog.size());
-    for (const auto &g : prog) fops.push_back(analyse_gate(g));
-    const auto stages = plan_stages(fops, s->pn, K);
-    const char *fq = std::getenv("VQB_FUSE_QUBITS");
-    const int max_support = fq ? std::atoi(fq) : 2;
-    cudaStream_t st = s->stream;
-    const size_t smem = (size_t)G * 2 * TS * sizeof(double2);
-    static bool attr = false;
-    if (!attr) {
-        VQB_CUDA(cudaFuncSetAttribute(k_regstage, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-        attr = true;
+struct DevMem {
+    void *p = nullptr;
+    size_t cap = 0;
+    void ensure(size_t bytes) {
+        if (bytes <= cap) return;
+        if (p) VQB_CUDA(cudaFree(p));
+        VQB_CUDA(cudaMalloc(&p, bytes));
+        cap = bytes;
     }
-    int nsm = 148, dev = 0, per_sm = 1;
-    VQB_CUDA(cudaGetDevice(&dev));
-    VQB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    VQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_regstage, T, smem));
-    static thread_local RParams P; // ~26 KB, host staging of the parameter block
+};
+
+int env_int(const char *name, int dflt) {
+    const char *v = std::getenv(name);
+    return v ? std::atoi(v) : dflt;
+}
+
+template <bool REV> size_t smem_bytes() {
+    return (size_t)((REV ? 2 : 1) + 1) * TS * sizeof(double2) + (REV ? kMaxSlots * NW * 8 : 0);
+}
+
+template <bool REV> int grid_size(unsigned long long ntiles) {
+    static int per_sm = -1, nsm = 148;
+    if (per_sm < 0) {
+        int dev = 0;
+        VQB_CUDA(cudaGetDevice(&dev));
+        VQB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        VQB_CUDA(cudaFuncSetAttribute(k_regstage<REV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem_bytes<REV>()));
+        VQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_regstage<REV>, T,
+                                                               smem_bytes<REV>()));
+        per_sm = std::max(per_sm, 1);
+    }
+    return (int)std::min<unsigned long long>((unsigned long long)nsm * per_sm, ntiles);
+}
+
+// Shared driver: stage planning, block fusion, lowering, launches.
+template <bool REV, typename Fallback>
+void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, double *dgrads,
+             Fallback &&fallback) {
+    const int pn = sphi->pn;
+    cudaStream_t st = sphi->stream;
+    const auto stages = plan_stages(fops, pn, K);
+    const int max_support = env_int("VQB_FUSE_QUBITS", 2);
+    const bool stats = std::getenv("VQB_PLAN_STATS") != nullptr;
+    const unsigned long long ntiles = 1ull << (pn - K);
+    const int grid = grid_size<REV>(ntiles);
+    // gradient slots of the whole sweep: partial[grid][total slots]
+    int total_slots = 0;
+    if (REV)
+        for (const auto &f : fops) total_slots += f.np;
+    static thread_local DevMem m_partial, m_slots;
+    if (REV && total_slots > 0) m_partial.ensure(sizeof(double) * (size_t)grid * total_slots);
+    SlotMap slots;
+    static thread_local RParams P;
     for (const Stage &sg : stages) {
         if (!sg.fused) {
-            apply_gate_fast(s->amps, s->pn, fops[sg.ops[0]].gate, st);
+            fallback(fops[sg.ops[0]]);
             continue;
         }
         std::vector<FusedOp> blocks;
         if (max_support > 0) blocks = fuse_blocks(fops, sg.ops, max_support);
         else
             for (int idx : sg.ops) blocks.push_back(fops[idx]);
-        if (!lower_stage_reg(sg, blocks, s->pn, P)) {
-            run_program_fused_smem_stage(s, fops, sg);
-            continue;
+        std::vector<int> remaining(blocks.size());
+        for (size_t i = 0; i < blocks.size(); ++i) remaining[i] = (int)i;
+        while (!remaining.empty()) {
+            lower_stage_reg(sg, blocks, remaining, pn, REV, P, slots);
+            P.partial_ld = total_slots;
+            if (stats) {
+                int nt_hist[5] = {0, 0, 0, 0, 0}, nops = 0;
+                for (int i = 0; i < P.nsubs; ++i) nops += P.subs[i].op_count;
+                for (int i = 0; i < nops; ++i) nt_hist[std::min(P.ops[i].nt, 4)]++;
+                std::fprintf(stderr, "[regstage%s] gates %zu blocks %zu subs %d ops nt0..4 %d %d %d %d %d slots %d\n",
+                             REV ? "-rev" : "", sg.ops.size(), blocks.size(), P.nsubs, nt_hist[0],
+                             nt_hist[1], nt_hist[2], nt_hist[3], nt_hist[4], P.nslots);
+            }
+            {
+                // algorithmic FP64 flops of this launch: a dense 2^nt x 2^nt
+                // complex matrix costs 8 * 2^nt flops per amplitude per state;
+                // a parametric step adds the np derivative contractions
+                double per_amp = 0;
+                int nops = 0;
+                for (int i = 0; i < P.nsubs; ++i) nops += P.subs[i].op_count;
+                for (int i = 0; i < nops; ++i) {
+                    const ROp &o = P.ops[i];
+                    const double mv = o.nt == 0 ? 6.0 : 8.0 * (1 << o.nt);
+                    per_amp += (REV ? 2.0 : 1.0) * mv + (REV ? o.np * (mv + 2.0) : 0.0);
+                }
+                note_flops(per_amp * double(1ull << pn));
+            }
+            const ProfMark pf_ = prof_begin(st);
+            k_regstage<REV><<<grid, T, smem_bytes<REV>(), st>>>(
+                sphi->amps, REV ? spsi->amps : nullptr, static_cast<double *>(m_partial.p), P);
+            check_launch(REV ? "k_regstage_rev" : "k_regstage", pf_);
         }
-        if (std::getenv("VQB_PLAN_STATS")) {
-            int nt_hist[5] = {0, 0, 0, 0, 0}, nops = 0;
-            for (int i = 0; i < P.nsubs; ++i) nops += P.subs[i].op_count;
-            for (int i = 0; i < nops; ++i) nt_hist[std::min(P.ops[i].nt, 4)]++;
-            std::fprintf(stderr, "[regstage] gates %zu blocks %zu subs %d ops nt0..4 %d %d %d %d %d\n",
-                         sg.ops.size(), blocks.size(), P.nsubs, nt_hist[0], nt_hist[1], nt_hist[2],
-                         nt_hist[3], nt_hist[4]);
-        }
-        const int grid = (int)std::min<unsigned long long>((unsigned long long)nsm * std::max(per_sm, 1),
-                                                           (P.ntiles + G - 1) / G);
-        const ProfMark pf_ = prof_begin(st);
-        k_regstage<<<grid, T, smem, st>>>(s->amps, P);
-        check_launch("k_regstage", pf_);
     }
-    VQB_CUDA(cudaStreamSynchronize(st));
+    if (REV && total_slots > 0) {
+        if ((int)slots.scale.size() != total_slots) raise(VQB_ERR_INTERNAL, "gradient slot mismatch");
+        m_slots.ensure((sizeof(double) + sizeof(long long)) * total_slots);
+        VQB_CUDA(cudaMemcpyAsync(m_slots.p, slots.scale.data(), sizeof(double) * total_slots,
+                                 cudaMemcpyHostToDevice, st));
+        VQB_CUDA(cudaMemcpyAsync(static_cast<char *>(m_slots.p) + sizeof(double) * total_slots,
+                                 slots.dst.data(), sizeof(long long) * total_slots,
+                                 cudaMemcpyHostToDevice, st));
+        const ProfMark pf_ = prof_begin(st);
+        k_grads<<<(total_slots + 127) / 128, 128, 0, st>>>(
+            static_cast<const double *>(m_partial.p), grid, total_slots,
+            static_cast<const double *>(m_slots.p),
+            reinterpret_cast<const long long *>(static_cast<char *>(m_slots.p) +
+                                                sizeof(double) * total_slots),
+            total_slots, dgrads);
+        check_launch("k_grads", pf_);
+    }
+    VQB_CUDA(cudaStreamSynchronize(st)); // host-side slot vectors outlive the copies
+}
+
+} // namespace
+
+bool regstage_available(int pn) { return pn >= K + 2; }
+
+void run_program_reg(DeviceState *s, const std::vector<Gate> &prog) {
+    std::vector<FusedOp> fops;
+    fops.reserve(prog.size());
+    for (const auto &g : prog) fops.push_back(analyse_gate(g));
+    run_reg<false>(s, nullptr, fops, nullptr, [&](const FusedOp &f) {
+        apply_gate_fast(s->amps, s->pn, f.gate, s->stream);
+    });
+}
+
+void run_reverse_reg(DeviceState *phi, DeviceState *psi, const std::vector<RevOp> &prog,
+                     double *dgrads) {
+    std::vector<FusedOp> fops;
+    fops.reserve(prog.size());
+    for (const auto &r : prog) {
+        fops.push_back(analyse_rev(r));
+        if (fops.back().np > 0 && fops.back().nt > 2) fops.back().fusable = false;
+    }
+    run_reg<true>(phi, psi, fops, dgrads, [&](const FusedOp &f) {
+        const RevOp &r = *f.rev;
+        if (r.dmats.empty()) {
+            apply_gate_fast(phi->amps, phi->pn, r.phi_op, phi->stream);
+            apply_gate_fast(psi->amps, psi->pn, r.psi_op, phi->stream);
+        } else {
+            reverse_step_async(phi->amps, psi->amps, phi->pn, r.phi_op.pos, r.phi_op.m,
+                               r.phi_op.mat, r.dmats, phi, nullptr, dgrads + r.grad_base, r.scale);
+        }
+    });
 }
 
 } // namespace vqb

@@ -73,6 +73,9 @@ class Engine:
     def launch_count(self) -> int:
         return int(self._fn("kernel_launch_count")())
 
+    def flop_count(self) -> float:
+        return float(self._fn("flop_count")())
+
     def profile_begin(self) -> None:
         self.check(self._fn("profile_begin")())
 

@@ -119,9 +119,9 @@ def test_multi_param_gates(dev, ref):
     assert rel_err(g, rg) <= RTOL
 
 
-def test_random_circuit_gradient(dev, ref):
-    rng = np.random.default_rng(77)
-    n = 10
+@pytest.mark.parametrize("n", [10, 15])
+def test_random_circuit_gradient(dev, ref, n):
+    rng = np.random.default_rng(77 + n)
     c = Circuit([random_gate(n, rng, active=True) for _ in range(120)])
     op = random_operator(n, 8, rng)
     amps = random_state(n, rng)
@@ -189,3 +189,24 @@ def test_config0_full_gradient_and_rqc_roundtrip(dev):
     s = dev.pure_state(28)
     dev.apply_circuit(w.circuit, s)
     assert abs(dev.norm(s) - 1.0) <= 1e-10
+
+
+@pytest.mark.parametrize("executor", ["reg", "smem"])
+def test_executors_agree_on_adjoint(dev, ref, monkeypatch, executor):
+    """Both fused executors (register-resident and shared-memory) on the
+    three gradient workloads at sizes where the register executor applies."""
+    monkeypatch.setenv("VQB_EXECUTOR", executor)
+    w = circuits.config2(n=14, p=2)
+    loss, g = dev.gradient_pure(w.observable, w.circuit, dev.pure_state(14))
+    rloss, rg = ref.gradient_pure(w.observable, w.circuit, ref.pure_state(14))
+    assert abs(loss - rloss) <= RTOL * abs(rloss) and rel_err(g, rg) <= RTOL
+    w = circuits.config3(n=7, layers=2)
+    loss, g = dev.gradient_mixed(w.observable, w.circuit, dev.mixed_state(7))
+    rloss, rg = ref.gradient_mixed(w.observable, w.circuit, ref.mixed_state(7))
+    assert abs(loss - rloss) <= RTOL * abs(rloss) and rel_err(g, rg) <= RTOL
+    w = circuits.config1(rows=3, cols=5, cycles=12)
+    s = dev.pure_state(15)
+    dev.apply_circuit(w.circuit, s)
+    r = ref.pure_state(15)
+    ref.apply_circuit(w.circuit, r)
+    assert np.max(np.abs(dev.download(s) - ref.download(r))) <= 1e-12
