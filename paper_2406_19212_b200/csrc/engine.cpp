@@ -1,6 +1,9 @@
 // Lowering of circuits to gate programs and the element-by-element executor.
 #include "engine.hpp"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace vqb {
 
 std::vector<Element> build_elements(const vqb_op *ops, int64_t count) {
@@ -133,6 +136,115 @@ std::vector<RevOp> mixed_reverse_program(const std::vector<Element> &es, int n,
     return prog;
 }
 
+namespace {
+
+// Matrix over positions P (1-based) embedded into the sorted union U.
+cvec embed_into(const cvec &M, const int *P, int m, const std::vector<int> &U) {
+    const int u = (int)U.size(), du = 1 << u, dp = 1 << m;
+    int where[VQB_MAX_POSITIONS];
+    int pmask = 0;
+    for (int i = 0; i < m; ++i) {
+        where[i] = (int)(std::find(U.begin(), U.end(), P[i]) - U.begin());
+        pmask |= 1 << where[i];
+    }
+    cvec out(size_t(du) * du);
+    for (int c = 0; c < du; ++c)
+        for (int r = 0; r < du; ++r) {
+            if ((r & ~pmask) != (c & ~pmask)) continue;
+            int rp = 0, cp = 0;
+            for (int i = 0; i < m; ++i) {
+                rp |= ((r >> where[i]) & 1) << i;
+                cp |= ((c >> where[i]) & 1) << i;
+            }
+            out[r + size_t(c) * du] = M[rp + size_t(cp) * dp];
+        }
+    return out;
+}
+
+std::vector<int> union_of(const Gate &a, const Gate &b) {
+    std::vector<int> u(a.pos, a.pos + a.m);
+    for (int i = 0; i < b.m; ++i)
+        if (std::find(u.begin(), u.end(), b.pos[i]) == u.end()) u.push_back(b.pos[i]);
+    std::sort(u.begin(), u.end());
+    return u;
+}
+
+bool overlaps(const Gate &a, const Gate &b) {
+    for (int i = 0; i < a.m; ++i)
+        for (int j = 0; j < b.m; ++j)
+            if (a.pos[i] == b.pos[j]) return true;
+    return false;
+}
+
+Gate on_union(const std::vector<int> &U, cvec mat) {
+    Gate g;
+    g.kind = VQB_GATE_GENERIC;
+    g.m = (int)U.size();
+    for (int i = 0; i < g.m; ++i) g.pos[i] = U[i];
+    g.mat = std::move(mat);
+    return g;
+}
+
+// A unitary non-parametric step (same matrix on both states) may be folded
+// into an adjacent parametric step when their supports overlap and the union
+// has at most two qubits.
+bool foldable(const RevOp &x, const RevOp &p) {
+    return x.dmats.empty() && x.phi_op.mat == x.psi_op.mat && overlaps(x.phi_op, p.phi_op) &&
+           union_of(x.phi_op, p.phi_op).size() <= 2;
+}
+
+} // namespace
+
+// Reverse-program rewrite: [A][P][B] -> [P'] with inv' = B inv A and
+// D'_p = A^dag D_p B^dag (A, B unitary). Same gradient contributions
+// (acc = <A psi| D |inv A phi> = <psi| A^dag D B^dag |B inv A phi>), fewer
+// passes over the two states. Applied to both the pure and the mixed sweep
+// (where A, B are the ket/bra halves of unitary gates; channel steps, whose
+// phi and psi matrices differ, are never folded).
+std::vector<RevOp> fold_reverse_program(const std::vector<RevOp> &prog) {
+    std::vector<RevOp> out;
+    out.reserve(prog.size());
+    for (const RevOp &r : prog) {
+        if (!r.dmats.empty() && !out.empty() && foldable(out.back(), r)) {
+            // A = out.back() runs before P: inv' = inv A, D' = A^dag D
+            const RevOp A = out.back();
+            out.pop_back();
+            const std::vector<int> U = union_of(A.phi_op, r.phi_op);
+            const int d = 1 << (int)U.size();
+            const cvec a = embed_into(A.phi_op.mat, A.phi_op.pos, A.phi_op.m, U);
+            const cvec adag = adjoint(a, d);
+            RevOp m;
+            m.phi_op = on_union(U, matmul(embed_into(r.phi_op.mat, r.phi_op.pos, r.phi_op.m, U), a, d));
+            m.psi_op = m.phi_op;
+            for (const auto &dm : r.dmats)
+                m.dmats.push_back(matmul(adag, embed_into(dm, r.phi_op.pos, r.phi_op.m, U), d));
+            m.grad_base = r.grad_base;
+            m.scale = r.scale;
+            out.push_back(std::move(m));
+            continue;
+        }
+        if (r.dmats.empty() && !out.empty() && !out.back().dmats.empty() && foldable(r, out.back())) {
+            // B = r runs after P: inv' = B inv, D' = D B^dag
+            RevOp &p = out.back();
+            const std::vector<int> U = union_of(r.phi_op, p.phi_op);
+            const int d = 1 << (int)U.size();
+            const cvec b = embed_into(r.phi_op.mat, r.phi_op.pos, r.phi_op.m, U);
+            const cvec bdag = adjoint(b, d);
+            const Gate inv = on_union(U, matmul(b, embed_into(p.phi_op.mat, p.phi_op.pos,
+                                                              p.phi_op.m, U), d));
+            std::vector<cvec> dm;
+            for (const auto &x : p.dmats)
+                dm.push_back(matmul(embed_into(x, p.phi_op.pos, p.phi_op.m, U), bdag, d));
+            p.phi_op = inv;
+            p.psi_op = inv;
+            p.dmats = std::move(dm);
+            continue;
+        }
+        out.push_back(r);
+    }
+    return out;
+}
+
 void run_program(DeviceState *s, const std::vector<Gate> &prog, bool fused) {
     if (fused) {
         run_program_fused(s, prog);
@@ -144,7 +256,13 @@ void run_program(DeviceState *s, const std::vector<Gate> &prog, bool fused) {
 void run_reverse(DeviceState *phi, DeviceState *psi, const std::vector<RevOp> &prog,
                  double *dgrads, bool fused) {
     if (fused) {
-        run_reverse_fused(phi, psi, prog, dgrads);
+        const char *nf = std::getenv("VQB_NO_FOLD");
+        if (nf && *nf == '1') {
+            run_reverse_fused(phi, psi, prog, dgrads);
+        } else {
+            const std::vector<RevOp> folded = fold_reverse_program(prog);
+            run_reverse_fused(phi, psi, folded, dgrads);
+        }
         return;
     }
     for (const auto &r : prog) {

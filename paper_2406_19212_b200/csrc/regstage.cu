@@ -51,7 +51,8 @@ constexpr int TS = 1 << K;  // tile size
 constexpr int kMaxSubs = 32;
 constexpr int kMaxOps = 56;
 constexpr int kMaxSlots = 64;
-constexpr int kMaxPool = 1280; // double2 entries
+constexpr int kMaxPool = 1088; // double2 entries
+constexpr int kMaxTab = 192;   // per-element diagonal tables, copied to shared memory
 
 struct RLayout {
     int reg[RB]; // tile-local bit of register bit b
@@ -68,6 +69,8 @@ struct ROp {
     int cp[kMaxCond];     // global bit / thread bit / register bit
     unsigned mat, mat_psi, mat_d; // pool offsets (2^nc sub-matrices each, ascending order)
     unsigned long long ident, ident_psi;
+    int rw[RB];           // condition-index bits contributed by register bit b
+    int tab, tab_psi;     // nt = 0 with register conditions: shared-memory tables
 };
 
 struct RSub {
@@ -82,6 +85,8 @@ struct RParams {
     RSub subs[kMaxSubs];
     ROp ops[kMaxOps];
     double2 pool[kMaxPool];
+    double2 tab[kMaxTab];
+    int ntab;
 };
 static_assert(sizeof(RParams) <= 32000, "kernel parameter block too large");
 
@@ -125,11 +130,13 @@ __device__ __forceinline__ int slot(const Addr &a, int i) {
     return s;
 }
 
+// condition value of register element i (a compile-time constant in the
+// unrolled loops): the per-register-bit masks are ORed in
 __device__ __forceinline__ int cond_of(const ROp &op, int cbase, int i) {
     int c = cbase;
 #pragma unroll
-    for (int q = 0; q < kMaxCond; ++q)
-        if (q < op.nc && op.ck[q] == 2) c |= ((i >> op.cp[q]) & 1) << q;
+    for (int b = 0; b < RB; ++b)
+        if ((i >> b) & 1) c |= op.rw[b];
     return c;
 }
 
@@ -146,6 +153,16 @@ template <int NT, int P0, int P1, int P2, int P3> struct Pos {
         return o;
     }
 };
+
+// select entry c (< 4) of a register table with predicated moves (no
+// divergent constant-cache loads)
+__device__ __forceinline__ double2 sel4(const double2 (&t)[4], int c) {
+    double2 r = t[0];
+    if (c == 1) r = t[1];
+    if (c == 2) r = t[2];
+    if (c == 3) r = t[3];
+    return r;
+}
 
 // out = M * v[group], written back in place; M read element by element.
 template <class PS>
@@ -198,6 +215,22 @@ __device__ __forceinline__ void param_r(double2 (&vf)[R], double2 (&vg)[R], cons
     using PS = Pos<NT, P0, P1, P2, P3>;
     constexpr int D = PS::D;
     const int nsub = 1 << op.nc;
+    if (NT == 0 && op.per_group && op.np == 1 && op.tab >= 0) {
+        // diagonal step with per-element conditions: tables in shared memory
+        // (the first kMaxTab entries of the dynamic shared memory)
+        extern __shared__ __align__(16) unsigned char smem_raw[];
+        const double2 *stab = reinterpret_cast<const double2 *>(smem_raw);
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            const int c = cond_of(op, cbase, i);
+            const double2 m = stab[op.tab + c], d = stab[op.tab + nsub + c];
+            const double2 w = cmul(m, vf[i]);
+            vf[i] = w;
+            acc[0] += re_cj(vg[i], cmul(d, w));
+            vg[i] = cmul(m, vg[i]);
+        }
+        return;
+    }
     if (NT <= 1 && !op.per_group && op.np == 1) {
         double2 m[D * D], d[D * D];
 #pragma unroll
@@ -252,6 +285,15 @@ __device__ __forceinline__ void apply_diag(double2 (&v)[R], const ROp &op, const
         const double2 ph = pool[mat + cbase];
 #pragma unroll
         for (int i = 0; i < R; ++i) v[i] = cmul(ph, v[i]);
+        return;
+    }
+    const int tabo = mat == op.mat ? op.tab : op.tab_psi;
+    if (tabo >= 0) {
+        // per-element phase from the shared-memory copy of the table
+        extern __shared__ __align__(16) unsigned char smem_raw[];
+        const double2 *stab = reinterpret_cast<const double2 *>(smem_raw) + tabo;
+#pragma unroll
+        for (int i = 0; i < R; ++i) v[i] = cmul(stab[cond_of(op, cbase, i)], v[i]);
         return;
     }
 #pragma unroll
@@ -405,13 +447,17 @@ __global__ void __launch_bounds__(T, 2)
                double *__restrict__ partial, const __grid_constant__ RParams P) {
     constexpr int NS = REV ? 2 : 1; // states per tile
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2 *stage_buf = reinterpret_cast<double2 *>(smem_raw); // NS tiles, cp.async target
-    double2 *xbuf = stage_buf + NS * TS;                          // relayout buffer (one tile)
-    double *pacc = reinterpret_cast<double *>(xbuf + TS);         // [nslots][NW]
+    // layout: diagonal tables | NS staging tiles (cp.async target) | relayout tile | slots
+    double2 *stab = reinterpret_cast<double2 *>(smem_raw);
+    double2 *stage_buf = stab + kMaxTab;
+    double2 *xbuf = stage_buf + NS * TS;
+    double *pacc = reinterpret_cast<double *>(xbuf + TS); // [nslots][NW]
     const int t = threadIdx.x;
     const int lane = t & 31, warp = t >> 5;
     if (REV)
         for (int i = t; i < P.nslots * NW; i += T) pacc[i] = 0;
+    for (int i = t; i < P.ntab; i += T) stab[i] = P.tab[i];
+    __syncthreads();
 
     // natural tile order j = t + T*s: global offset glo | gh(s), slot swz(j)
     unsigned long long glo = 0;
@@ -760,6 +806,27 @@ void lower_stage_reg(const Stage &sg, const std::vector<FusedOp> &blocks,
                 }
                 nslots += f.np;
             }
+            // per-register-bit condition masks
+            for (int q = 0; q < f.nc; ++q)
+                if (o.ck[q] == 2) o.rw[o.cp[q]] |= 1 << q;
+            // diagonal steps with register-bit conditions read their tables
+            // from shared memory (phi table, [D table for a parametric step])
+            o.tab = o.tab_psi = -1;
+            const int nsub = 1 << f.nc;
+            auto push_tab = [&](const cvec &src, size_t first) {
+                const int off = P.ntab;
+                for (int c = 0; c < nsub; ++c)
+                    P.tab[P.ntab++] = make_double2(src[first + c].real(), src[first + c].imag());
+                return off;
+            };
+            if (f.nt == 0 && o.per_group) {
+                const int need = nsub * (1 + (f.pair ? 1 : 0) + (o.np == 1 ? 1 : 0));
+                if (P.ntab + need <= kMaxTab && o.np <= 1) {
+                    o.tab = push_tab(f.sub_phi, 0);
+                    if (o.np == 1) push_tab(f.sub_d, 0); // at o.tab + nsub
+                    if (f.pair) o.tab_psi = push_tab(f.sub_psi, 0);
+                }
+            }
         }
         sb.op_count = nops - sb.op_begin;
         remaining.swap(deferred);
@@ -784,7 +851,8 @@ int env_int(const char *name, int dflt) {
 }
 
 template <bool REV> size_t smem_bytes() {
-    return (size_t)((REV ? 2 : 1) + 1) * TS * sizeof(double2) + (REV ? kMaxSlots * NW * 8 : 0);
+    return (size_t)kMaxTab * sizeof(double2) + (size_t)((REV ? 2 : 1) + 1) * TS * sizeof(double2) +
+           (REV ? kMaxSlots * NW * 8 : 0);
 }
 
 template <bool REV> int grid_size(unsigned long long ntiles) {
