@@ -71,6 +71,7 @@ struct ROp {
     unsigned long long ident, ident_psi;
     int rw[RB];           // condition-index bits contributed by register bit b
     int tab, tab_psi;     // nt = 0 with register conditions: shared-memory tables
+    int xoff, nx;         // nt >= 3: XOR patterns of the diagonal-times-permutation terms
 };
 
 struct RSub {
@@ -86,7 +87,8 @@ struct RParams {
     ROp ops[kMaxOps];
     double2 pool[kMaxPool];
     double2 tab[kMaxTab];
-    int ntab;
+    int ntab, nxpat;
+    unsigned char xpat[256];
 };
 static_assert(sizeof(RParams) <= 32000, "kernel parameter block too large");
 
@@ -376,7 +378,7 @@ template <int NT>
 __device__ __forceinline__ void smem_op(double2 (&v)[R], const Addr &A, const RLayout &L,
                                         double2 *xbuf, const ROp &op, const double2 *pool,
                                         int cbase_uni, unsigned mat, unsigned long long ident,
-                                        int t) {
+                                        int t, const unsigned char *P_xpat) {
     constexpr int D = 1 << NT;
     // register positions of the mixing bits (ascending), then their local bits
     int rp[4] = {0, 1, 2, 3};
@@ -422,18 +424,26 @@ __device__ __forceinline__ void smem_op(double2 (&v)[R], const Addr &A, const RL
             if (l >= 0) c |= ((b >> l) & 1) << q;
         }
         if ((ident >> c) & 1) continue;
-        const double2 *M = pool + mat + c * D * D;
+        // S = sum_k diag(d_k) P_{x_k}: out[r] = sum_k d_k[r] in[r ^ x_k]; the
+        // swizzle is XOR-linear, so slot(r ^ x) = slot(r) ^ slot(x)
+        const double2 *Mc = pool + mat + c * op.nx * D;
         const int sb = swz(b);
-        double2 in[D];
+        double2 out[D];
 #pragma unroll
-        for (int r = 0; r < D; ++r) in[r] = xbuf[sb ^ sw_off[r]];
-#pragma unroll 1
-        for (int r = 0; r < D; ++r) {
-            double2 acc = cmul(M[r], in[0]);
+        for (int r = 0; r < D; ++r) out[r] = make_double2(0, 0);
+        for (int k = 0; k < op.nx; ++k) {
+            const int x = P_xpat[op.xoff + k];
+            int sx = 0;
 #pragma unroll
-            for (int s = 1; s < D; ++s) acc = cfma(M[r + s * D], in[s], acc);
-            xbuf[sb ^ sw_off[r]] = acc;
+            for (int q = 0; q < NT; ++q)
+                if ((x >> q) & 1) sx ^= sw_off[1 << q];
+            const double2 *dk = Mc + k * D;
+#pragma unroll
+            for (int r = 0; r < D; ++r) out[r] = cfma(dk[r], xbuf[sb ^ sw_off[r] ^ sx], out[r]);
         }
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < D; ++r) xbuf[sb ^ sw_off[r]] = out[r];
     }
     __syncthreads();
 #pragma unroll
@@ -441,8 +451,9 @@ __device__ __forceinline__ void smem_op(double2 (&v)[R], const Addr &A, const RL
     __syncthreads();
 }
 
-template <bool REV>
-__global__ void __launch_bounds__(T, 2)
+// WIDE = false: forward stages without nt >= 3 operations (leaner registers)
+template <bool REV, bool WIDE = true>
+__global__ void __launch_bounds__(T, (!REV && !WIDE) ? 3 : 2)
     k_regstage(double2 *__restrict__ phi, double2 *__restrict__ psi,
                double *__restrict__ partial, const __grid_constant__ RParams P) {
     constexpr int NS = REV ? 2 : 1; // states per tile
@@ -544,7 +555,15 @@ __global__ void __launch_bounds__(T, 2)
                 }
                 const int cbase = cuni | cthr;
                 if constexpr (!REV) {
-                    dispatch<2, 4>(vf, op, P.pool, cbase, op.mat, op.ident);
+                    if (!WIDE || op.nt <= 2) {
+                        dispatch<2, 2>(vf, op, P.pool, cbase, op.mat, op.ident);
+                    } else if (op.nt == 3) {
+                        smem_op<3>(vf, A, P.subs[sub].L, xbuf, op, P.pool, cuni, op.mat, op.ident, t,
+                                   P.xpat);
+                    } else {
+                        smem_op<4>(vf, A, P.subs[sub].L, xbuf, op, P.pool, cuni, op.mat, op.ident, t,
+                                   P.xpat);
+                    }
                 } else if (op.np == 0 && op.nt <= 2) {
                     dispatch<1, 2>(vf, op, P.pool, cbase, op.mat, op.ident);
                     dispatch<1, 2>(vg, op, P.pool, cbase, op.pair ? op.mat_psi : op.mat,
@@ -554,11 +573,11 @@ __global__ void __launch_bounds__(T, 2)
                     const unsigned mg = op.pair ? op.mat_psi : op.mat;
                     const unsigned long long ig = op.pair ? op.ident_psi : op.ident;
                     if (op.nt == 3) {
-                        smem_op<3>(vf, A, Lc, xbuf, op, P.pool, cuni, op.mat, op.ident, t);
-                        smem_op<3>(vg, A, Lc, xbuf, op, P.pool, cuni, mg, ig, t);
+                        smem_op<3>(vf, A, Lc, xbuf, op, P.pool, cuni, op.mat, op.ident, t, P.xpat);
+                        smem_op<3>(vg, A, Lc, xbuf, op, P.pool, cuni, mg, ig, t, P.xpat);
                     } else {
-                        smem_op<4>(vf, A, Lc, xbuf, op, P.pool, cuni, op.mat, op.ident, t);
-                        smem_op<4>(vg, A, Lc, xbuf, op, P.pool, cuni, mg, ig, t);
+                        smem_op<4>(vf, A, Lc, xbuf, op, P.pool, cuni, op.mat, op.ident, t, P.xpat);
+                        smem_op<4>(vg, A, Lc, xbuf, op, P.pool, cuni, mg, ig, t, P.xpat);
                     }
                 } else {
                     double acc[VQB_MAX_PARAMS] = {0, 0, 0, 0, 0};
@@ -690,7 +709,23 @@ void lower_stage_reg(const Stage &sg, const std::vector<FusedOp> &blocks,
         for (int q = 0; q < f.nt; ++q) mix |= 1u << local_of(f.mix[q]);
         return mix;
     };
+    auto count_x = [&](const FusedOp &f) { // XOR patterns of a wide op
+        if (f.nt < 3) return 0;
+        const int D = 1 << f.nt, dd = D * D;
+        int nx = 0;
+        for (int x = 0; x < D; ++x) {
+            bool any = false;
+            for (int c = 0; c < (1 << f.nc) && !any; ++c)
+                for (int r = 0; r < D && !any; ++r)
+                    any = f.sub_phi[size_t(c) * dd + r + size_t(r ^ x) * D] != cplx(0) ||
+                          (f.pair && f.sub_psi[size_t(c) * dd + r + size_t(r ^ x) * D] != cplx(0));
+            nx += any ? 1 : 0;
+        }
+        return nx;
+    };
     auto pool_need = [&](const FusedOp &f) {
+        if (f.nt >= 3) // XOR-term form: |X| * D entries per sub-matrix
+            return (count_x(f) * (1 << f.nt) << f.nc) * (1 + (f.pair ? 1 : 0));
         const int dd = (1 << (2 * f.nt)) << f.nc;
         return dd * (1 + (f.pair ? 1 : 0) + (rev ? f.np : 0));
     };
@@ -700,13 +735,15 @@ void lower_stage_reg(const Stage &sg, const std::vector<FusedOp> &blocks,
         unsigned rset = 0;
         uint64_t blocked = 0;
         std::vector<int> taken, deferred;
-        int pool_used = 0, ops_used = 0, slots_used = 0;
+        int pool_used = 0, ops_used = 0, slots_used = 0, xp_used = 0;
         for (int i : remaining) {
             const FusedOp &f = blocks[i];
             const unsigned mix = mixmask(f);
+            const int nx = count_x(f);
             const bool fits_res = nops + ops_used < kMaxOps &&
                                   npool + pool_used + pool_need(f) <= kMaxPool &&
-                                  nslots + slots_used + (rev ? f.np : 0) <= kMaxSlots;
+                                  nslots + slots_used + (rev ? f.np : 0) <= kMaxSlots &&
+                                  P.nxpat + xp_used + nx <= 256;
             if ((f.support & blocked) || __builtin_popcount(rset | mix) > RB || !fits_res) {
                 deferred.push_back(i);
                 blocked |= f.support;
@@ -715,6 +752,7 @@ void lower_stage_reg(const Stage &sg, const std::vector<FusedOp> &blocks,
             rset |= mix;
             taken.push_back(i);
             pool_used += pool_need(f);
+            xp_used += nx;
             ++ops_used;
             slots_used += rev ? f.np : 0;
         }
@@ -793,8 +831,56 @@ void lower_stage_reg(const Stage &sg, const std::vector<FusedOp> &blocks,
                 }
                 return off;
             };
-            o.mat = push(f.sub_phi, 0, &o.ident);
-            if (f.pair) o.mat_psi = push(f.sub_psi, 0, &o.ident_psi);
+            if (f.nt >= 3) {
+                // wide ops run in smem_op as sum_k diag(d_k) P_{x_k}: store the
+                // XOR patterns x_k and, per sub-matrix, d_k[r] = S[r, r ^ x_k]
+                auto permuted = [&](const cvec &src, int c) {
+                    const cvec sub(src.begin() + size_t(c) * dd, src.begin() + size_t(c + 1) * dd);
+                    return permute_matrix(sub, f.nt, order);
+                };
+                std::vector<int> X;
+                auto scan = [&](const cvec &src) {
+                    for (int c = 0; c < (1 << f.nc); ++c) {
+                        const cvec pm = permuted(src, c);
+                        for (int x = 0; x < D; ++x) {
+                            if (std::find(X.begin(), X.end(), x) != X.end()) continue;
+                            for (int r = 0; r < D; ++r)
+                                if (pm[r + size_t(r ^ x) * D] != cplx(0)) {
+                                    X.push_back(x);
+                                    break;
+                                }
+                        }
+                    }
+                };
+                scan(f.sub_phi);
+                if (f.pair) scan(f.sub_psi);
+                std::sort(X.begin(), X.end());
+                o.xoff = P.nxpat;
+                o.nx = (int)X.size();
+                for (int x : X) P.xpat[P.nxpat++] = (unsigned char)x;
+                auto pushx = [&](const cvec &src, unsigned long long *ident) {
+                    const unsigned off = (unsigned)npool;
+                    for (int c = 0; c < (1 << f.nc); ++c) {
+                        const cvec pm = permuted(src, c);
+                        bool id = true;
+                        for (int r = 0; r < D; ++r)
+                            for (int s = 0; s < D; ++s)
+                                if (pm[r + s * D] != (r == s ? cplx(1) : cplx(0))) id = false;
+                        if (id) *ident |= 1ull << c;
+                        for (int x : X)
+                            for (int r = 0; r < D; ++r) {
+                                const cplx v = pm[r + size_t(r ^ x) * D];
+                                P.pool[npool++] = make_double2(v.real(), v.imag());
+                            }
+                    }
+                    return off;
+                };
+                o.mat = pushx(f.sub_phi, &o.ident);
+                if (f.pair) o.mat_psi = pushx(f.sub_psi, &o.ident_psi);
+            } else {
+                o.mat = push(f.sub_phi, 0, &o.ident);
+                if (f.pair) o.mat_psi = push(f.sub_psi, 0, &o.ident_psi);
+            }
             if (o.np > 0) {
                 o.mat_d = (unsigned)npool;
                 for (int p = 0; p < f.np; ++p) push(f.sub_d, size_t(p) << f.nc, nullptr);
@@ -855,15 +941,16 @@ template <bool REV> size_t smem_bytes() {
            (REV ? kMaxSlots * NW * 8 : 0);
 }
 
-template <bool REV> int grid_size(unsigned long long ntiles) {
+template <bool REV, bool WIDE> int grid_size(unsigned long long ntiles) {
     static int per_sm = -1, nsm = 148;
     if (per_sm < 0) {
         int dev = 0;
         VQB_CUDA(cudaGetDevice(&dev));
         VQB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        VQB_CUDA(cudaFuncSetAttribute(k_regstage<REV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        VQB_CUDA(cudaFuncSetAttribute(k_regstage<REV, WIDE>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem_bytes<REV>()));
-        VQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_regstage<REV>, T,
+        VQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_regstage<REV, WIDE>, T,
                                                                smem_bytes<REV>()));
         per_sm = std::max(per_sm, 1);
     }
@@ -880,7 +967,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
     const int max_support = env_int("VQB_FUSE_QUBITS", 2);
     const bool stats = std::getenv("VQB_PLAN_STATS") != nullptr;
     const unsigned long long ntiles = 1ull << (pn - K);
-    const int grid = grid_size<REV>(ntiles);
+    const int grid = grid_size<REV, true>(ntiles);
     // gradient slots of the whole sweep: partial[grid][total slots]
     int total_slots = 0;
     if (REV)
@@ -925,9 +1012,18 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
                 }
                 note_flops(per_amp * double(1ull << pn));
             }
+            bool wide = REV;
+            for (int i = 0; i < P.nsubs; ++i)
+                for (int o = 0; o < P.subs[i].op_count; ++o)
+                    wide = wide || P.ops[P.subs[i].op_begin + o].nt >= 3;
             const ProfMark pf_ = prof_begin(st);
-            k_regstage<REV><<<grid, T, smem_bytes<REV>(), st>>>(
-                sphi->amps, REV ? spsi->amps : nullptr, static_cast<double *>(m_partial.p), P);
+            if (wide) {
+                k_regstage<REV, true><<<grid, T, smem_bytes<REV>(), st>>>(
+                    sphi->amps, REV ? spsi->amps : nullptr, static_cast<double *>(m_partial.p), P);
+            } else {
+                k_regstage<REV, false><<<grid_size<REV, false>(ntiles), T, smem_bytes<REV>(), st>>>(
+                    sphi->amps, REV ? spsi->amps : nullptr, static_cast<double *>(m_partial.p), P);
+            }
             check_launch(REV ? "k_regstage_rev" : "k_regstage", pf_);
         }
     }
