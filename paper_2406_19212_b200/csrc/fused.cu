@@ -761,8 +761,31 @@ void execute(DeviceState *sphi, DeviceState *spsi, const std::vector<FusedOp> &f
 
 } // namespace
 
-bool regstage_available(int pn);
-void run_program_reg(DeviceState *s, const std::vector<Gate> &prog);
+// register executors (regstage_impl.cuh), one namespace per geometry
+#define VQB_DECLARE_REGSTAGE(ns)                                                            \
+    namespace ns {                                                                          \
+    bool regstage_available(int pn);                                                        \
+    void run_program_reg(DeviceState *s, const std::vector<Gate> &prog);                    \
+    void run_reverse_reg(DeviceState *phi, DeviceState *psi, const std::vector<RevOp> &prog, \
+                         double *dgrads);                                                   \
+    }
+VQB_DECLARE_REGSTAGE(rs16)
+VQB_DECLARE_REGSTAGE(rs8)
+#undef VQB_DECLARE_REGSTAGE
+
+namespace {
+// register-executor geometry: VQB_REGS / VQB_REV_REGS = 8 or 16 amplitudes per
+// thread (defaults: 16 for forward programs, 8 for adjoint sweeps)
+bool use_rs8(bool rev) {
+    const char *v = std::getenv(rev ? "VQB_REV_REGS" : "VQB_REGS");
+    if (v && *v) return std::atoi(v) == 8;
+    return rev;
+}
+bool smem_forced() {
+    const char *ex = std::getenv("VQB_EXECUTOR");
+    return ex && std::strcmp(ex, "smem") == 0;
+}
+} // namespace
 
 // One stage through the shared-memory executor (used by the register
 // executor when a stage's program exceeds its parameter block).
@@ -775,10 +798,12 @@ void run_program_fused_smem_stage(DeviceState *s, const std::vector<FusedOp> &fo
 void run_program_fused(DeviceState *s, const std::vector<Gate> &prog) {
     // register-resident executor for states of >= 2^12 amplitudes
     // (VQB_EXECUTOR=smem selects the shared-memory interpreter instead)
-    const char *ex = std::getenv("VQB_EXECUTOR");
-    if (regstage_available(s->pn) && !(ex && std::strcmp(ex, "smem") == 0)) {
-        run_program_reg(s, prog);
-        return;
+    if (!smem_forced()) {
+        if (use_rs8(false) ? rs8::regstage_available(s->pn) : rs16::regstage_available(s->pn)) {
+            if (use_rs8(false)) rs8::run_program_reg(s, prog);
+            else rs16::run_program_reg(s, prog);
+            return;
+        }
     }
     std::vector<FusedOp> fops;
     fops.reserve(prog.size());
@@ -790,15 +815,14 @@ void run_program_fused(DeviceState *s, const std::vector<Gate> &prog) {
     });
 }
 
-void run_reverse_reg(DeviceState *phi, DeviceState *psi, const std::vector<RevOp> &prog,
-                     double *dgrads);
-
 void run_reverse_fused(DeviceState *phi, DeviceState *psi, const std::vector<RevOp> &prog,
                        double *dgrads) {
-    const char *ex = std::getenv("VQB_EXECUTOR");
-    if (regstage_available(phi->pn) && !(ex && std::strcmp(ex, "smem") == 0)) {
-        run_reverse_reg(phi, psi, prog, dgrads);
-        return;
+    if (!smem_forced()) {
+        if (use_rs8(true) ? rs8::regstage_available(phi->pn) : rs16::regstage_available(phi->pn)) {
+            if (use_rs8(true)) rs8::run_reverse_reg(phi, psi, prog, dgrads);
+            else rs16::run_reverse_reg(phi, psi, prog, dgrads);
+            return;
+        }
     }
     std::vector<FusedOp> fops;
     fops.reserve(prog.size());

@@ -1,1083 +1,8 @@
-// Register-resident stage executor (forward programs and adjoint sweeps).
-//
-// A stage's tile (K = 11 tile bits = 2048 amplitudes per state) is split over
-// 128 threads x 16 registers. A *layout* assigns 4 tile bits to the register
-// index and 7 to the thread index. Within a sub-stage every operation's
-// mixing bits are register bits, so the operation is pure register arithmetic
-// (FP64 FMA bound, no shared memory, no barrier). Between sub-stages the tile
-// is re-laid out once through shared memory, XOR-swizzled so the three
-// quarter-warp lane bits always hit distinct bank groups. The next tile is
-// prefetched with cp.async (LDGSTS) into a staging buffer while the current
-// one is computed; results are stored straight from registers. Two blocks run
-// per SM, so one block's relayout or load phase overlaps the other's FP64.
-//
-// The stage program (layouts, operations, sub-matrices) is one
-// __grid_constant__ parameter block (read through the constant cache);
-// programs that do not fit are split over several launches of the same tile
-// bits.
-//
-// Adjoint mode (REV): each thread holds 16 amplitudes of Phi and of Psi; a
-// parametric step computes Phi <- inv Phi, Re <Psi| D_p |Phi>, Psi <- inv Psi
-// in registers (reverse_sweep_step kernels.hpp:659-697); contributions are
-// reduced per warp into shared-memory slots, per block into a partial row,
-// and over blocks in fixed order by k_grads (deterministic for a fixed grid).
-#include <cuda_runtime.h>
-
-#include <algorithm>
-#include <cstdio>
-#include <cstdlib>
-#include <cstring>
-
-#include "plan.hpp"
-
-namespace vqb {
-
-void apply_gate_fast(double2 *a, int pn, const Gate &g, cudaStream_t st);
-void note_flops(double f);
-void reverse_step_async(double2 *phi, double2 *psi, int pn, const int *pos1, int m,
-                        const cvec &inv, const std::vector<cvec> &dmats, DeviceState *w,
-                        double2 *out_c, double *out_r, double real_scale);
-
-namespace {
-
-constexpr int RB = 4;       // register bits
-constexpr int R = 1 << RB;  // amplitudes per thread (per state)
-constexpr int TB = 7;       // thread bits
-constexpr int T = 1 << TB;  // threads per block (one tile per block at a time)
-constexpr int NW = T / 32;  // warps per block
-constexpr int K = RB + TB;  // tile bits
-constexpr int TS = 1 << K;  // tile size
-
-constexpr int kMaxSubs = 32;
-constexpr int kMaxOps = 56;
-constexpr int kMaxSlots = 64;
-constexpr int kMaxPool = 1088; // double2 entries
-constexpr int kMaxTab = 192;   // per-element diagonal tables, copied to shared memory
-
-struct RLayout {
-    int reg[RB]; // tile-local bit of register bit b
-    int thr[TB]; // tile-local bit of thread bit b (thr[0..2]: quarter-warp lanes)
-};
-
-struct ROp {
-    int nt, nc, np;
-    int code;             // nt = 1: p0; nt = 2: pair index; nt = 3: triple index
-    int per_group;        // condition depends on register bits
-    int pair;             // psi has its own matrices (channel steps)
-    int slot;             // first gradient slot (param ops)
-    int ck[kMaxCond];     // 0: outside tile, 1: thread bit, 2: register bit
-    int cp[kMaxCond];     // global bit / thread bit / register bit
-    unsigned mat, mat_psi, mat_d; // pool offsets (2^nc sub-matrices each, ascending order)
-    unsigned long long ident, ident_psi;
-    int rw[RB];           // condition-index bits contributed by register bit b
-    int tab, tab_psi;     // nt = 0 with register conditions: shared-memory tables
-    int xoff, nx;         // nt >= 3: XOR patterns of the diagonal-times-permutation terms
-};
-
-struct RSub {
-    RLayout L;
-    int op_begin, op_count;
-};
-
-struct RParams {
-    int bits[K];                // tile bits ascending (global); local bit j <-> bits[j]
-    unsigned long long ntiles;
-    int nsubs, nslots, slot_begin, partial_ld;
-    RSub subs[kMaxSubs];
-    ROp ops[kMaxOps];
-    double2 pool[kMaxPool];
-    double2 tab[kMaxTab];
-    int ntab, nxpat;
-    unsigned char xpat[256];
-};
-static_assert(sizeof(RParams) <= 32000, "kernel parameter block too large");
-
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
-}
-__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
-    return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
-}
-// Re(conj(a) * b)
-__device__ __forceinline__ double re_cj(double2 a, double2 b) { return fma(a.x, b.x, a.y * b.y); }
-
-// shared-memory slot of a tile-local index: low 3 bits XOR-folded with the
-// higher 3-bit chunks (local bit l contributes to bank bit l mod 3).
-// XOR-linear: swz(a | b) = swz(a) ^ swz(b) for disjoint a, b.
-__host__ __device__ __forceinline__ int swz(int l) {
-    return l ^ ((l >> 3) & 7) ^ ((l >> 6) & 7) ^ ((l >> 9) & 7);
-}
-
-struct Addr {
-    int st;
-    int sw[RB];
-};
-
-__device__ __forceinline__ Addr layout_addr(const RLayout &L, int t) {
-    Addr a;
-    int td = 0;
-#pragma unroll
-    for (int b = 0; b < TB; ++b) td |= ((t >> b) & 1) << L.thr[b];
-    a.st = swz(td);
-#pragma unroll
-    for (int b = 0; b < RB; ++b) a.sw[b] = swz(1 << L.reg[b]);
-    return a;
-}
-
-__device__ __forceinline__ int slot(const Addr &a, int i) {
-    int s = a.st;
-#pragma unroll
-    for (int b = 0; b < RB; ++b)
-        if ((i >> b) & 1) s ^= a.sw[b];
-    return s;
-}
-
-// condition value of register element i (a compile-time constant in the
-// unrolled loops): the per-register-bit masks are ORed in
-__device__ __forceinline__ int cond_of(const ROp &op, int cbase, int i) {
-    int c = cbase;
-#pragma unroll
-    for (int b = 0; b < RB; ++b)
-        if ((i >> b) & 1) c |= op.rw[b];
-    return c;
-}
-
-template <int NT, int P0, int P1, int P2, int P3> struct Pos {
-    static constexpr int D = 1 << NT;
-    static constexpr int MASK = (NT > 0 ? 1 << P0 : 0) | (NT > 1 ? 1 << P1 : 0) |
-                                (NT > 2 ? 1 << P2 : 0) | (NT > 3 ? 1 << P3 : 0);
-    __host__ __device__ static constexpr int off(int r) {
-        int o = 0;
-        if (NT > 0 && (r & 1)) o |= 1 << P0;
-        if (NT > 1 && (r & 2)) o |= 1 << P1;
-        if (NT > 2 && (r & 4)) o |= 1 << P2;
-        if (NT > 3 && (r & 8)) o |= 1 << P3;
-        return o;
-    }
-};
-
-// select entry c (< 4) of a register table with predicated moves (no
-// divergent constant-cache loads)
-__device__ __forceinline__ double2 sel4(const double2 (&t)[4], int c) {
-    double2 r = t[0];
-    if (c == 1) r = t[1];
-    if (c == 2) r = t[2];
-    if (c == 3) r = t[3];
-    return r;
-}
-
-// out = M * v[group], written back in place; M read element by element.
-template <class PS>
-__device__ __forceinline__ void group_mv(double2 (&v)[R], int i, const double2 *M) {
-    constexpr int D = PS::D;
-    double2 out[D];
-#pragma unroll
-    for (int r = 0; r < D; ++r) {
-        double2 acc = cmul(M[r], v[i | PS::off(0)]);
-#pragma unroll
-        for (int s = 1; s < D; ++s) acc = cfma(M[r + s * D], v[i | PS::off(s)], acc);
-        out[r] = acc;
-    }
-#pragma unroll
-    for (int r = 0; r < D; ++r) v[i | PS::off(r)] = out[r];
-}
-
-// Apply an nt-bit operation (sub-matrices at `mat`) to one register state.
-// HOIST: a uniform sub-matrix of nt <= HOIST is loaded into registers once.
-template <int HOIST, int NT, int P0, int P1 = 0, int P2 = 0, int P3 = 0>
-__device__ __forceinline__ void apply_r(double2 (&v)[R], const ROp &op, const double2 *pool,
-                                        int cbase, unsigned mat, unsigned long long ident) {
-    using PS = Pos<NT, P0, P1, P2, P3>;
-    constexpr int D = PS::D;
-    if (NT <= HOIST && !op.per_group) {
-        if ((ident >> cbase) & 1) return;
-        const double2 *M = pool + mat + cbase * D * D;
-        double2 m[D * D];
-#pragma unroll
-        for (int e = 0; e < D * D; ++e) m[e] = M[e];
-#pragma unroll
-        for (int i = 0; i < R; ++i)
-            if (!(i & PS::MASK)) group_mv<PS>(v, i, m);
-        return;
-    }
-    if (!op.per_group && ((ident >> cbase) & 1)) return;
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-        if (i & PS::MASK) continue;
-        const int c = op.per_group ? cond_of(op, cbase, i) : cbase;
-        if (op.per_group && ((ident >> c) & 1)) continue;
-        group_mv<PS>(v, i, pool + mat + c * D * D);
-    }
-}
-
-// Reverse-sweep parametric step on (phi, psi) registers.
-template <int NT, int P0, int P1 = 0, int P2 = 0, int P3 = 0>
-__device__ __forceinline__ void param_r(double2 (&vf)[R], double2 (&vg)[R], const ROp &op,
-                                        const double2 *pool, int cbase, double (&acc)[VQB_MAX_PARAMS]) {
-    using PS = Pos<NT, P0, P1, P2, P3>;
-    constexpr int D = PS::D;
-    const int nsub = 1 << op.nc;
-    if (NT == 0 && op.per_group && op.np == 1 && op.tab >= 0) {
-        // diagonal step with per-element conditions: tables in shared memory
-        // (the first kMaxTab entries of the dynamic shared memory)
-        extern __shared__ __align__(16) unsigned char smem_raw[];
-        const double2 *stab = reinterpret_cast<const double2 *>(smem_raw);
-#pragma unroll
-        for (int i = 0; i < R; ++i) {
-            const int c = cond_of(op, cbase, i);
-            const double2 m = stab[op.tab + c], d = stab[op.tab + nsub + c];
-            const double2 w = cmul(m, vf[i]);
-            vf[i] = w;
-            acc[0] += re_cj(vg[i], cmul(d, w));
-            vg[i] = cmul(m, vg[i]);
-        }
-        return;
-    }
-    if (NT <= 1 && !op.per_group && op.np == 1) {
-        double2 m[D * D], d[D * D];
-#pragma unroll
-        for (int e = 0; e < D * D; ++e) {
-            m[e] = pool[op.mat + cbase * D * D + e];
-            d[e] = pool[op.mat_d + cbase * D * D + e];
-        }
-#pragma unroll
-        for (int i = 0; i < R; ++i) {
-            if (i & PS::MASK) continue;
-            group_mv<PS>(vf, i, m);
-            double a = 0;
-#pragma unroll
-            for (int r = 0; r < D; ++r) {
-                double2 x = cmul(d[r], vf[i | PS::off(0)]);
-#pragma unroll
-                for (int s = 1; s < D; ++s) x = cfma(d[r + s * D], vf[i | PS::off(s)], x);
-                a += re_cj(vg[i | PS::off(r)], x);
-            }
-            acc[0] += a;
-            group_mv<PS>(vg, i, m);
-        }
-        return;
-    }
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-        if (i & PS::MASK) continue;
-        const int c = op.per_group ? cond_of(op, cbase, i) : cbase;
-        group_mv<PS>(vf, i, pool + op.mat + c * D * D);
-#pragma unroll
-        for (int p = 0; p < VQB_MAX_PARAMS; ++p) {
-            if (p >= op.np) break;
-            const double2 *Dm = pool + op.mat_d + (p * nsub + c) * D * D;
-            double a = 0;
-#pragma unroll
-            for (int r = 0; r < D; ++r) {
-                double2 x = cmul(Dm[r], vf[i | PS::off(0)]);
-#pragma unroll
-                for (int s = 1; s < D; ++s) x = cfma(Dm[r + s * D], vf[i | PS::off(s)], x);
-                a += re_cj(vg[i | PS::off(r)], x);
-            }
-            acc[p] += a;
-        }
-        group_mv<PS>(vg, i, pool + op.mat + c * D * D);
-    }
-}
-
-__device__ __forceinline__ void apply_diag(double2 (&v)[R], const ROp &op, const double2 *pool,
-                                           int cbase, unsigned mat, unsigned long long ident) {
-    if (!op.per_group) {
-        if ((ident >> cbase) & 1) return;
-        const double2 ph = pool[mat + cbase];
-#pragma unroll
-        for (int i = 0; i < R; ++i) v[i] = cmul(ph, v[i]);
-        return;
-    }
-    const int tabo = mat == op.mat ? op.tab : op.tab_psi;
-    if (tabo >= 0) {
-        // per-element phase from the shared-memory copy of the table
-        extern __shared__ __align__(16) unsigned char smem_raw[];
-        const double2 *stab = reinterpret_cast<const double2 *>(smem_raw) + tabo;
-#pragma unroll
-        for (int i = 0; i < R; ++i) v[i] = cmul(stab[cond_of(op, cbase, i)], v[i]);
-        return;
-    }
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-        const int c = cond_of(op, cbase, i);
-        if ((ident >> c) & 1) continue;
-        v[i] = cmul(pool[mat + c], v[i]);
-    }
-}
-
-template <int HOIST, int MAXNT>
-__device__ __forceinline__ void dispatch(double2 (&v)[R], const ROp &op, const double2 *pool,
-                                         int cbase, unsigned mat, unsigned long long ident) {
-    if (op.nt > MAXNT) return; // the caller routes wider ops elsewhere
-    switch (op.nt) {
-    case 0: apply_diag(v, op, pool, cbase, mat, ident); return;
-    case 1:
-        switch (op.code) {
-        case 0: apply_r<HOIST, 1, 0>(v, op, pool, cbase, mat, ident); return;
-        case 1: apply_r<HOIST, 1, 1>(v, op, pool, cbase, mat, ident); return;
-        case 2: apply_r<HOIST, 1, 2>(v, op, pool, cbase, mat, ident); return;
-        default: apply_r<HOIST, 1, 3>(v, op, pool, cbase, mat, ident); return;
-        }
-    case 2:
-        switch (op.code) {
-        case 0: apply_r<HOIST, 2, 0, 1>(v, op, pool, cbase, mat, ident); return;
-        case 1: apply_r<HOIST, 2, 0, 2>(v, op, pool, cbase, mat, ident); return;
-        case 2: apply_r<HOIST, 2, 0, 3>(v, op, pool, cbase, mat, ident); return;
-        case 3: apply_r<HOIST, 2, 1, 2>(v, op, pool, cbase, mat, ident); return;
-        case 4: apply_r<HOIST, 2, 1, 3>(v, op, pool, cbase, mat, ident); return;
-        default: apply_r<HOIST, 2, 2, 3>(v, op, pool, cbase, mat, ident); return;
-        }
-    case 3:
-        if constexpr (MAXNT >= 3) {
-            switch (op.code) {
-            case 0: apply_r<HOIST, 3, 0, 1, 2>(v, op, pool, cbase, mat, ident); return;
-            case 1: apply_r<HOIST, 3, 0, 1, 3>(v, op, pool, cbase, mat, ident); return;
-            case 2: apply_r<HOIST, 3, 0, 2, 3>(v, op, pool, cbase, mat, ident); return;
-            default: apply_r<HOIST, 3, 1, 2, 3>(v, op, pool, cbase, mat, ident); return;
-            }
-        }
-        return;
-    default:
-        if constexpr (MAXNT >= 4) apply_r<HOIST, 4, 0, 1, 2, 3>(v, op, pool, cbase, mat, ident);
-        return;
-    }
-}
-
-__device__ __forceinline__ void dispatch_param(double2 (&vf)[R], double2 (&vg)[R], const ROp &op,
-                                               const double2 *pool, int cbase,
-                                               double (&acc)[VQB_MAX_PARAMS]) {
-    switch (op.nt) {
-    case 0: param_r<0, 0>(vf, vg, op, pool, cbase, acc); return;
-    case 1:
-        switch (op.code) {
-        case 0: param_r<1, 0>(vf, vg, op, pool, cbase, acc); return;
-        case 1: param_r<1, 1>(vf, vg, op, pool, cbase, acc); return;
-        case 2: param_r<1, 2>(vf, vg, op, pool, cbase, acc); return;
-        default: param_r<1, 3>(vf, vg, op, pool, cbase, acc); return;
-        }
-    case 2:
-        switch (op.code) {
-        case 0: param_r<2, 0, 1>(vf, vg, op, pool, cbase, acc); return;
-        case 1: param_r<2, 0, 2>(vf, vg, op, pool, cbase, acc); return;
-        case 2: param_r<2, 0, 3>(vf, vg, op, pool, cbase, acc); return;
-        case 3: param_r<2, 1, 2>(vf, vg, op, pool, cbase, acc); return;
-        case 4: param_r<2, 1, 3>(vf, vg, op, pool, cbase, acc); return;
-        default: param_r<2, 2, 3>(vf, vg, op, pool, cbase, acc); return;
-        }
-    default: return; // wider parametric steps are planned as unfusable
-    }
-}
-
-// Wide (nt >= 3) operation on one state through the relayout buffer: the
-// registers go to shared memory in layout L, the operation runs over 2^(K-nt)
-// groups per tile with the outputs written straight back, and the registers
-// are reloaded. Used by the adjoint kernel, whose two register states leave
-// no room for 8- or 16-element groups.
-template <int NT>
-__device__ __forceinline__ void smem_op(double2 (&v)[R], const Addr &A, const RLayout &L,
-                                        double2 *xbuf, const ROp &op, const double2 *pool,
-                                        int cbase_uni, unsigned mat, unsigned long long ident,
-                                        int t, const unsigned char *P_xpat) {
-    constexpr int D = 1 << NT;
-    // register positions of the mixing bits (ascending), then their local bits
-    int rp[4] = {0, 1, 2, 3};
-    if (NT == 3) {
-        const int missing = 3 - op.code; // triple_code inverse
-        for (int q = 0, k = 0; q < 4; ++q)
-            if (q != missing) rp[k++] = q;
-    }
-    int lb[NT], sorted[NT];
-#pragma unroll
-    for (int q = 0; q < NT; ++q) sorted[q] = lb[q] = L.reg[rp[q]];
-#pragma unroll
-    for (int a = 0; a < NT; ++a)
-#pragma unroll
-        for (int b = 0; b + 1 < NT - a; ++b)
-            if (sorted[b] > sorted[b + 1]) {
-                const int x = sorted[b];
-                sorted[b] = sorted[b + 1];
-                sorted[b + 1] = x;
-            }
-    int sw_off[D];
-#pragma unroll
-    for (int r = 0; r < D; ++r) {
-        int o = 0;
-#pragma unroll
-        for (int q = 0; q < NT; ++q)
-            if (r >> q & 1) o |= 1 << lb[q];
-        sw_off[r] = swz(o);
-    }
-#pragma unroll
-    for (int i = 0; i < R; ++i) xbuf[slot(A, i)] = v[i];
-    __syncthreads();
-    for (int g = t; g < (TS >> NT); g += T) {
-        int b = g;
-#pragma unroll
-        for (int q = 0; q < NT; ++q) {
-            const int s = sorted[q];
-            b = ((b >> s) << (s + 1)) | (b & ((1 << s) - 1));
-        }
-        int c = cbase_uni;
-        for (int q = 0; q < op.nc; ++q) {
-            const int l = op.ck[q] == 1 ? L.thr[op.cp[q]] : (op.ck[q] == 2 ? L.reg[op.cp[q]] : -1);
-            if (l >= 0) c |= ((b >> l) & 1) << q;
-        }
-        if ((ident >> c) & 1) continue;
-        // S = sum_k diag(d_k) P_{x_k}: out[r] = sum_k d_k[r] in[r ^ x_k]; the
-        // swizzle is XOR-linear, so slot(r ^ x) = slot(r) ^ slot(x)
-        const double2 *Mc = pool + mat + c * op.nx * D;
-        const int sb = swz(b);
-        double2 out[D];
-#pragma unroll
-        for (int r = 0; r < D; ++r) out[r] = make_double2(0, 0);
-        for (int k = 0; k < op.nx; ++k) {
-            const int x = P_xpat[op.xoff + k];
-            int sx = 0;
-#pragma unroll
-            for (int q = 0; q < NT; ++q)
-                if ((x >> q) & 1) sx ^= sw_off[1 << q];
-            const double2 *dk = Mc + k * D;
-#pragma unroll
-            for (int r = 0; r < D; ++r) out[r] = cfma(dk[r], xbuf[sb ^ sw_off[r] ^ sx], out[r]);
-        }
-        __syncwarp();
-#pragma unroll
-        for (int r = 0; r < D; ++r) xbuf[sb ^ sw_off[r]] = out[r];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < R; ++i) v[i] = xbuf[slot(A, i)];
-    __syncthreads();
-}
-
-// WIDE = false: forward stages without nt >= 3 operations (leaner registers)
-template <bool REV, bool WIDE = true>
-__global__ void __launch_bounds__(T, (!REV && !WIDE) ? 3 : 2)
-    k_regstage(double2 *__restrict__ phi, double2 *__restrict__ psi,
-               double *__restrict__ partial, const __grid_constant__ RParams P) {
-    constexpr int NS = REV ? 2 : 1; // states per tile
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    // layout: diagonal tables | NS staging tiles (cp.async target) | relayout tile | slots
-    double2 *stab = reinterpret_cast<double2 *>(smem_raw);
-    double2 *stage_buf = stab + kMaxTab;
-    double2 *xbuf = stage_buf + NS * TS;
-    double *pacc = reinterpret_cast<double *>(xbuf + TS); // [nslots][NW]
-    const int t = threadIdx.x;
-    const int lane = t & 31, warp = t >> 5;
-    if (REV)
-        for (int i = t; i < P.nslots * NW; i += T) pacc[i] = 0;
-    for (int i = t; i < P.ntab; i += T) stab[i] = P.tab[i];
-    __syncthreads();
-
-    // natural tile order j = t + T*s: global offset glo | gh(s), slot swz(j)
-    unsigned long long glo = 0;
-#pragma unroll
-    for (int b = 0; b < TB; ++b)
-        if ((t >> b) & 1) glo |= 1ull << P.bits[b];
-    unsigned long long gh[RB];
-#pragma unroll
-    for (int b = 0; b < RB; ++b) gh[b] = 1ull << P.bits[TB + b];
-    const int nat_st = swz(t);
-    int nat_sw[RB];
-#pragma unroll
-    for (int b = 0; b < RB; ++b) nat_sw[b] = swz(T << b);
-    auto tile_base = [&](unsigned long long c) {
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-            const int s = P.bits[i];
-            c = ((c >> s) << (s + 1)) | (c & ((1ull << s) - 1));
-        }
-        return c;
-    };
-    auto prefetch = [&](unsigned long long tile) {
-        const unsigned long long base = tile_base(tile);
-#pragma unroll
-        for (int s = 0; s < R; ++s) {
-            unsigned long long g = base | glo;
-            int sl = nat_st;
-#pragma unroll
-            for (int b = 0; b < RB; ++b)
-                if ((s >> b) & 1) {
-                    g |= gh[b];
-                    sl ^= nat_sw[b];
-                }
-#pragma unroll
-            for (int q = 0; q < NS; ++q) {
-                const unsigned sa = (unsigned)__cvta_generic_to_shared(&stage_buf[q * TS + sl]);
-                const double2 *src = (q == 0 ? phi : psi) + g;
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src));
-            }
-        }
-        asm volatile("cp.async.commit_group;\n" ::);
-    };
-    auto relayout = [&](double2 (&v)[R], const Addr &A, const Addr &B) {
-#pragma unroll
-        for (int i = 0; i < R; ++i) xbuf[slot(A, i)] = v[i];
-        __syncthreads();
-#pragma unroll
-        for (int i = 0; i < R; ++i) v[i] = xbuf[slot(B, i)];
-        __syncthreads();
-    };
-
-    unsigned long long tile = blockIdx.x;
-    if (tile < P.ntiles) prefetch(tile);
-    for (; tile < P.ntiles; tile += gridDim.x) {
-        const unsigned long long base = tile_base(tile);
-        asm volatile("cp.async.wait_group 0;\n" ::);
-        __syncthreads();
-        double2 vf[R], vg[REV ? R : 1];
-        Addr A = layout_addr(P.subs[0].L, t);
-#pragma unroll
-        for (int i = 0; i < R; ++i) vf[i] = stage_buf[slot(A, i)];
-        if constexpr (REV) {
-#pragma unroll
-            for (int i = 0; i < R; ++i) vg[i] = stage_buf[TS + slot(A, i)];
-        }
-        __syncthreads(); // staging consumed: refill it with the next tile
-        if (tile + gridDim.x < P.ntiles) prefetch(tile + gridDim.x);
-        int cur = 0;
-        for (int sub = 0; sub < P.nsubs; ++sub) {
-            if (sub > 0) {
-                const Addr B = layout_addr(P.subs[sub].L, t);
-                relayout(vf, A, B);
-                if constexpr (REV) relayout(vg, A, B);
-                A = B;
-                cur = sub;
-            }
-            const RSub &sb = P.subs[sub];
-            for (int o = 0; o < sb.op_count; ++o) {
-                const ROp &op = P.ops[sb.op_begin + o];
-                int cuni = 0, cthr = 0;
-                for (int q = 0; q < op.nc; ++q) {
-                    if (op.ck[q] == 0) cuni |= (int)((base >> op.cp[q]) & 1) << q;
-                    else if (op.ck[q] == 1) cthr |= ((t >> op.cp[q]) & 1) << q;
-                }
-                const int cbase = cuni | cthr;
-                if constexpr (!REV) {
-                    if (!WIDE || op.nt <= 2) {
-                        dispatch<2, 2>(vf, op, P.pool, cbase, op.mat, op.ident);
-                    } else if (op.nt == 3) {
-                        smem_op<3>(vf, A, P.subs[sub].L, xbuf, op, P.pool, cuni, op.mat, op.ident, t,
-                                   P.xpat);
-                    } else {
-                        smem_op<4>(vf, A, P.subs[sub].L, xbuf, op, P.pool, cuni, op.mat, op.ident, t,
-                                   P.xpat);
-                    }
-                } else if (op.np == 0 && op.nt <= 2) {
-                    dispatch<1, 2>(vf, op, P.pool, cbase, op.mat, op.ident);
-                    dispatch<1, 2>(vg, op, P.pool, cbase, op.pair ? op.mat_psi : op.mat,
-                                   op.pair ? op.ident_psi : op.ident);
-                } else if (op.np == 0) {
-                    const RLayout &Lc = P.subs[sub].L;
-                    const unsigned mg = op.pair ? op.mat_psi : op.mat;
-                    const unsigned long long ig = op.pair ? op.ident_psi : op.ident;
-                    if (op.nt == 3) {
-                        smem_op<3>(vf, A, Lc, xbuf, op, P.pool, cuni, op.mat, op.ident, t, P.xpat);
-                        smem_op<3>(vg, A, Lc, xbuf, op, P.pool, cuni, mg, ig, t, P.xpat);
-                    } else {
-                        smem_op<4>(vf, A, Lc, xbuf, op, P.pool, cuni, op.mat, op.ident, t, P.xpat);
-                        smem_op<4>(vg, A, Lc, xbuf, op, P.pool, cuni, mg, ig, t, P.xpat);
-                    }
-                } else {
-                    double acc[VQB_MAX_PARAMS] = {0, 0, 0, 0, 0};
-                    dispatch_param(vf, vg, op, P.pool, cbase, acc);
-#pragma unroll
-                    for (int p = 0; p < VQB_MAX_PARAMS; ++p) {
-                        if (p >= op.np) break;
-                        double x = acc[p];
-#pragma unroll
-                        for (int sh = 16; sh > 0; sh >>= 1) x += __shfl_down_sync(0xffffffffu, x, sh);
-                        if (lane == 0) pacc[(op.slot + p) * NW + warp] += x;
-                    }
-                }
-            }
-        }
-        // store from registers in the final layout
-        const RLayout &L = P.subs[cur].L;
-        unsigned long long g0 = base;
-#pragma unroll
-        for (int b = 0; b < TB; ++b)
-            if ((t >> b) & 1) g0 |= 1ull << P.bits[L.thr[b]];
-        unsigned long long gr[RB];
-#pragma unroll
-        for (int b = 0; b < RB; ++b) gr[b] = 1ull << P.bits[L.reg[b]];
-#pragma unroll
-        for (int i = 0; i < R; ++i) {
-            unsigned long long g = g0;
-#pragma unroll
-            for (int b = 0; b < RB; ++b)
-                if ((i >> b) & 1) g |= gr[b];
-            phi[g] = vf[i];
-            if constexpr (REV) psi[g] = vg[i];
-        }
-    }
-    asm volatile("cp.async.wait_group 0;\n" ::);
-    if constexpr (REV) {
-        __syncthreads();
-        for (int s = t; s < P.nslots; s += T) {
-            double x = 0;
-            for (int w = 0; w < NW; ++w) x += pacc[s * NW + w];
-            partial[(size_t)blockIdx.x * P.partial_ld + P.slot_begin + s] = x;
-        }
-    }
-}
-
-// grads[dst[j]] = scale[j] * sum_b partial[b][j] (fixed block order)
-__global__ void k_grads(const double *__restrict__ partial, int nblocks, int ld,
-                        const double *__restrict__ scale, const long long *__restrict__ dst,
-                        int ncols, double *__restrict__ grads) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= ncols) return;
-    double v = 0;
-    for (int b = 0; b < nblocks; ++b) v += partial[(size_t)b * ld + j];
-    grads[dst[j]] = scale[j] * v;
-}
-
-// ---------------------------------------------------------------- host planning
-int pair_code(int a, int b) { // a < b in [0,4)
-    static const int code[4][4] = {{-1, 0, 1, 2}, {-1, -1, 3, 4}, {-1, -1, -1, 5}, {}};
-    return code[a][b];
-}
-int triple_code(int a, int b, int c) {
-    return 3 - (6 - a - b - c); // {0,1,2}->0, {0,1,3}->1, {0,2,3}->2, {1,2,3}->3
-}
-
-// reorder the local bits of a (2^nt x 2^nt) matrix: new bit q = old bit perm[q]
-cvec permute_matrix(const cvec &m, int nt, const int *perm) {
-    const int d = 1 << nt;
-    auto map = [&](int nidx) {
-        int o = 0;
-        for (int q = 0; q < nt; ++q)
-            if (nidx >> q & 1) o |= 1 << perm[q];
-        return o;
-    };
-    cvec out(m.size());
-    for (int c = 0; c < d; ++c)
-        for (int r = 0; r < d; ++r) out[r + c * d] = m[map(r) + map(c) * d];
-    return out;
-}
-
-// thr[0..2] get distinct residues mod 3 (bank-conflict free under swz),
-// preferring local bits 0,1,2 (coalesced stores).
-void choose_threads(RLayout &L, const std::vector<int> &fb) {
-    int lanes[3] = {-1, -1, -1};
-    auto used = [&](int b) { return lanes[0] == b || lanes[1] == b || lanes[2] == b; };
-    for (int want = 0; want < 3; ++want)
-        if (std::find(fb.begin(), fb.end(), want) != fb.end()) lanes[want] = want;
-    for (int r = 0; r < 3; ++r)
-        if (lanes[r] < 0)
-            for (int b : fb)
-                if (!used(b) && b % 3 == r) {
-                    lanes[r] = b;
-                    break;
-                }
-    for (int r = 0; r < 3; ++r)
-        if (lanes[r] < 0)
-            for (int b : fb)
-                if (!used(b)) {
-                    lanes[r] = b;
-                    break;
-                }
-    int k = 0;
-    for (int r = 0; r < 3; ++r) L.thr[k++] = lanes[r];
-    for (int b : fb)
-        if (!used(b)) L.thr[k++] = b;
-}
-
-struct SlotMap {
-    std::vector<double> scale;
-    std::vector<long long> dst;
-};
-
-// Lower as much of a stage's block list as fits one parameter block.
-// `remaining` (block indices, in a valid order) is consumed; what is left
-// must run in a following launch with the same tile bits.
-void lower_stage_reg(const Stage &sg, const std::vector<FusedOp> &blocks,
-                     std::vector<int> &remaining, int pn, bool rev, RParams &P, SlotMap &slots) {
-    std::memset(&P, 0, sizeof P);
-    for (int j = 0; j < K; ++j) P.bits[j] = sg.bits[j];
-    P.ntiles = 1ull << (pn - K);
-    P.slot_begin = (int)slots.scale.size();
-    auto local_of = [&](int g) {
-        for (int j = 0; j < K; ++j)
-            if (sg.bits[j] == g) return j;
-        return -1;
-    };
-    auto mixmask = [&](const FusedOp &f) {
-        unsigned mix = 0;
-        for (int q = 0; q < f.nt; ++q) mix |= 1u << local_of(f.mix[q]);
-        return mix;
-    };
-    auto count_x = [&](const FusedOp &f) { // XOR patterns of a wide op
-        if (f.nt < 3) return 0;
-        const int D = 1 << f.nt, dd = D * D;
-        int nx = 0;
-        for (int x = 0; x < D; ++x) {
-            bool any = false;
-            for (int c = 0; c < (1 << f.nc) && !any; ++c)
-                for (int r = 0; r < D && !any; ++r)
-                    any = f.sub_phi[size_t(c) * dd + r + size_t(r ^ x) * D] != cplx(0) ||
-                          (f.pair && f.sub_psi[size_t(c) * dd + r + size_t(r ^ x) * D] != cplx(0));
-            nx += any ? 1 : 0;
-        }
-        return nx;
-    };
-    auto pool_need = [&](const FusedOp &f) {
-        if (f.nt >= 3) // XOR-term form: |X| * D entries per sub-matrix
-            return (count_x(f) * (1 << f.nt) << f.nc) * (1 + (f.pair ? 1 : 0));
-        const int dd = (1 << (2 * f.nt)) << f.nc;
-        return dd * (1 + (f.pair ? 1 : 0) + (rev ? f.np : 0));
-    };
-    int nops = 0, npool = 0, nslots = 0;
-    while (!remaining.empty()) {
-        if (P.nsubs >= kMaxSubs) break;
-        unsigned rset = 0;
-        uint64_t blocked = 0;
-        std::vector<int> taken, deferred;
-        int pool_used = 0, ops_used = 0, slots_used = 0, xp_used = 0;
-        for (int i : remaining) {
-            const FusedOp &f = blocks[i];
-            const unsigned mix = mixmask(f);
-            const int nx = count_x(f);
-            const bool fits_res = nops + ops_used < kMaxOps &&
-                                  npool + pool_used + pool_need(f) <= kMaxPool &&
-                                  nslots + slots_used + (rev ? f.np : 0) <= kMaxSlots &&
-                                  P.nxpat + xp_used + nx <= 256;
-            if ((f.support & blocked) || __builtin_popcount(rset | mix) > RB || !fits_res) {
-                deferred.push_back(i);
-                blocked |= f.support;
-                continue;
-            }
-            rset |= mix;
-            taken.push_back(i);
-            pool_used += pool_need(f);
-            xp_used += nx;
-            ++ops_used;
-            slots_used += rev ? f.np : 0;
-        }
-        if (taken.empty()) break; // parameter block full: continue in the next launch
-        for (int i : deferred) {
-            const unsigned mix = mixmask(blocks[i]);
-            if (__builtin_popcount(rset | mix) <= RB) rset |= mix;
-        }
-        for (int j = K - 1; j >= 0 && __builtin_popcount(rset) < RB; --j) rset |= 1u << j;
-        RSub &sb = P.subs[P.nsubs++];
-        int nr = 0;
-        std::vector<int> free_bits;
-        for (int j = 0; j < K; ++j) {
-            if (rset >> j & 1) sb.L.reg[nr++] = j;
-            else free_bits.push_back(j);
-        }
-        choose_threads(sb.L, free_bits);
-        auto reg_of = [&](int j) {
-            for (int b = 0; b < RB; ++b)
-                if (sb.L.reg[b] == j) return b;
-            return -1;
-        };
-        auto thr_of = [&](int j) {
-            for (int b = 0; b < TB; ++b)
-                if (sb.L.thr[b] == j) return b;
-            return -1;
-        };
-        sb.op_begin = nops;
-        for (int i : taken) {
-            const FusedOp &f = blocks[i];
-            ROp &o = P.ops[nops++];
-            o.nt = f.nt;
-            o.nc = f.nc;
-            o.np = rev ? f.np : 0;
-            o.pair = f.pair ? 1 : 0;
-            int rp[kMaxMix], order[kMaxMix];
-            for (int q = 0; q < f.nt; ++q) {
-                rp[q] = reg_of(local_of(f.mix[q]));
-                order[q] = q;
-            }
-            std::sort(order, order + f.nt, [&](int x, int y) { return rp[x] < rp[y]; });
-            int srp[kMaxMix];
-            for (int q = 0; q < f.nt; ++q) srp[q] = rp[order[q]];
-            if (f.nt == 1) o.code = srp[0];
-            if (f.nt == 2) o.code = pair_code(srp[0], srp[1]);
-            if (f.nt == 3) o.code = triple_code(srp[0], srp[1], srp[2]);
-            for (int q = 0; q < f.nc; ++q) {
-                const int j = local_of(f.cnd[q]);
-                if (j < 0) {
-                    o.ck[q] = 0;
-                    o.cp[q] = f.cnd[q];
-                } else if (reg_of(j) >= 0) {
-                    o.ck[q] = 2;
-                    o.cp[q] = reg_of(j);
-                    o.per_group = 1;
-                } else {
-                    o.ck[q] = 1;
-                    o.cp[q] = thr_of(j);
-                }
-            }
-            const int D = 1 << f.nt, dd = D * D;
-            // push 2^nc sub-matrices of `src` (permuted to ascending register
-            // order); returns the pool offset and the identity mask
-            auto push = [&](const cvec &src, size_t first_block, unsigned long long *ident) {
-                const unsigned off = (unsigned)npool;
-                for (int c = 0; c < (1 << f.nc); ++c) {
-                    const cvec sub(src.begin() + (first_block + c) * dd,
-                                   src.begin() + (first_block + c + 1) * dd);
-                    const cvec pm = f.nt > 1 ? permute_matrix(sub, f.nt, order) : sub;
-                    bool id = true;
-                    for (int r = 0; r < D; ++r)
-                        for (int s = 0; s < D; ++s)
-                            if (pm[r + s * D] != (r == s ? cplx(1) : cplx(0))) id = false;
-                    if (ident && id) *ident |= 1ull << c;
-                    for (const auto &x : pm) P.pool[npool++] = make_double2(x.real(), x.imag());
-                }
-                return off;
-            };
-            if (f.nt >= 3) {
-                // wide ops run in smem_op as sum_k diag(d_k) P_{x_k}: store the
-                // XOR patterns x_k and, per sub-matrix, d_k[r] = S[r, r ^ x_k]
-                auto permuted = [&](const cvec &src, int c) {
-                    const cvec sub(src.begin() + size_t(c) * dd, src.begin() + size_t(c + 1) * dd);
-                    return permute_matrix(sub, f.nt, order);
-                };
-                std::vector<int> X;
-                auto scan = [&](const cvec &src) {
-                    for (int c = 0; c < (1 << f.nc); ++c) {
-                        const cvec pm = permuted(src, c);
-                        for (int x = 0; x < D; ++x) {
-                            if (std::find(X.begin(), X.end(), x) != X.end()) continue;
-                            for (int r = 0; r < D; ++r)
-                                if (pm[r + size_t(r ^ x) * D] != cplx(0)) {
-                                    X.push_back(x);
-                                    break;
-                                }
-                        }
-                    }
-                };
-                scan(f.sub_phi);
-                if (f.pair) scan(f.sub_psi);
-                std::sort(X.begin(), X.end());
-                o.xoff = P.nxpat;
-                o.nx = (int)X.size();
-                for (int x : X) P.xpat[P.nxpat++] = (unsigned char)x;
-                auto pushx = [&](const cvec &src, unsigned long long *ident) {
-                    const unsigned off = (unsigned)npool;
-                    for (int c = 0; c < (1 << f.nc); ++c) {
-                        const cvec pm = permuted(src, c);
-                        bool id = true;
-                        for (int r = 0; r < D; ++r)
-                            for (int s = 0; s < D; ++s)
-                                if (pm[r + s * D] != (r == s ? cplx(1) : cplx(0))) id = false;
-                        if (id) *ident |= 1ull << c;
-                        for (int x : X)
-                            for (int r = 0; r < D; ++r) {
-                                const cplx v = pm[r + size_t(r ^ x) * D];
-                                P.pool[npool++] = make_double2(v.real(), v.imag());
-                            }
-                    }
-                    return off;
-                };
-                o.mat = pushx(f.sub_phi, &o.ident);
-                if (f.pair) o.mat_psi = pushx(f.sub_psi, &o.ident_psi);
-            } else {
-                o.mat = push(f.sub_phi, 0, &o.ident);
-                if (f.pair) o.mat_psi = push(f.sub_psi, 0, &o.ident_psi);
-            }
-            if (o.np > 0) {
-                o.mat_d = (unsigned)npool;
-                for (int p = 0; p < f.np; ++p) push(f.sub_d, size_t(p) << f.nc, nullptr);
-                o.ident = 0;
-                o.slot = nslots;
-                for (int p = 0; p < f.np; ++p) {
-                    slots.scale.push_back(f.scale);
-                    slots.dst.push_back(f.grad_base + p);
-                }
-                nslots += f.np;
-            }
-            // per-register-bit condition masks
-            for (int q = 0; q < f.nc; ++q)
-                if (o.ck[q] == 2) o.rw[o.cp[q]] |= 1 << q;
-            // diagonal steps with register-bit conditions read their tables
-            // from shared memory (phi table, [D table for a parametric step])
-            o.tab = o.tab_psi = -1;
-            const int nsub = 1 << f.nc;
-            auto push_tab = [&](const cvec &src, size_t first) {
-                const int off = P.ntab;
-                for (int c = 0; c < nsub; ++c)
-                    P.tab[P.ntab++] = make_double2(src[first + c].real(), src[first + c].imag());
-                return off;
-            };
-            if (f.nt == 0 && o.per_group) {
-                const int need = nsub * (1 + (f.pair ? 1 : 0) + (o.np == 1 ? 1 : 0));
-                if (P.ntab + need <= kMaxTab && o.np <= 1) {
-                    o.tab = push_tab(f.sub_phi, 0);
-                    if (o.np == 1) push_tab(f.sub_d, 0); // at o.tab + nsub
-                    if (f.pair) o.tab_psi = push_tab(f.sub_psi, 0);
-                }
-            }
-        }
-        sb.op_count = nops - sb.op_begin;
-        remaining.swap(deferred);
-    }
-    P.nslots = nslots;
-}
-
-struct DevMem {
-    void *p = nullptr;
-    size_t cap = 0;
-    void ensure(size_t bytes) {
-        if (bytes <= cap) return;
-        if (p) VQB_CUDA(cudaFree(p));
-        VQB_CUDA(cudaMalloc(&p, bytes));
-        cap = bytes;
-    }
-};
-
-int env_int(const char *name, int dflt) {
-    const char *v = std::getenv(name);
-    return v ? std::atoi(v) : dflt;
-}
-
-template <bool REV> size_t smem_bytes() {
-    return (size_t)kMaxTab * sizeof(double2) + (size_t)((REV ? 2 : 1) + 1) * TS * sizeof(double2) +
-           (REV ? kMaxSlots * NW * 8 : 0);
-}
-
-template <bool REV, bool WIDE> int grid_size(unsigned long long ntiles) {
-    static int per_sm = -1, nsm = 148;
-    if (per_sm < 0) {
-        int dev = 0;
-        VQB_CUDA(cudaGetDevice(&dev));
-        VQB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        VQB_CUDA(cudaFuncSetAttribute(k_regstage<REV, WIDE>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem_bytes<REV>()));
-        VQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_regstage<REV, WIDE>, T,
-                                                               smem_bytes<REV>()));
-        per_sm = std::max(per_sm, 1);
-    }
-    return (int)std::min<unsigned long long>((unsigned long long)nsm * per_sm, ntiles);
-}
-
-// Shared driver: stage planning, block fusion, lowering, launches.
-template <bool REV, typename Fallback>
-void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, double *dgrads,
-             Fallback &&fallback) {
-    const int pn = sphi->pn;
-    cudaStream_t st = sphi->stream;
-    const auto stages = plan_stages(fops, pn, K);
-    const int max_support = env_int("VQB_FUSE_QUBITS", 2);
-    const bool stats = std::getenv("VQB_PLAN_STATS") != nullptr;
-    const unsigned long long ntiles = 1ull << (pn - K);
-    const int grid = grid_size<REV, true>(ntiles);
-    // gradient slots of the whole sweep: partial[grid][total slots]
-    int total_slots = 0;
-    if (REV)
-        for (const auto &f : fops) total_slots += f.np;
-    static thread_local DevMem m_partial, m_slots;
-    if (REV && total_slots > 0) m_partial.ensure(sizeof(double) * (size_t)grid * total_slots);
-    SlotMap slots;
-    static thread_local RParams P;
-    for (const Stage &sg : stages) {
-        if (!sg.fused) {
-            fallback(fops[sg.ops[0]]);
-            continue;
-        }
-        std::vector<FusedOp> blocks;
-        if (max_support > 0) blocks = fuse_blocks(fops, sg.ops, max_support);
-        else
-            for (int idx : sg.ops) blocks.push_back(fops[idx]);
-        std::vector<int> remaining(blocks.size());
-        for (size_t i = 0; i < blocks.size(); ++i) remaining[i] = (int)i;
-        while (!remaining.empty()) {
-            lower_stage_reg(sg, blocks, remaining, pn, REV, P, slots);
-            P.partial_ld = total_slots;
-            if (stats) {
-                int nt_hist[5] = {0, 0, 0, 0, 0}, nops = 0;
-                for (int i = 0; i < P.nsubs; ++i) nops += P.subs[i].op_count;
-                for (int i = 0; i < nops; ++i) nt_hist[std::min(P.ops[i].nt, 4)]++;
-                std::fprintf(stderr, "[regstage%s] gates %zu blocks %zu subs %d ops nt0..4 %d %d %d %d %d slots %d\n",
-                             REV ? "-rev" : "", sg.ops.size(), blocks.size(), P.nsubs, nt_hist[0],
-                             nt_hist[1], nt_hist[2], nt_hist[3], nt_hist[4], P.nslots);
-            }
-            {
-                // algorithmic FP64 flops of this launch: a dense 2^nt x 2^nt
-                // complex matrix costs 8 * 2^nt flops per amplitude per state;
-                // a parametric step adds the np derivative contractions
-                double per_amp = 0;
-                int nops = 0;
-                for (int i = 0; i < P.nsubs; ++i) nops += P.subs[i].op_count;
-                for (int i = 0; i < nops; ++i) {
-                    const ROp &o = P.ops[i];
-                    const double mv = o.nt == 0 ? 6.0 : 8.0 * (1 << o.nt);
-                    per_amp += (REV ? 2.0 : 1.0) * mv + (REV ? o.np * (mv + 2.0) : 0.0);
-                }
-                note_flops(per_amp * double(1ull << pn));
-            }
-            bool wide = REV;
-            for (int i = 0; i < P.nsubs; ++i)
-                for (int o = 0; o < P.subs[i].op_count; ++o)
-                    wide = wide || P.ops[P.subs[i].op_begin + o].nt >= 3;
-            const ProfMark pf_ = prof_begin(st);
-            if (wide) {
-                k_regstage<REV, true><<<grid, T, smem_bytes<REV>(), st>>>(
-                    sphi->amps, REV ? spsi->amps : nullptr, static_cast<double *>(m_partial.p), P);
-            } else {
-                k_regstage<REV, false><<<grid_size<REV, false>(ntiles), T, smem_bytes<REV>(), st>>>(
-                    sphi->amps, REV ? spsi->amps : nullptr, static_cast<double *>(m_partial.p), P);
-            }
-            check_launch(REV ? "k_regstage_rev" : "k_regstage", pf_);
-        }
-    }
-    if (REV && total_slots > 0) {
-        if ((int)slots.scale.size() != total_slots) raise(VQB_ERR_INTERNAL, "gradient slot mismatch");
-        m_slots.ensure((sizeof(double) + sizeof(long long)) * total_slots);
-        VQB_CUDA(cudaMemcpyAsync(m_slots.p, slots.scale.data(), sizeof(double) * total_slots,
-                                 cudaMemcpyHostToDevice, st));
-        VQB_CUDA(cudaMemcpyAsync(static_cast<char *>(m_slots.p) + sizeof(double) * total_slots,
-                                 slots.dst.data(), sizeof(long long) * total_slots,
-                                 cudaMemcpyHostToDevice, st));
-        const ProfMark pf_ = prof_begin(st);
-        k_grads<<<(total_slots + 127) / 128, 128, 0, st>>>(
-            static_cast<const double *>(m_partial.p), grid, total_slots,
-            static_cast<const double *>(m_slots.p),
-            reinterpret_cast<const long long *>(static_cast<char *>(m_slots.p) +
-                                                sizeof(double) * total_slots),
-            total_slots, dgrads);
-        check_launch("k_grads", pf_);
-    }
-    VQB_CUDA(cudaStreamSynchronize(st)); // host-side slot vectors outlive the copies
-}
-
-} // namespace
-
-bool regstage_available(int pn) { return pn >= K + 2; }
-
-void run_program_reg(DeviceState *s, const std::vector<Gate> &prog) {
-    std::vector<FusedOp> fops;
-    fops.reserve(prog.size());
-    for (const auto &g : prog) fops.push_back(analyse_gate(g));
-    run_reg<false>(s, nullptr, fops, nullptr, [&](const FusedOp &f) {
-        apply_gate_fast(s->amps, s->pn, f.gate, s->stream);
-    });
-}
-
-void run_reverse_reg(DeviceState *phi, DeviceState *psi, const std::vector<RevOp> &prog,
-                     double *dgrads) {
-    std::vector<FusedOp> fops;
-    fops.reserve(prog.size());
-    for (const auto &r : prog) {
-        fops.push_back(analyse_rev(r));
-        if (fops.back().np > 0 && fops.back().nt > 2) fops.back().fusable = false;
-    }
-    run_reg<true>(phi, psi, fops, dgrads, [&](const FusedOp &f) {
-        const RevOp &r = *f.rev;
-        if (r.dmats.empty()) {
-            apply_gate_fast(phi->amps, phi->pn, r.phi_op, phi->stream);
-            apply_gate_fast(psi->amps, psi->pn, r.psi_op, phi->stream);
-        } else {
-            reverse_step_async(phi->amps, psi->amps, phi->pn, r.phi_op.pos, r.phi_op.m,
-                               r.phi_op.mat, r.dmats, phi, nullptr, dgrads + r.grad_base, r.scale);
-        }
-    });
-}
-
-} // namespace vqb
+// Register executor, 16 amplitudes per thread and state (K = 11 tile bits):
+// forward programs (two to three blocks per SM) and, by default, adjoint sweeps.
+#define VQB_RS_RB 4
+#define VQB_RS_TB 7
+#define VQB_RS_NS rs16
+#define VQB_RS_FWD_BLOCKS 3
+#define VQB_RS_REV_BLOCKS 2
+#include "regstage_impl.cuh"
