@@ -3,6 +3,9 @@
 #define VQB_RS_RB 4
 #define VQB_RS_TB 7
 #define VQB_RS_NS rs16
-#define VQB_RS_FWD_BLOCKS 3
+#ifndef VQB_RS16_FWD_BLOCKS
+#define VQB_RS16_FWD_BLOCKS 3
+#endif
+#define VQB_RS_FWD_BLOCKS VQB_RS16_FWD_BLOCKS
 #define VQB_RS_REV_BLOCKS 2
 #include "regstage_impl.cuh"

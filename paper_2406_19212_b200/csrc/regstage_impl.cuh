@@ -97,7 +97,7 @@ struct RParams {
     ROp ops[kMaxOps];
     double2 pool[kMaxPool];
     double2 tab[kMaxTab];
-    int ntab, nxpat;
+    int ntab, nxpat, npool;
     unsigned char xpat[256];
     // forward fast path: unconditioned 1- and 2-bit register ops packed as
     // (pool offset << 4) | variant (1..4: nt=1 on register bit v-1; 5..10:
@@ -315,6 +315,13 @@ template <int NT, int P0, int P1 = 0>
 __device__ __forceinline__ void apply_hoisted(double2 (&v)[R], const double2 *M) {
     using PS = Pos<NT, P0, P1, 0, 0>;
     constexpr int D = PS::D;
+#if !VQB_RS_HOIST
+    // entries re-read per group (broadcast shared-memory loads), no register copy
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+        if (!(i & PS::MASK)) group_mv<PS>(v, i, M);
+    return;
+#endif
     double2 m[D * D];
 #pragma unroll
     for (int e = 0; e < D * D; ++e) m[e] = M[e];
@@ -472,7 +479,13 @@ __device__ __forceinline__ void smem_op(double2 (&v)[R], const Addr &A, const RL
 // natural order) and re-laid out once, with no cp.async staging tile, so the
 // smaller shared-memory footprint fits more blocks per SM and the other
 // blocks' arithmetic covers each block's load.
-template <bool REV, bool WIDE> constexpr bool kStaged = REV || WIDE;
+#ifndef VQB_RS_HOIST
+#define VQB_RS_HOIST 0
+#endif
+#ifndef VQB_RS_FWD_STAGED
+#define VQB_RS_FWD_STAGED 1
+#endif
+template <bool REV, bool WIDE> constexpr bool kStaged = REV || WIDE || VQB_RS_FWD_STAGED;
 template <bool REV, bool WIDE>
 constexpr int kBlocksPerSm = REV ? VQB_RS_REV_BLOCKS : (WIDE ? 2 : VQB_RS_FWD_BLOCKS);
 
@@ -487,12 +500,15 @@ __global__ void __launch_bounds__(T, (kBlocksPerSm<REV, WIDE>))
     double2 *stab = reinterpret_cast<double2 *>(smem_raw);
     double2 *stage_buf = stab + kMaxTab;
     double2 *xbuf = STAGED ? stage_buf + NS * TS : stage_buf;
-    double *pacc = reinterpret_cast<double *>(xbuf + TS); // [nslots][NW]
+    double *pacc = reinterpret_cast<double *>(xbuf + TS); // [nslots][NW] (REV)
+    // the stage's matrix pool, read with broadcast shared-memory loads
+    double2 *spool = REV ? reinterpret_cast<double2 *>(pacc + kMaxSlots * NW) : xbuf + TS;
     const int t = threadIdx.x;
     const int lane = t & 31, warp = t >> 5;
     if (REV)
         for (int i = t; i < P.nslots * NW; i += T) pacc[i] = 0;
     for (int i = t; i < P.ntab; i += T) stab[i] = P.tab[i];
+    for (int i = t; i < P.npool; i += T) spool[i] = P.pool[i];
     __syncthreads();
 
     // natural tile order j = t + T*s: global offset glo | gh(s), slot swz(j)
@@ -600,7 +616,7 @@ __global__ void __launch_bounds__(T, (kBlocksPerSm<REV, WIDE>))
                     const int w = wnext;
                     if (o + 1 < sb.op_count) wnext = P.fast[sb.op_begin + o + 1];
                     if (w) {
-                        apply_fast(vf, P.pool, w);
+                        apply_fast(vf, spool, w);
                         continue;
                     }
                 }
@@ -613,32 +629,32 @@ __global__ void __launch_bounds__(T, (kBlocksPerSm<REV, WIDE>))
                 const int cbase = cuni | cthr;
                 if constexpr (!REV) {
                     if (!WIDE || op.nt <= 2) {
-                        dispatch<2, 2>(vf, op, P.pool, cbase, op.mat, op.ident);
+                        dispatch<2, 2>(vf, op, spool, cbase, op.mat, op.ident);
                     } else if (op.nt == 3) {
-                        smem_op<3>(vf, A, P.subs[sub].L, xbuf, op, P.pool, cuni, op.mat, op.ident, t,
+                        smem_op<3>(vf, A, P.subs[sub].L, xbuf, op, spool, cuni, op.mat, op.ident, t,
                                    P.xpat);
                     } else {
-                        smem_op<4>(vf, A, P.subs[sub].L, xbuf, op, P.pool, cuni, op.mat, op.ident, t,
+                        smem_op<4>(vf, A, P.subs[sub].L, xbuf, op, spool, cuni, op.mat, op.ident, t,
                                    P.xpat);
                     }
                 } else if (op.np == 0 && op.nt <= 2) {
-                    dispatch<1, 2>(vf, op, P.pool, cbase, op.mat, op.ident);
-                    dispatch<1, 2>(vg, op, P.pool, cbase, op.pair ? op.mat_psi : op.mat,
+                    dispatch<1, 2>(vf, op, spool, cbase, op.mat, op.ident);
+                    dispatch<1, 2>(vg, op, spool, cbase, op.pair ? op.mat_psi : op.mat,
                                    op.pair ? op.ident_psi : op.ident);
                 } else if (op.np == 0) {
                     const RLayout &Lc = P.subs[sub].L;
                     const unsigned mg = op.pair ? op.mat_psi : op.mat;
                     const unsigned long long ig = op.pair ? op.ident_psi : op.ident;
                     if (op.nt == 3) {
-                        smem_op<3>(vf, A, Lc, xbuf, op, P.pool, cuni, op.mat, op.ident, t, P.xpat);
-                        smem_op<3>(vg, A, Lc, xbuf, op, P.pool, cuni, mg, ig, t, P.xpat);
+                        smem_op<3>(vf, A, Lc, xbuf, op, spool, cuni, op.mat, op.ident, t, P.xpat);
+                        smem_op<3>(vg, A, Lc, xbuf, op, spool, cuni, mg, ig, t, P.xpat);
                     } else {
-                        smem_op<4>(vf, A, Lc, xbuf, op, P.pool, cuni, op.mat, op.ident, t, P.xpat);
-                        smem_op<4>(vg, A, Lc, xbuf, op, P.pool, cuni, mg, ig, t, P.xpat);
+                        smem_op<4>(vf, A, Lc, xbuf, op, spool, cuni, op.mat, op.ident, t, P.xpat);
+                        smem_op<4>(vg, A, Lc, xbuf, op, spool, cuni, mg, ig, t, P.xpat);
                     }
                 } else {
                     double acc[VQB_MAX_PARAMS] = {0, 0, 0, 0, 0};
-                    dispatch_param(vf, vg, op, P.pool, cbase, acc);
+                    dispatch_param(vf, vg, op, spool, cbase, acc);
 #pragma unroll
                     for (int p = 0; p < VQB_MAX_PARAMS; ++p) {
                         if (p >= op.np) break;
@@ -980,6 +996,7 @@ void lower_stage_reg(const Stage &sg, const std::vector<FusedOp> &blocks,
         remaining.swap(deferred);
     }
     P.nslots = nslots;
+    P.npool = npool;
 }
 
 struct DevMem {
@@ -998,26 +1015,34 @@ int env_int(const char *name, int dflt) {
     return v ? std::atoi(v) : dflt;
 }
 
-template <bool REV, bool WIDE = true> size_t smem_bytes() {
+// dynamic shared memory: tables | staging | relayout tile | slots (REV) or
+// the matrix pool (forward, npool entries)
+template <bool REV, bool WIDE = true> size_t smem_bytes(int npool = kMaxPool) {
     const int staging = kStaged<REV, WIDE> ? (REV ? 2 : 1) : 0;
     return (size_t)kMaxTab * sizeof(double2) + (size_t)(staging + 1) * TS * sizeof(double2) +
-           (REV ? kMaxSlots * NW * 8 : 0);
+           (REV ? kMaxSlots * NW * 8 : 0) + (size_t)npool * sizeof(double2);
 }
 
-template <bool REV, bool WIDE> int grid_size(unsigned long long ntiles) {
-    static int per_sm = -1, nsm = 148;
-    if (per_sm < 0) {
+// resident blocks (grid = SMs x blocks per SM) for a launch with `smem` bytes
+template <bool REV, bool WIDE> int grid_size(unsigned long long ntiles, size_t smem) {
+    static int nsm = -1;
+    static int per_sm[64] = {}; // by smem in KiB
+    if (nsm < 0) {
         int dev = 0;
         VQB_CUDA(cudaGetDevice(&dev));
         VQB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
         VQB_CUDA(cudaFuncSetAttribute(k_regstage<REV, WIDE>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem_bytes<REV, WIDE>()));
-        VQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_regstage<REV, WIDE>, T,
-                                                               smem_bytes<REV, WIDE>()));
-        per_sm = std::max(per_sm, 1);
     }
-    return (int)std::min<unsigned long long>((unsigned long long)nsm * per_sm, ntiles);
+    const size_t kib = std::min<size_t>((smem + 1023) / 1024, 63);
+    if (per_sm[kib] == 0) {
+        int b = 0;
+        VQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_regstage<REV, WIDE>, T,
+                                                               kib * 1024));
+        per_sm[kib] = std::max(b, 1);
+    }
+    return (int)std::min<unsigned long long>((unsigned long long)nsm * per_sm[kib], ntiles);
 }
 
 // Shared driver: stage planning, block fusion, lowering, launches.
@@ -1030,13 +1055,18 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
     const int max_support = env_int("VQB_FUSE_QUBITS", 2);
     const bool stats = std::getenv("VQB_PLAN_STATS") != nullptr;
     const unsigned long long ntiles = 1ull << (pn - K);
-    const int grid = grid_size<REV, true>(ntiles);
+    // upper bound of the per-launch grids (no pool): partial rows of blocks a
+    // launch does not run stay zero
+    const int grid = grid_size<REV, true>(ntiles, smem_bytes<REV>(0));
     // gradient slots of the whole sweep: partial[grid][total slots]
     int total_slots = 0;
     if (REV)
         for (const auto &f : fops) total_slots += f.np;
     static thread_local DevMem m_partial, m_slots;
-    if (REV && total_slots > 0) m_partial.ensure(sizeof(double) * (size_t)grid * total_slots);
+    if (REV && total_slots > 0) {
+        m_partial.ensure(sizeof(double) * (size_t)grid * total_slots);
+        VQB_CUDA(cudaMemsetAsync(m_partial.p, 0, sizeof(double) * (size_t)grid * total_slots, st));
+    }
     SlotMap slots;
     static thread_local RParams P;
     for (const Stage &sg : stages) {
@@ -1081,10 +1111,12 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
                     wide = wide || P.ops[P.subs[i].op_begin + o].nt >= 3;
             const ProfMark pf_ = prof_begin(st);
             if (wide) {
-                k_regstage<REV, true><<<grid, T, smem_bytes<REV>(), st>>>(
+                const size_t sm = smem_bytes<REV>(P.npool);
+                k_regstage<REV, true><<<grid_size<REV, true>(ntiles, sm), T, sm, st>>>(
                     sphi->amps, REV ? spsi->amps : nullptr, static_cast<double *>(m_partial.p), P);
             } else {
-                k_regstage<REV, false><<<grid_size<REV, false>(ntiles), T, smem_bytes<REV, false>(), st>>>(
+                const size_t sm = smem_bytes<REV, false>(P.npool);
+                k_regstage<REV, false><<<grid_size<REV, false>(ntiles, sm), T, sm, st>>>(
                     sphi->amps, REV ? spsi->amps : nullptr, static_cast<double *>(m_partial.p), P);
             }
             check_launch(REV ? "k_regstage_rev" : "k_regstage", pf_);
