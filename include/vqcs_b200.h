@@ -231,6 +231,47 @@ VQB_API int vqb_gradient_mixed(const vqb_op *ops, int64_t count,
                                int64_t capacity, int64_t *num_grads,
                                double *reverse_residual);
 
+/* ---- measurement: circuit.hpp:303-375 ---- */
+/* measure(state, qubit, rng) (circuit.hpp:303-337 pure, :339-375 mixed):
+ * p1 = sum over basis states with bit (qubit-1) set of |a_k|^2 (pure) or
+ * rho_kk (mixed), clamped to [0,1]; p0 = clamp(1 - p1); outcome =
+ * (uniform < p1); the state collapses in place (scale 1/sqrt(p) pure, 1/p
+ * mixed) and *probability = p of the drawn outcome. `uniform` is the value
+ * the reference draws from its stream (detail::uniform_unit, circuit.hpp:288:
+ * (rng() >> 11) * 2^-53); the C++ facade draws it from the caller's
+ * std::mt19937_64, so outcomes follow the same stream. Errors: INDEX (bad
+ * qubit), DEGENERATE (both probabilities vanish / drawn outcome has p = 0). */
+VQB_API int vqb_measure(vqb_state *st, int32_t qubit, double uniform, int32_t *outcome,
+                        double *probability);
+/* The two halves of vqb_measure, for sharded states (per-rank partial p1,
+ * all-reduced by the caller): the unclamped local p1, and the collapse of
+ * qubit to `outcome` with scale 1/sqrt(p) (pure) or 1/p (mixed). */
+VQB_API int vqb_measure_probability(const vqb_state *st, int32_t qubit, double *p1);
+VQB_API int vqb_collapse(vqb_state *st, int32_t qubit, int32_t outcome, double probability);
+
+/* ---- state dump I/O: io.hpp:40-128 ---- */
+/* save_state (io.hpp:56-82): "VQCS" | u32 version 1 | u32 n | u8 precision
+ * (2 = complex double) | 2^n little-endian (re, im) doubles. Pure states only
+ * (TYPE for a density matrix); the state is streamed from the device in
+ * chunks through a pinned buffer. IO on open/write failure. */
+VQB_API int vqb_state_save(const vqb_state *st, const char *path);
+/* load_state (io.hpp:84-128) into a new device pure state; *precision
+ * (nullable) receives the file's precision tag (1 or 2). IO errors exactly as
+ * the reference: bad magic, unsupported version, qubit count out of range,
+ * unknown precision tag, truncated payload. */
+VQB_API int vqb_state_load(const char *path, vqb_state **out, int32_t *precision);
+
+/* ---- circuit fusion: circuit.hpp:199-276 ---- */
+/* fuse_gates: absorbs single-qubit gates into the next (else the previous)
+ * two-qubit gate acting on the same qubit; every surviving gate becomes a
+ * non-parametric generic gate. UNSUPPORTED for circuits with channels.
+ * Two-phase: with cap == 0 only *num_out and *num_entries (total matrix
+ * entries) are set; otherwise out_ops[0..*num_out) are written with
+ * out_ops[i].matrix pointing into out_matrices (matrices back to back). */
+VQB_API int vqb_fuse_gates(const vqb_op *ops, int64_t count, int64_t cap, vqb_op *out_ops,
+                           int64_t matrix_cap, vqb_c128 *out_matrices, int64_t *num_out,
+                           int64_t *num_entries);
+
 /* ---- host-only planning (no device work; no reference analogue) ---- */
 /* Plans the fused execution of a circuit exactly as vqb_apply_circuit does
  * (stage packing into 2^tile_bits tiles, then block fusion on at most

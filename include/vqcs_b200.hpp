@@ -12,6 +12,9 @@
 //   vqcs::apply_operator  (observables.hpp:216-237)-> vqb::apply_operator
 //   vqcs::loss_pure / gradient_pure   (autodiff.hpp:80-156)  -> vqb::...
 //   vqcs::loss_mixed / gradient_mixed (autodiff.hpp:160-329) -> vqb::...
+//   vqcs::measure         (circuit.hpp:303-385)    -> vqb::measure
+//   vqcs::fuse_gates      (circuit.hpp:199-276)    -> vqb::fuse_gates
+//   vqcs::save_state / load_state (io.hpp:56-128)  -> vqb::save_state / load_state
 //
 // States stay host objects (as in the reference); each call uploads the state,
 // runs on the B200 and downloads the result. vqb::DeviceState keeps a state
@@ -24,6 +27,7 @@
 
 #include <complex>
 #include <memory>
+#include <random>
 #include <span>
 #include <string>
 #include <vector>
@@ -31,6 +35,7 @@
 #include "vqcs/autodiff.hpp"
 #include "vqcs/circuit.hpp"
 #include "vqcs/errors.hpp"
+#include "vqcs/io.hpp"
 #include "vqcs/observables.hpp"
 #include "vqcs/state.hpp"
 #include "vqcs_b200.h"
@@ -165,8 +170,13 @@ class DeviceState {
         check(vqb_state_download(s_, reinterpret_cast<vqb_c128 *>(a.data()), a.size()));
     }
     vqb_state *get() const { return s_; }
+    // adopt a handle created by the library (vqb_state_load)
+    static std::unique_ptr<DeviceState> adopt(vqb_state *s) {
+        return std::unique_ptr<DeviceState>(new DeviceState(s));
+    }
 
   private:
+    explicit DeviceState(vqb_state *s) : s_(s) {}
     vqb_state *s_ = nullptr;
 };
 
@@ -271,6 +281,71 @@ inline vqcs::GradientResult gradient_mixed(const vqcs::PauliOperator &op,
                                            const vqcs::MixedState<double> &dm0,
                                            vqcs::GradientDiagnostics *diag = nullptr) {
     return detail::gradient(vqb_gradient_mixed, op, c, dm0, diag);
+}
+
+// ---- measure (circuit.hpp:303-385): the uniform is drawn from the caller's
+// stream exactly as the reference draws it (detail::uniform_unit), so the
+// same std::mt19937_64 yields the same outcomes ----
+inline vqcs::MeasurementOutcome measure(DeviceState &s, int qubit, std::mt19937_64 &rng) {
+    const double u = vqcs::detail::uniform_unit(rng);
+    int32_t outcome = 0;
+    double p = 0;
+    check(vqb_measure(s.get(), qubit, u, &outcome, &p));
+    return {outcome, p};
+}
+
+inline vqcs::MeasurementOutcome measure(vqcs::PureState<double> &state, int qubit,
+                                        std::mt19937_64 &rng) {
+    DeviceState d(state);
+    const auto r = measure(d, qubit, rng);
+    d.download(state.amplitudes());
+    return r;
+}
+
+inline vqcs::MeasurementOutcome measure(vqcs::MixedState<double> &dm, int qubit,
+                                        std::mt19937_64 &rng) {
+    DeviceState d(dm);
+    const auto r = measure(d, qubit, rng);
+    d.download(dm.entries());
+    return r;
+}
+
+// ---- fuse_gates (circuit.hpp:199-276) ----
+inline vqcs::Circuit<double> fuse_gates(const vqcs::Circuit<double> &c) {
+    const auto L = lower(c);
+    int64_t nout = 0, nent = 0;
+    check(vqb_fuse_gates(L.ops.data(), static_cast<int64_t>(L.ops.size()), 0, nullptr, 0, nullptr,
+                         &nout, &nent));
+    std::vector<vqb_op> ops(static_cast<size_t>(std::max<int64_t>(nout, 1)));
+    std::vector<std::complex<double>> mats(static_cast<size_t>(std::max<int64_t>(nent, 1)));
+    check(vqb_fuse_gates(L.ops.data(), static_cast<int64_t>(L.ops.size()),
+                         static_cast<int64_t>(ops.size()), ops.data(),
+                         static_cast<int64_t>(mats.size()),
+                         reinterpret_cast<vqb_c128 *>(mats.data()), &nout, &nent));
+    vqcs::Circuit<double> out;
+    for (int64_t i = 0; i < nout; ++i) {
+        const vqb_op &o = ops[static_cast<size_t>(i)];
+        const size_t d = size_t(1) << o.num_positions;
+        const auto *m = reinterpret_cast<const std::complex<double> *>(o.matrix);
+        out.push_back(vqcs::make_gate<double>(
+            std::vector<int>(o.positions, o.positions + o.num_positions),
+            vqcs::cvector<double>(m, m + d * d)));
+    }
+    return out;
+}
+
+// ---- state dumps (io.hpp:56-128), device-resident states ----
+inline void save_state(const DeviceState &s, const std::string &path) {
+    check(vqb_state_save(s.get(), path.c_str()));
+}
+
+inline std::unique_ptr<DeviceState> load_state(const std::string &path,
+                                               vqcs::Precision *precision = nullptr) {
+    vqb_state *h = nullptr;
+    int32_t prec = 0;
+    check(vqb_state_load(path.c_str(), &h, &prec));
+    if (precision) *precision = static_cast<vqcs::Precision>(prec);
+    return DeviceState::adopt(h);
 }
 
 } // namespace vqb

@@ -68,3 +68,21 @@ def checker() -> Engine:
 
 def set_reference_threads(t: int) -> None:
     reference().lib.vqcsref_set_num_threads(int(t))
+
+
+def reference_uniform(seed: int, skip: int = 0) -> float:
+    """The uniform the reference's measure() draws from std::mt19937_64(seed)
+    after `skip` draws (circuit.hpp:287-290)."""
+    u = ct.c_double()
+    rc = reference().lib.vqcsref_uniform_unit(ct.c_uint64(seed), ct.c_uint64(skip), ct.byref(u))
+    reference().check(rc)
+    return u.value
+
+
+def reference_measure(state, qubit: int, seed: int, skip: int = 0):
+    """The reference's own measure() on std::mt19937_64(seed) -> (outcome, p)."""
+    eng = reference()
+    o, p = ct.c_int32(), ct.c_double()
+    eng.check(eng.lib.vqcsref_measure_seeded(state.handle, qubit, ct.c_uint64(seed),
+                                             ct.c_uint64(skip), ct.byref(o), ct.byref(p)))
+    return o.value, p.value

@@ -14,12 +14,14 @@
 #include <cstring>
 #include <memory>
 #include <optional>
+#include <random>
 #include <string>
 #include <vector>
 
 #include "vqcs/autodiff.hpp"
 #include "vqcs/circuit.hpp"
 #include "vqcs/gates.hpp"
+#include "vqcs/io.hpp"
 #include "vqcs/kernels.hpp"
 #include "vqcs/observables.hpp"
 #include "vqcs/state.hpp"
@@ -458,4 +460,85 @@ REF_API int vqcsref_gate_inverse(const vqb_op *op, vqb_c128 *out) {
 
 REF_API int vqcsref_channel_superop(const vqb_op *op, vqb_c128 *out) {
     return guard([&] { from_cvec(channel_superoperator(to_channel(*op)).matrix, out); });
+}
+
+// ---- measurement (circuit.hpp:303-375) ----
+// The reference draws the outcome from a caller-supplied std::mt19937_64; the
+// C-ABI takes the drawn uniform instead. These two entry points let tests
+// reproduce a reference draw: the uniform a stream (seed, after `skip`
+// draws) yields, and measure() run on that very stream.
+REF_API int vqcsref_uniform_unit(uint64_t seed, uint64_t skip, double *u) {
+    return guard([&] {
+        std::mt19937_64 rng(seed);
+        rng.discard(skip);
+        *u = detail::uniform_unit(rng);
+    });
+}
+
+REF_API int vqcsref_measure_seeded(RefState *s, int32_t qubit, uint64_t seed, uint64_t skip,
+                                   int32_t *outcome, double *probability) {
+    return guard([&] {
+        std::mt19937_64 rng(seed);
+        rng.discard(skip);
+        const MeasurementOutcome r =
+            s->pure ? measure(*s->pure, qubit, rng) : measure(*s->mixed, qubit, rng);
+        *outcome = r.outcome;
+        *probability = r.probability;
+    });
+}
+
+// ---- state dumps (io.hpp) ----
+REF_API int vqcsref_state_save(const RefState *s, const char *path) {
+    return guard([&] {
+        if (!s->pure) {
+            throw TypeError("save_state: only pure states can be dumped");
+        }
+        save_state(*s->pure, std::string(path));
+    });
+}
+
+REF_API int vqcsref_state_load(const char *path, RefState **out, int32_t *precision) {
+    return guard([&] {
+        const LoadedState ls = load_state(std::string(path));
+        auto s = std::make_unique<RefState>();
+        s->pure.emplace(ls.to_pure<double>());
+        if (precision) *precision = static_cast<int32_t>(ls.precision);
+        *out = s.release();
+    });
+}
+
+// ---- fuse_gates (circuit.hpp:199-276) ----
+REF_API int vqcsref_fuse_gates(const vqb_op *ops, int64_t count, int64_t cap, vqb_op *out_ops,
+                               int64_t matrix_cap, vqb_c128 *out_matrices, int64_t *num_out,
+                               int64_t *num_entries) {
+    return guard([&] {
+        const Circuit<double> fused = fuse_gates(to_circuit(ops, count));
+        std::vector<GateOp<double>> gates;
+        fused.for_each_gate([&](const GateOp<double> &g) { gates.push_back(g); });
+        int64_t entries = 0;
+        for (const auto &g : gates) entries += (int64_t)g.matrix.size();
+        *num_out = (int64_t)gates.size();
+        *num_entries = entries;
+        if (cap == 0) {
+            return;
+        }
+        if (cap < (int64_t)gates.size() || matrix_cap < entries) {
+            throw ShapeError("fuse_gates: output buffers too small");
+        }
+        int64_t off = 0;
+        for (std::size_t i = 0; i < gates.size(); ++i) {
+            vqb_op o;
+            std::memset(&o, 0, sizeof o);
+            o.elem = VQB_ELEM_GATE;
+            o.kind = static_cast<int32_t>(gates[i].kind);
+            o.num_positions = (int32_t)gates[i].positions.size();
+            for (std::size_t k = 0; k < gates[i].positions.size(); ++k) {
+                o.positions[k] = gates[i].positions[k];
+            }
+            o.matrix = out_matrices + off;
+            from_cvec(gates[i].matrix, out_matrices + off);
+            off += (int64_t)gates[i].matrix.size();
+            out_ops[i] = o;
+        }
+    });
 }

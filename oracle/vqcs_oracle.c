@@ -1269,3 +1269,221 @@ ORC_API int vqcsorc_channel_superop(const vqb_op *op, cd *out) {
     superop(&c, out);
     return VQB_OK;
 }
+
+/* ================= measurement: circuit.hpp:278-375 ================= */
+static double clamp_probability(double p) { return p < 0 ? 0.0 : (p > 1 ? 1.0 : p); } /* :283-285 */
+
+static int check_measure_qubit(const ostate *s, int32_t q) {
+    if (q < 1 || q > s->n) return fail(VQB_ERR_INDEX, "measure: qubit does not fit the state");
+    return VQB_OK;
+}
+
+/* p1 loop of measure (circuit.hpp:311-317 pure, :346-352 mixed) */
+ORC_API int vqcsorc_measure_probability(const ostate *s, int32_t q, double *p1) {
+    int rc = check_measure_qubit(s, q);
+    if (rc) return rc;
+    const uint64_t mask = (uint64_t)1 << (q - 1);
+    double p = 0;
+    if (!s->mixed) {
+        for (uint64_t k = 0; k < s->size; ++k)
+            if (k & mask) p += s->a[k].re * s->a[k].re + s->a[k].im * s->a[k].im; /* std::norm */
+    } else {
+        const uint64_t dim = (uint64_t)1 << s->n;
+        for (uint64_t k = 0; k < dim; ++k)
+            if (k & mask) p += s->a[k + k * dim].re;
+    }
+    *p1 = p;
+    return VQB_OK;
+}
+
+/* collapse loops (circuit.hpp:328-335 pure, :363-373 mixed) */
+ORC_API int vqcsorc_collapse(ostate *s, int32_t q, int32_t outcome, double p) {
+    int rc = check_measure_qubit(s, q);
+    if (rc) return rc;
+    if (outcome != 0 && outcome != 1) return fail(VQB_ERR_DOMAIN, "collapse: outcome must be 0 or 1");
+    if (!(p > 0)) return fail(VQB_ERR_DEGENERATE, "collapse: outcome probability must be > 0");
+    const uint64_t mask = (uint64_t)1 << (q - 1);
+    if (!s->mixed) {
+        const double scale = 1.0 / sqrt(p);
+        for (uint64_t k = 0; k < s->size; ++k) {
+            if (((k & mask) != 0) == (outcome == 1)) s->a[k] = C(s->a[k].re * scale, s->a[k].im * scale);
+            else s->a[k] = C(0, 0);
+        }
+    } else {
+        const double scale = 1.0 / p;
+        const uint64_t dim = (uint64_t)1 << s->n;
+        for (uint64_t col = 0; col < dim; ++col) {
+            const int col_keep = ((col & mask) != 0) == (outcome == 1);
+            for (uint64_t row = 0; row < dim; ++row) {
+                const int keep = col_keep && (((row & mask) != 0) == (outcome == 1));
+                cd *e = &s->a[row + col * dim];
+                *e = keep ? C(e->re * scale, e->im * scale) : C(0, 0);
+            }
+        }
+    }
+    return VQB_OK;
+}
+
+/* measure (circuit.hpp:303-337, :339-375) with the drawn uniform given */
+ORC_API int vqcsorc_measure(ostate *s, int32_t q, double uniform, int32_t *outcome, double *prob) {
+    double p1;
+    int rc = vqcsorc_measure_probability(s, q, &p1);
+    if (rc) return rc;
+    p1 = clamp_probability(p1);
+    const double p0 = clamp_probability(1.0 - p1);
+    if (p0 == 0 && p1 == 0) return fail(VQB_ERR_DEGENERATE, "measure: both outcome probabilities vanish");
+    const int o = uniform < p1 ? 1 : 0;
+    const double p = o == 1 ? p1 : p0;
+    if (p == 0) return fail(VQB_ERR_DEGENERATE, "measure: drawn outcome has zero probability");
+    rc = vqcsorc_collapse(s, q, o, p);
+    if (rc) return rc;
+    *outcome = o;
+    *prob = p;
+    return VQB_OK;
+}
+
+/* ================= state dumps: io.hpp:15-128 ================= */
+ORC_API int vqcsorc_state_save(const ostate *s, const char *path) { /* io.hpp:56-82 */
+    if (s->mixed) return fail(VQB_ERR_TYPE, "save_state: only pure states can be dumped");
+    FILE *f = fopen(path, "wb");
+    if (!f) return fail(VQB_ERR_IO, "save_state: cannot open file for writing");
+    const uint32_t version = 1, n = (uint32_t)s->n;
+    const uint8_t prec = 2;
+    int ok = fwrite("VQCS", 1, 4, f) == 4 && fwrite(&version, 4, 1, f) == 1 && fwrite(&n, 4, 1, f) == 1 &&
+             fwrite(&prec, 1, 1, f) == 1;
+    for (uint64_t k = 0; ok && k < s->size; ++k) {
+        const double pair[2] = {s->a[k].re, s->a[k].im};
+        ok = fwrite(pair, sizeof pair, 1, f) == 1;
+    }
+    if (fclose(f) != 0) ok = 0;
+    return ok ? VQB_OK : fail(VQB_ERR_IO, "save_state: write failed");
+}
+
+ORC_API int vqcsorc_state_load(const char *path, ostate **out, int32_t *precision) { /* io.hpp:84-128 */
+    FILE *f = fopen(path, "rb");
+    if (!f) return fail(VQB_ERR_IO, "load_state: cannot open file");
+    char magic[4] = {0, 0, 0, 0};
+    uint32_t version = 0, n = 0;
+    uint8_t prec = 0;
+    const int hdr = fread(magic, 1, 4, f) == 4 && fread(&version, 4, 1, f) == 1 && fread(&n, 4, 1, f) == 1 &&
+                    fread(&prec, 1, 1, f) == 1;
+    int rc = VQB_OK;
+    if (!hdr || memcmp(magic, "VQCS", 4) != 0) rc = fail(VQB_ERR_IO, "load_state: not a state dump (bad magic)");
+    else if (version != 1) rc = fail(VQB_ERR_IO, "load_state: unsupported format version");
+    else if (n < 1 || n > 40) rc = fail(VQB_ERR_IO, "load_state: qubit count out of range");
+    else if (prec != 1 && prec != 2) rc = fail(VQB_ERR_IO, "load_state: unknown precision tag");
+    ostate *s = NULL;
+    if (!rc) rc = vqcsorc_state_create((int32_t)n, 0, &s);
+    for (uint64_t k = 0; !rc && k < s->size; ++k) {
+        double pair[2];
+        if (fread(pair, sizeof pair, 1, f) != 1) rc = fail(VQB_ERR_IO, "load_state: truncated amplitude payload");
+        else s->a[k] = C(pair[0], pair[1]);
+    }
+    fclose(f);
+    if (rc) {
+        vqcsorc_state_destroy(s);
+        return rc;
+    }
+    if (precision) *precision = prec;
+    *out = s;
+    return VQB_OK;
+}
+
+/* ================= fuse_gates: circuit.hpp:190-276 ================= */
+static void matmul(const cd *a, const cd *b, int d, cd *c) { /* linalg.hpp:40-55 */
+    for (int i = 0; i < d * d; ++i) c[i] = C(0, 0);
+    for (int j = 0; j < d; ++j)
+        for (int k = 0; k < d; ++k) {
+            const cd bkj = b[k + j * d];
+            if (bkj.re == 0 && bkj.im == 0) continue;
+            for (int i = 0; i < d; ++i) c[i + j * d] = cadd(c[i + j * d], cmul(a[i + k * d], bkj));
+        }
+}
+
+typedef struct {
+    int m;
+    int32_t pos[VQB_MAX_POSITIONS];
+    cd *mat; /* 4^m */
+} small_gate;
+
+ORC_API int vqcsorc_fuse_gates(const vqb_op *ops, int64_t count, int64_t cap, vqb_op *out_ops,
+                               int64_t matrix_cap, cd *out_matrices, int64_t *num_out, int64_t *num_entries) {
+    for (int64_t i = 0; i < count; ++i)
+        if (ops[i].elem == VQB_ELEM_CHANNEL)
+            return fail(VQB_ERR_UNSUPPORTED, "fuse_gates: circuit contains quantum channels");
+    small_gate *flat = (small_gate *)calloc(count > 0 ? count : 1, sizeof(small_gate));
+    int64_t *merge = (int64_t *)malloc(sizeof(int64_t) * (count > 0 ? count : 1));
+    gate_t *g = (gate_t *)malloc(sizeof(gate_t));
+    int rc = VQB_OK;
+    for (int64_t i = 0; i < count && !rc; ++i) {
+        rc = build_gate(&ops[i], g);
+        if (rc) break;
+        const int dd = 1 << (2 * g->m);
+        flat[i].m = g->m;
+        memcpy(flat[i].pos, g->pos, sizeof(int32_t) * g->m);
+        flat[i].mat = (cd *)malloc(sizeof(cd) * dd);
+        memcpy(flat[i].mat, g->mat, sizeof(cd) * dd);
+    }
+    free(g);
+    int64_t nout = 0, entries = 0;
+    if (!rc) {
+        for (int64_t i = 0; i < count; ++i) { /* circuit.hpp:219-246 */
+            merge[i] = -1;
+            if (flat[i].m != 1) continue;
+            const int q = flat[i].pos[0];
+            int64_t prev = -1, next = -1;
+            for (int64_t j = i - 1; j >= 0 && prev < 0; --j)
+                for (int k = 0; k < flat[j].m; ++k)
+                    if (flat[j].pos[k] == q) prev = j;
+            for (int64_t j = i + 1; j < count && next < 0; ++j)
+                for (int k = 0; k < flat[j].m; ++k)
+                    if (flat[j].pos[k] == q) next = j;
+            if (next >= 0 && flat[next].m == 2) merge[i] = next;
+            else if (prev >= 0 && flat[prev].m == 2) merge[i] = prev;
+        }
+        for (int64_t i = 0; i < count; ++i)
+            if (merge[i] < 0) {
+                ++nout;
+                entries += (int64_t)1 << (2 * flat[i].m);
+            }
+        *num_out = nout;
+        *num_entries = entries;
+        if (cap > 0 && (cap < nout || matrix_cap < entries)) rc = fail(VQB_ERR_SHAPE, "fuse_gates: output buffers too small");
+    }
+    if (!rc && cap > 0) {
+        int64_t o = 0, off = 0;
+        for (int64_t i = 0; i < count; ++i) { /* circuit.hpp:248-275 */
+            if (merge[i] >= 0) continue;
+            const int d = 1 << flat[i].m;
+            cd cur[16], emb[16], tmp[16];
+            cd *dst = out_matrices + off;
+            memcpy(dst, flat[i].mat, sizeof(cd) * d * d);
+            if (flat[i].m == 2) {
+                memcpy(cur, flat[i].mat, sizeof cur);
+                for (int64_t k = 0; k < count; ++k) {
+                    if (merge[k] != i) continue;
+                    const cd eye[4] = {C(1, 0), C(0, 0), C(0, 0), C(1, 0)};
+                    if (flat[k].pos[0] == flat[i].pos[0]) kron(eye, 2, flat[k].mat, 2, emb); /* low bit */
+                    else kron(flat[k].mat, 2, eye, 2, emb);
+                    if (k < i) matmul(cur, emb, 4, tmp);
+                    else matmul(emb, cur, 4, tmp);
+                    memcpy(cur, tmp, sizeof cur);
+                }
+                memcpy(dst, cur, sizeof cur);
+            }
+            vqb_op op;
+            memset(&op, 0, sizeof op);
+            op.elem = VQB_ELEM_GATE;
+            op.kind = VQB_GATE_GENERIC;
+            op.num_positions = flat[i].m;
+            memcpy(op.positions, flat[i].pos, sizeof(int32_t) * flat[i].m);
+            op.matrix = dst;
+            out_ops[o++] = op;
+            off += (int64_t)d * d;
+        }
+    }
+    for (int64_t i = 0; i < count; ++i) free(flat[i].mat);
+    free(flat);
+    free(merge);
+    return rc;
+}

@@ -374,6 +374,13 @@ def bind_abi(lib: ct.CDLL, prefix: str) -> None:
         "gate_derivative": (ct.c_int, [op_p, i32, c128_p]),
         "gate_inverse": (ct.c_int, [op_p, c128_p]),
         "channel_superop": (ct.c_int, [op_p, c128_p]),
+        "measure": (ct.c_int, [vp, i32, ct.c_double, ct.POINTER(i32), dp]),
+        "measure_probability": (ct.c_int, [vp, i32, dp]),
+        "collapse": (ct.c_int, [vp, i32, i32, ct.c_double]),
+        "state_save": (ct.c_int, [vp, ct.c_char_p]),
+        "state_load": (ct.c_int, [ct.c_char_p, ct.POINTER(vp), ct.POINTER(i32)]),
+        "fuse_gates": (ct.c_int, [op_p, i64, i64, op_p, i64, c128_p, ct.POINTER(i64),
+                                  ct.POINTER(i64)]),
         # product-only
         "state_wrap": (ct.c_int, [vp, i32, i32, u64, i32, ct.POINTER(vp)]),
         "state_device_ptr": (ct.c_int, [vp, ct.POINTER(vp)]),
@@ -389,6 +396,8 @@ def bind_abi(lib: ct.CDLL, prefix: str) -> None:
                                    ct.POINTER(i64), ct.POINTER(i32), ct.POINTER(i32), c128_p]),
         # oracle-only
         "apply_gate_naive": (ct.c_int, [vp, op_p]),
+        "uniform_unit": (ct.c_int, [u64, u64, dp]),
+        "measure_seeded": (ct.c_int, [vp, i32, u64, u64, ct.POINTER(i32), dp]),
         "set_num_threads": (None, [ct.c_int]),
         "get_num_threads": (ct.c_int, []),
     }
@@ -408,5 +417,6 @@ ABI_FUNCTIONS = [
     "apply_circuit", "apply_circuit_unfused", "norm", "trace", "expectation",
     "apply_operator", "bilinear_form", "reverse_step", "loss_pure", "gradient_pure",
     "loss_mixed", "gradient_mixed", "gate_matrix", "gate_derivative", "gate_inverse",
-    "channel_superop", "plan_blocks",
+    "channel_superop", "plan_blocks", "measure", "measure_probability", "collapse",
+    "state_save", "state_load", "fuse_gates",
 ]

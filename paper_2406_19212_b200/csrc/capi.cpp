@@ -403,6 +403,117 @@ VQB_API int vqb_gradient_mixed(const vqb_op *ops, int64_t count, const vqb_pauli
     });
 }
 
+// ---- measurement (circuit.hpp:303-375) ----
+namespace {
+void check_qubit(const DeviceState *d, int32_t qubit) {
+    if (qubit < 1 || qubit > d->n)
+        raise(VQB_ERR_INDEX, "measure: qubit " + std::to_string(qubit) + " does not fit a " +
+                                 std::to_string(d->n) + "-qubit state");
+}
+double clamp_probability(double p) { return p < 0 ? 0.0 : (p > 1 ? 1.0 : p); } // :283-285
+} // namespace
+
+VQB_API int vqb_measure(vqb_state *s, int32_t qubit, double uniform, int32_t *outcome,
+                        double *probability) {
+    return guard([&] {
+        DeviceState *d = ds(s);
+        need(outcome, "outcome");
+        need(probability, "probability");
+        check_qubit(d, qubit);
+        const double p1 = clamp_probability(prob_one(d, qubit));
+        const double p0 = clamp_probability(1.0 - p1);
+        if (p0 == 0 && p1 == 0)
+            raise(VQB_ERR_DEGENERATE, "measure: both outcome probabilities vanish");
+        const int o = uniform < p1 ? 1 : 0;
+        const double p = o == 1 ? p1 : p0;
+        if (p == 0) raise(VQB_ERR_DEGENERATE, "measure: drawn outcome has zero probability");
+        collapse(d, qubit, o, d->mixed ? 1.0 / p : 1.0 / std::sqrt(p));
+        *outcome = o;
+        *probability = p;
+    });
+}
+
+VQB_API int vqb_measure_probability(const vqb_state *s, int32_t qubit, double *p1) {
+    return guard([&] {
+        DeviceState *d = ds(s);
+        need(p1, "p1");
+        check_qubit(d, qubit);
+        *p1 = prob_one(d, qubit);
+    });
+}
+
+VQB_API int vqb_collapse(vqb_state *s, int32_t qubit, int32_t outcome, double probability) {
+    return guard([&] {
+        DeviceState *d = ds(s);
+        check_qubit(d, qubit);
+        if (outcome != 0 && outcome != 1) raise(VQB_ERR_DOMAIN, "collapse: outcome must be 0 or 1");
+        if (!(probability > 0)) raise(VQB_ERR_DEGENERATE, "collapse: outcome probability must be > 0");
+        collapse(d, qubit, outcome, d->mixed ? 1.0 / probability : 1.0 / std::sqrt(probability));
+    });
+}
+
+// ---- state dumps (io.hpp:40-128) ----
+VQB_API int vqb_state_save(const vqb_state *s, const char *path) {
+    return guard([&] {
+        need(path, "path");
+        state_save(ds(s), path);
+    });
+}
+
+VQB_API int vqb_state_load(const char *path, vqb_state **out, int32_t *precision) {
+    return guard([&] {
+        need(path, "path");
+        need(out, "out");
+        int prec = 0;
+        *out = static_cast<vqb_state *>(state_load(path, &prec));
+        if (precision) *precision = prec;
+    });
+}
+
+// ---- fuse_gates (circuit.hpp:199-276) ----
+VQB_API int vqb_fuse_gates(const vqb_op *ops, int64_t count, int64_t cap, vqb_op *out_ops,
+                           int64_t matrix_cap, vqb_c128 *out_matrices, int64_t *num_out,
+                           int64_t *num_entries) {
+    return guard([&] {
+        need(num_out, "num_out");
+        need(num_entries, "num_entries");
+        if (count > 0) need(ops, "ops");
+        std::vector<Gate> flat;
+        for (int64_t i = 0; i < count; ++i) {
+            if (ops[i].elem == VQB_ELEM_CHANNEL)
+                raise(VQB_ERR_UNSUPPORTED, "fuse_gates: circuit contains quantum channels");
+        }
+        for (int64_t i = 0; i < count; ++i) flat.push_back(gate_from_op(ops[i]));
+        const std::vector<Gate> fused = fuse_gates(flat);
+        int64_t entries = 0;
+        for (const auto &g : fused) entries += (int64_t)g.mat.size();
+        *num_out = (int64_t)fused.size();
+        *num_entries = entries;
+        if (cap == 0) return;
+        if (cap < (int64_t)fused.size() || matrix_cap < entries)
+            raise(VQB_ERR_SHAPE, "fuse_gates: output buffers too small");
+        need(out_ops, "out_ops");
+        need(out_matrices, "out_matrices");
+        int64_t off = 0;
+        for (size_t i = 0; i < fused.size(); ++i) {
+            const Gate &g = fused[i];
+            vqb_op o;
+            std::memset(&o, 0, sizeof o);
+            o.elem = VQB_ELEM_GATE;
+            o.kind = VQB_GATE_GENERIC;
+            o.num_positions = g.m;
+            for (int k = 0; k < g.m; ++k) o.positions[k] = g.pos[k];
+            o.matrix = out_matrices + off;
+            for (const cplx &x : g.mat) {
+                out_matrices[off].re = x.real();
+                out_matrices[off].im = x.imag();
+                ++off;
+            }
+            out_ops[i] = o;
+        }
+    });
+}
+
 VQB_API int vqb_plan_blocks(const vqb_op *ops, int64_t count, int32_t n, int32_t mixed,
                             int32_t tile_bits, int32_t max_support, int64_t cap,
                             int64_t *num_blocks, int64_t *num_stages, int32_t *num_positions,

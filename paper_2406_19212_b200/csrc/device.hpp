@@ -66,6 +66,12 @@ void reverse_step_async(double2 *phi, double2 *psi, int pn, const int *pos1, int
                         const cvec &inv, const std::vector<cvec> &dmats, DeviceState *ws_owner,
                         double2 *out_c, double *out_r, double real_scale);
 double max_abs_diff(DeviceState *s, const double2 *a, const double2 *b);
+// measurement (circuit.hpp:303-375): unclamped P(qubit = 1), and the collapse
+double prob_one(DeviceState *s, int qubit);
+void collapse(DeviceState *s, int qubit, int outcome, double scale);
+// state dumps (io.hpp:40-128), streamed through a pinned chunk buffer
+void state_save(DeviceState *s, const char *path);
+DeviceState *state_load(const char *path, int *precision);
 
 // ---- Pauli operator packing (observables.hpp:38-110) ----
 struct PauliGroupDev {

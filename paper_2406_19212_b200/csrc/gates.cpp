@@ -440,6 +440,7 @@ cvec matmul(const cvec &a, const cvec &b, int d) {
     for (int j = 0; j < d; ++j)
         for (int k = 0; k < d; ++k) {
             const cplx bkj = b[k + j * d];
+            if (bkj == cplx(0)) continue; // linalg.hpp:46-48
             for (int i = 0; i < d; ++i) r[i + j * d] += a[i + k * d] * bkj;
         }
     return r;

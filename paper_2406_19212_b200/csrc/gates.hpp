@@ -45,6 +45,7 @@ Channel channel_from_op(const vqb_op &op);
 cvec gate_derivative(const Gate &g, int p);   // gates.hpp:543-577
 Gate gate_inverse(const Gate &g);             // gates.hpp:581-619
 cvec channel_superop(const Channel &c);       // gates.hpp:708-732
+std::vector<Gate> fuse_gates(const std::vector<Gate> &flat); // circuit.hpp:199-276
 
 // Small dense linear algebra on column-major d x d matrices.
 cvec kron(const cvec &high, int dh, const cvec &low, int dl); // linalg.hpp:75-93

@@ -431,6 +431,61 @@ cplx trace(DeviceState *s) {
     return fetch_result(s);
 }
 
+// ---- measurement (circuit.hpp:303-375) ----
+// P(bit set): pure sum_{k & mask} |a_k|^2; mixed sum_{k & mask} Re rho_kk
+// (stride dim + 1 along the diagonal of vec(rho)).
+__global__ void __launch_bounds__(kThreads) k_prob_one(const double2 *__restrict__ a,
+                                                       uint64_t count, uint64_t stride,
+                                                       uint64_t mask, int pure,
+                                                       double2 *partials, unsigned *counter,
+                                                       Epilogue ep) {
+    double2 v[1] = {make_double2(0, 0)};
+    const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count; k += step) {
+        if (!(k & mask)) continue;
+        const double2 x = a[k * stride];
+        v[0].x = pure ? fma(x.x, x.x, fma(x.y, x.y, v[0].x)) : v[0].x + x.x;
+    }
+    reduce_epilogue<1>(v, 1, partials, counter, ep);
+}
+
+// Collapse: keep entries whose bits under mask_a and mask_b (the ket and, for
+// a density matrix, the bra copy of the qubit) both equal the outcome; scale
+// the kept ones, zero the rest.
+__global__ void __launch_bounds__(kThreads) k_collapse(double2 *__restrict__ a, uint64_t size,
+                                                       uint64_t mask_a, uint64_t mask_b,
+                                                       int outcome, double scale) {
+    const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < size; k += step) {
+        const bool keep = (((k & mask_a) != 0) == (outcome == 1)) &&
+                          (((k & mask_b) != 0) == (outcome == 1));
+        const double2 x = a[k];
+        a[k] = keep ? make_double2(x.x * scale, x.y * scale) : make_double2(0, 0);
+    }
+}
+
+double prob_one(DeviceState *s, int qubit) {
+    const uint64_t mask = 1ull << (qubit - 1);
+    const uint64_t count = s->mixed ? (1ull << s->n) : s->size;
+    const uint64_t stride = s->mixed ? (1ull << s->n) + 1 : 1;
+    const unsigned g = reduce_grid(count);
+    const ProfMark pf_ = prof_begin(s->stream);
+    k_prob_one<<<g, kThreads, 0, s->stream>>>(s->amps, count, stride, mask, s->mixed ? 0 : 1,
+                                              s->ws.partials, s->ws.counter, ep_result(s));
+    check_launch("k_prob_one", pf_);
+    return fetch_result(s).real();
+}
+
+void collapse(DeviceState *s, int qubit, int outcome, double scale) {
+    const uint64_t mask_a = 1ull << (qubit - 1);
+    const uint64_t mask_b = s->mixed ? mask_a << s->n : mask_a;
+    const ProfMark pf_ = prof_begin(s->stream);
+    k_collapse<<<grid_for(s->size, kThreads, 148 * 16), kThreads, 0, s->stream>>>(
+        s->amps, s->size, mask_a, mask_b, outcome, scale);
+    check_launch("k_collapse", pf_);
+    VQB_CUDA(cudaStreamSynchronize(s->stream));
+}
+
 void dot_async(DeviceState *s, const double2 *a, const double2 *b, double2 *out_dev) {
     const unsigned g = reduce_grid(s->size);
     const ProfMark pf_ = prof_begin(s->stream);

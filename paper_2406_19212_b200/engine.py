@@ -233,6 +233,54 @@ class Engine:
     def gradient_mixed(self, op, c, dm0, with_residual=False):
         return self._gradient("gradient_mixed", op, c, dm0, with_residual)
 
+    # ---- measurement (circuit.hpp:303-375) ----
+    def measure(self, s: State, qubit: int, uniform: float):
+        """Collapse `qubit` given the reference's uniform draw -> (outcome, p)."""
+        o, p = ct.c_int32(), ct.c_double()
+        self.check(self._fn("measure")(s.handle, qubit, uniform, ct.byref(o), ct.byref(p)))
+        return o.value, p.value
+
+    def measure_probability(self, s: State, qubit: int) -> float:
+        p = ct.c_double()
+        self.check(self._fn("measure_probability")(s.handle, qubit, ct.byref(p)))
+        return p.value
+
+    def collapse(self, s: State, qubit: int, outcome: int, probability: float) -> None:
+        self.check(self._fn("collapse")(s.handle, qubit, outcome, probability))
+
+    # ---- state dumps (io.hpp) ----
+    def save_state(self, s: State, path: str) -> None:
+        self.check(self._fn("state_save")(s.handle, str(path).encode()))
+
+    def load_state(self, path: str):
+        """-> (State, precision tag)."""
+        h = ct.c_void_p()
+        prec = ct.c_int32()
+        self.check(self._fn("state_load")(str(path).encode(), ct.byref(h), ct.byref(prec)))
+        n = ct.c_int32()
+        self.check(self._fn("state_info")(h, ct.byref(n), None, None))
+        return State(self, h, n.value, False), prec.value
+
+    # ---- fuse_gates (circuit.hpp:199-276) ----
+    def fuse_gates(self, c) -> Circuit:
+        p = c.pack() if isinstance(c, Circuit) else pack_ops(c)
+        nout, nent = ct.c_int64(), ct.c_int64()
+        fn = self._fn("fuse_gates")
+        self.check(fn(p.arr, p.count, 0, None, 0, None, ct.byref(nout), ct.byref(nent)))
+        ops = (abi.vqb_op * max(nout.value, 1))()
+        mats = np.zeros(max(nent.value, 1), dtype=np.complex128)
+        self.check(fn(p.arr, p.count, max(nout.value, 1), ops, max(nent.value, 1),
+                      mats.ctypes.data_as(c128_p), ct.byref(nout), ct.byref(nent)))
+        out = Circuit()
+        off = 0
+        for i in range(nout.value):
+            m = ops[i].num_positions
+            d = 1 << m
+            out.push_back(abi.make_gate([ops[i].positions[k] for k in range(m)],
+                                        mats[off: off + d * d].copy()))
+            off += d * d
+        return out
+
     # ---- host-only planning (product library) ----
     def plan_blocks(self, c: Circuit, n: int, mixed: bool = False, tile_bits: int = 12,
                     max_support: int = 2):

@@ -6,9 +6,11 @@
 #include <cmath>
 #include <cstdio>
 #include <numbers>
+#include <random>
 
 #include "vqcs/autodiff.hpp"
 #include "vqcs/bench_circuits.hpp"
+#include "vqcs/io.hpp"
 #include "vqcs/observables.hpp"
 #include "vqcs_b200.hpp"
 
@@ -56,8 +58,43 @@ int main() {
     } catch (const NonInvertibleChannelError &) {
         threw = true;
     }
+    // fuse_gates (circuit.hpp:199-276): same gate list, same matrices
+    const Circuit<double> fr = vqcs::fuse_gates(c), fd = vqb::fuse_gates(c);
+    std::vector<GateOp<double>> gr, gd;
+    fr.for_each_gate([&](const GateOp<double> &g) { gr.push_back(g); });
+    fd.for_each_gate([&](const GateOp<double> &g) { gd.push_back(g); });
+    double fmax = gr.size() == gd.size() ? 0 : 1;
+    for (size_t i = 0; i < std::min(gr.size(), gd.size()); ++i) {
+        if (gr[i].positions != gd[i].positions) fmax = 1;
+        for (size_t k = 0; k < gr[i].matrix.size(); ++k)
+            fmax = std::max(fmax, std::abs(gr[i].matrix[k] - gd[i].matrix[k]));
+    }
+
+    // measure (circuit.hpp:303-385): identical streams give identical outcomes
+    std::mt19937_64 r1(77), r2(77);
+    PureState<double> m1 = a, m2 = a;
+    bool m_ok = true;
+    double mmax = 0;
+    for (int q = 1; q <= n; ++q) {
+        const auto x = vqcs::measure(m1, q, r1);
+        const auto y = vqb::measure(m2, q, r2);
+        m_ok = m_ok && x.outcome == y.outcome && std::abs(x.probability - y.probability) <= 1e-12;
+    }
+    for (std::uint64_t k = 0; k < m1.size(); ++k) mmax = std::max(mmax, std::abs(m1[k] - m2[k]));
+
+    // state dumps (io.hpp): a device dump loads back through the reference
+    vqb::DeviceState ds(a);
+    vqb::save_state(ds, "/tmp/vqb_facade_demo.vqcs");
+    const LoadedState ls = vqcs::load_state(std::string("/tmp/vqb_facade_demo.vqcs"));
+    double iomax = ls.num_qubits == n ? 0 : 1;
+    for (std::uint64_t k = 0; k < a.size(); ++k) iomax = std::max(iomax, std::abs(ls.amplitudes[k] - a[k]));
+
     std::printf("grad max|d|=%.3e (max|g|=%.3e) state max|d|=%.3e noisy max|d|=%.3e "
-                "non-invertible->vqcs::NonInvertibleChannelError:%d\n",
-                dmax, gmax, amax, nmax, threw);
-    return (g_ok && amax <= 1e-12 && nmax <= 1e-10 * ngmax && threw) ? 0 : 1;
+                "non-invertible->vqcs::NonInvertibleChannelError:%d fuse max|d|=%.3e "
+                "measure outcomes equal:%d max|d|=%.3e dump max|d|=%.3e\n",
+                dmax, gmax, amax, nmax, threw, fmax, m_ok, mmax, iomax);
+    return (g_ok && amax <= 1e-12 && nmax <= 1e-10 * ngmax && threw && fmax <= 1e-15 && m_ok &&
+            mmax <= 1e-12 && iomax == 0)
+               ? 0
+               : 1;
 }
