@@ -205,6 +205,24 @@ VQB_API int vqb_reverse_step(vqb_state *phi, vqb_state *psi, const int32_t *posi
                              int32_t m, const vqb_c128 *inv, const vqb_c128 *dmats,
                              int32_t np, vqb_c128 *out);
 
+/* A batch of reverse steps (the reverse loop of autodiff.hpp:130-150 with
+ * explicit matrices): each step is reverse_sweep_step (kernels.hpp:659-697). */
+typedef struct vqb_rev_step {
+    int32_t num_positions;                /* m, 1..4 (pseudo-state positions) */
+    int32_t positions[VQB_MAX_POSITIONS]; /* 1-based; first = local LSB */
+    const vqb_c128 *inv;                  /* 2^m x 2^m column-major, applied to phi and psi */
+    int32_t num_dmats;                    /* 0..VQB_MAX_PARAMS */
+    const vqb_c128 *dmats;                /* num_dmats matrices back to back */
+    int64_t grad_index;                   /* first gradient slot of this step */
+} vqb_rev_step;
+/* Runs steps[0..count) in order through the fused adjoint executor: phi <-
+ * inv phi; grads[grad_index + p] += scale * Re <psi| D_p |phi>; psi <- inv psi.
+ * Used by sharded gradients (each rank sweeps its shard between global<->local
+ * swaps, with controls on global qubits restricted on the host; the per-rank
+ * gradients are summed by one all-reduce). */
+VQB_API int vqb_reverse_sweep(vqb_state *phi, vqb_state *psi, const vqb_rev_step *steps,
+                              int64_t count, double scale, double *grads, int64_t grads_len);
+
 /* ---- losses and gradients: autodiff.hpp ---- */
 /* loss_pure (autodiff.hpp:80-89). s0 is not mutated. */
 VQB_API int vqb_loss_pure(const vqb_op *ops, int64_t count, const vqb_pauli_term *terms,

@@ -542,3 +542,31 @@ REF_API int vqcsref_fuse_gates(const vqb_op *ops, int64_t count, int64_t cap, vq
         }
     });
 }
+
+// ---- batched reverse steps: reverse_sweep_step (kernels.hpp:659-697) per step ----
+REF_API int vqcsref_reverse_sweep(RefState *phi, RefState *psi, const vqb_rev_step *steps,
+                                  int64_t count, double scale, double *grads, int64_t grads_len) {
+    return guard([&] {
+        if (phi == psi) {
+            throw UsageError("reverse_sweep: phi and psi must be distinct states");
+        }
+        for (int64_t i = 0; i < count; ++i) {
+            const vqb_rev_step &st = steps[i];
+            const std::vector<int> pos(st.positions, st.positions + st.num_positions);
+            const std::size_t d = std::size_t(1) << st.num_positions;
+            std::vector<cvector<double>> dm;
+            for (int p = 0; p < st.num_dmats; ++p) {
+                dm.push_back(to_cvec(st.dmats + p * d * d, d * d));
+            }
+            if (st.num_dmats > 0 && (st.grad_index < 0 || st.grad_index + st.num_dmats > grads_len)) {
+                throw IndexError("reverse_sweep: gradient slot out of range");
+            }
+            const auto acc = reverse_sweep_step<double>(
+                phi->amps(), psi->amps(), phi->pseudo_qubits(), pos, to_cvec(st.inv, d * d),
+                std::span<const cvector<double>>(dm), cfg());
+            for (int p = 0; p < st.num_dmats; ++p) {
+                grads[st.grad_index + p] += scale * acc[p].real();
+            }
+        }
+    });
+}

@@ -1487,3 +1487,27 @@ ORC_API int vqcsorc_fuse_gates(const vqb_op *ops, int64_t count, int64_t cap, vq
     free(merge);
     return rc;
 }
+
+/* ================= batched reverse steps (autodiff.hpp:130-150) ================= */
+ORC_API int vqcsorc_reverse_sweep(ostate *phi, ostate *psi, const vqb_rev_step *steps, int64_t count,
+                                  double scale, double *grads, int64_t grads_len) {
+    if (phi == psi) return fail(VQB_ERR_USAGE, "reverse_sweep: phi and psi must be distinct states");
+    if (phi->size != psi->size) return fail(VQB_ERR_SHAPE, "reverse_sweep: shape mismatch");
+    for (int64_t i = 0; i < count; ++i) {
+        const vqb_rev_step *st = &steps[i];
+        if (st->num_positions < 1 || st->num_positions > 4)
+            return fail(VQB_ERR_SHAPE, "reverse_sweep: steps act on 1..4 positions");
+        int rc = check_positions(st->positions, st->num_positions);
+        if (!rc) rc = check_fit(st->positions, st->num_positions, phi->pn);
+        if (rc) return rc;
+        if (st->num_dmats < 0 || st->num_dmats > VQB_MAX_PARAMS)
+            return fail(VQB_ERR_SHAPE, "reverse_sweep: at most 5 derivative matrices per step");
+        if (st->num_dmats > 0 && (st->grad_index < 0 || st->grad_index + st->num_dmats > grads_len))
+            return fail(VQB_ERR_INDEX, "reverse_sweep: gradient slot out of range");
+        cd acc[VQB_MAX_PARAMS];
+        reverse_step_raw(phi->a, psi->a, phi->pn, st->positions, st->num_positions, st->inv, st->dmats,
+                         st->num_dmats, acc);
+        for (int p = 0; p < st->num_dmats; ++p) grads[st->grad_index + p] += scale * acc[p].re;
+    }
+    return VQB_OK;
+}

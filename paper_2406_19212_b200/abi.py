@@ -77,6 +77,19 @@ class vqb_op(ct.Structure):
     ]
 
 
+class vqb_rev_step(ct.Structure):
+    """One reverse step (reverse_sweep_step kernels.hpp:659-697) with explicit
+    matrices, for vqb_reverse_sweep."""
+    _fields_ = [
+        ("num_positions", ct.c_int32),
+        ("positions", ct.c_int32 * MAX_POSITIONS),
+        ("inv", c128_p),
+        ("num_dmats", ct.c_int32),
+        ("dmats", c128_p),
+        ("grad_index", ct.c_int64),
+    ]
+
+
 class vqb_pauli_term(ct.Structure):
     _fields_ = [
         ("coeff", c128),
@@ -381,6 +394,7 @@ def bind_abi(lib: ct.CDLL, prefix: str) -> None:
         "state_load": (ct.c_int, [ct.c_char_p, ct.POINTER(vp), ct.POINTER(i32)]),
         "fuse_gates": (ct.c_int, [op_p, i64, i64, op_p, i64, c128_p, ct.POINTER(i64),
                                   ct.POINTER(i64)]),
+        "reverse_sweep": (ct.c_int, [vp, vp, ct.POINTER(vqb_rev_step), i64, ct.c_double, dp, i64]),
         # product-only
         "state_wrap": (ct.c_int, [vp, i32, i32, u64, i32, ct.POINTER(vp)]),
         "state_device_ptr": (ct.c_int, [vp, ct.POINTER(vp)]),
@@ -418,5 +432,5 @@ ABI_FUNCTIONS = [
     "apply_operator", "bilinear_form", "reverse_step", "loss_pure", "gradient_pure",
     "loss_mixed", "gradient_mixed", "gate_matrix", "gate_derivative", "gate_inverse",
     "channel_superop", "plan_blocks", "measure", "measure_probability", "collapse",
-    "state_save", "state_load", "fuse_gates",
+    "state_save", "state_load", "fuse_gates", "reverse_sweep",
 ]

@@ -403,6 +403,74 @@ VQB_API int vqb_gradient_mixed(const vqb_op *ops, int64_t count, const vqb_pauli
     });
 }
 
+// ---- batched reverse steps (autodiff.hpp:130-150 with explicit matrices) ----
+VQB_API int vqb_reverse_sweep(vqb_state *phi, vqb_state *psi, const vqb_rev_step *steps,
+                              int64_t count, double scale, double *grads, int64_t grads_len) {
+    return guard([&] {
+        DeviceState *a = ds(phi), *b = ds(psi);
+        if (a == b) raise(VQB_ERR_USAGE, "reverse_sweep: phi and psi must be distinct states");
+        if (a->size != b->size) raise(VQB_ERR_SHAPE, "reverse_sweep: shape mismatch");
+        if (count > 0) need(steps, "steps");
+        std::vector<RevOp> prog;
+        prog.reserve((size_t)count);
+        bool any_param = false;
+        for (int64_t i = 0; i < count; ++i) {
+            const vqb_rev_step &st = steps[i];
+            const int m = st.num_positions;
+            if (m < 1 || m > 4) raise(VQB_ERR_SHAPE, "reverse_sweep: steps act on 1..4 positions");
+            check_positions(st.positions, m, "reverse_sweep");
+            check_fit(st.positions, m, a->pn);
+            need(st.inv, "inv");
+            if (st.num_dmats < 0 || st.num_dmats > VQB_MAX_PARAMS)
+                raise(VQB_ERR_SHAPE, "reverse_sweep: at most 5 derivative matrices per step");
+            const size_t dd = size_t(1) << (2 * m);
+            RevOp r;
+            r.phi_op.m = m;
+            for (int k = 0; k < m; ++k) r.phi_op.pos[k] = st.positions[k];
+            r.phi_op.mat.resize(dd);
+            for (size_t e = 0; e < dd; ++e) r.phi_op.mat[e] = cplx(st.inv[e].re, st.inv[e].im);
+            r.psi_op = r.phi_op;
+            if (st.num_dmats > 0) {
+                need(st.dmats, "dmats");
+                need(grads, "grads");
+                if (st.grad_index < 0 || st.grad_index + st.num_dmats > grads_len)
+                    raise(VQB_ERR_INDEX, "reverse_sweep: gradient slot out of range");
+                for (int p = 0; p < st.num_dmats; ++p) {
+                    cvec d(dd);
+                    for (size_t e = 0; e < dd; ++e)
+                        d[e] = cplx(st.dmats[p * dd + e].re, st.dmats[p * dd + e].im);
+                    r.dmats.push_back(std::move(d));
+                }
+                r.grad_base = st.grad_index;
+                r.scale = scale;
+                any_param = true;
+            }
+            prog.push_back(std::move(r));
+        }
+        double *dg = nullptr;
+        if (any_param) {
+            VQB_CUDA(cudaMalloc(&dg, sizeof(double) * (size_t)grads_len + 16));
+            VQB_CUDA(cudaMemsetAsync(dg, 0, sizeof(double) * (size_t)grads_len, a->stream));
+        }
+        struct Free {
+            double *p;
+            ~Free() {
+                if (p) cudaFree(p);
+            }
+        } free_dg{dg};
+        sync(b);
+        run_reverse(a, b, prog, dg, true);
+        sync(a);
+        if (any_param) {
+            std::vector<double> h((size_t)grads_len);
+            VQB_CUDA(cudaMemcpy(h.data(), dg, sizeof(double) * (size_t)grads_len,
+                                cudaMemcpyDeviceToHost));
+            for (const RevOp &r : prog)
+                for (size_t p = 0; p < r.dmats.size(); ++p) grads[r.grad_base + p] += h[r.grad_base + p];
+        }
+    });
+}
+
 // ---- measurement (circuit.hpp:303-375) ----
 namespace {
 void check_qubit(const DeviceState *d, int32_t qubit) {

@@ -188,9 +188,17 @@ Gate on_union(const std::vector<int> &U, cvec mat) {
 // A unitary non-parametric step (same matrix on both states) may be folded
 // into an adjacent parametric step when their supports overlap and the union
 // has at most two qubits.
+bool is_unitary(const cvec &a, int d) {
+    const cvec p = matmul(adjoint(a, d), a, d);
+    for (int j = 0; j < d; ++j)
+        for (int i = 0; i < d; ++i)
+            if (std::abs(p[i + j * d] - (i == j ? cplx(1) : cplx(0))) > 1e-12) return false;
+    return true;
+}
+
 bool foldable(const RevOp &x, const RevOp &p) {
     return x.dmats.empty() && x.phi_op.mat == x.psi_op.mat && overlaps(x.phi_op, p.phi_op) &&
-           union_of(x.phi_op, p.phi_op).size() <= 2;
+           union_of(x.phi_op, p.phi_op).size() <= 2 && is_unitary(x.phi_op.mat, x.phi_op.dim());
 }
 
 } // namespace

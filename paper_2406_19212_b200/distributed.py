@@ -24,6 +24,17 @@ Reductions (norm, Z-string expectations): rank-local partials + one
 all-reduce. ``gather`` returns the full state in the canonical (logical) order,
 un-permuting the qubit map bit-exactly.
 
+Adjoint gradients (``gradient_pure``, Algorithm 2 of autodiff.hpp:95-156):
+the forward pass and the loss as above; the costate Psi = H|Phi> is built per
+rank (Z factors on global qubits fold into a rank sign, X/Y factors are
+swapped local first); Psi is a second shard that follows every swap of Phi (one
+qubit map for both). The reverse loop walks the elements backwards; runs of
+local steps (inverse and derivative matrices restricted on global condition
+bits) go to the local engine as one batched reverse sweep (vqb_reverse_sweep,
+the fused adjoint executor), a mixing bit on a global qubit swaps both shards
+first. Each rank accumulates its partial gradient vector; one all-reduce sums
+them at the end.
+
 The local engine is any include/vqcs_b200.h implementation exposing
 ``wrap(tensor)``: the CUDA library on GPUs (``vqb_state_wrap`` over the shard's
 device memory, no copy). Tests may pass a CPU engine.
@@ -95,6 +106,7 @@ class ShardedState:
         self.local = tensor  # complex128 tensor of 2^n_loc amplitudes
         self.log2phys = list(range(n))  # logical qubit (0-based) -> physical bit
         self.chunk = chunk_amps
+        self.followers: list = []  # extra shards (the adjoint costate) sharing the qubit map
         self.swaps = 0
         self.bytes_exchanged = 0
         self._gate_matrix = engine.gate_matrix
@@ -135,21 +147,22 @@ class ShardedState:
         mine = (self.rank >> j) & 1
         # local amplitudes with bit lpos == 1 - mine go to the partner, which
         # sends back its amplitudes with bit lpos == mine
-        v = self.local.view(-1, 2, 1 << lpos)  # [hi, bit lpos, lo]
-        send_half = v[:, 1 - mine, :]
-        hi, lo = v.shape[0], v.shape[2]
-        rows_per_chunk = max(1, self.chunk // lo)
-        for r0 in range(0, hi, rows_per_chunk):
-            r1 = min(hi, r0 + rows_per_chunk)
-            sbuf = torch.view_as_real(send_half[r0:r1].contiguous())
-            rbuf = torch.empty_like(sbuf)
-            if self.world > 1:
-                ops = [self.dist.P2POp(self.dist.isend, sbuf, partner),
-                       self.dist.P2POp(self.dist.irecv, rbuf, partner)]
-                for req in self.dist.batch_isend_irecv(ops):
-                    req.wait()
-            send_half[r0:r1] = torch.view_as_complex(rbuf)
-            self.bytes_exchanged += sbuf.numel() * 8
+        for shard in [self.local] + self.followers:
+            v = shard.view(-1, 2, 1 << lpos)  # [hi, bit lpos, lo]
+            send_half = v[:, 1 - mine, :]
+            hi, lo = v.shape[0], v.shape[2]
+            rows_per_chunk = max(1, self.chunk // lo)
+            for r0 in range(0, hi, rows_per_chunk):
+                r1 = min(hi, r0 + rows_per_chunk)
+                sbuf = torch.view_as_real(send_half[r0:r1].contiguous())
+                rbuf = torch.empty_like(sbuf)
+                if self.world > 1:
+                    ops = [self.dist.P2POp(self.dist.isend, sbuf, partner),
+                           self.dist.P2POp(self.dist.irecv, rbuf, partner)]
+                    for req in self.dist.batch_isend_irecv(ops):
+                        req.wait()
+                send_half[r0:r1] = torch.view_as_complex(rbuf)
+                self.bytes_exchanged += sbuf.numel() * 8
         # logical qubits on the two physical bits trade places
         a = self.log2phys.index(gpos)
         b = self.log2phys.index(lpos)
@@ -215,10 +228,9 @@ class ShardedState:
             self.engine.local_norm_sq(self)
         return math.sqrt(self._allreduce(complex(local, 0)).real)
 
-    def expectation(self, op: PauliOperator) -> complex:
-        """Sum of Z-strings (any qubits, global ones fold into a sign) and, for
-        X/Y factors, local qubits only (global X/Y factors are swapped local
-        first)."""
+    def _local_operator(self, op: PauliOperator) -> PauliOperator:
+        """This rank's share of a Pauli sum: X/Y factors made local (swaps),
+        Z factors on global qubits folded into the rank's sign."""
         # every qubit carrying an X or Y factor in any term must be local; swap
         # global ones with local bits whose qubits carry no X/Y factor at all
         xy = {q - 1 for t in op.terms for q, l in t.factors if str(l).lower() in "xy"}
@@ -241,8 +253,93 @@ class ShardedState:
                 else:
                     factors.append((p + 1, l))
             local_terms.append(PauliTerm(factors, sign * complex(t.coeff)))
-        part = self.engine.local_expectation(self, PauliOperator(local_terms))
+        return PauliOperator(local_terms)
+
+    def expectation(self, op: PauliOperator) -> complex:
+        """Sum of Z-strings (any qubits, global ones fold into a sign) and, for
+        X/Y factors, local qubits only (global X/Y factors are swapped local
+        first)."""
+        part = self.engine.local_expectation(self, self._local_operator(op))
         return self._allreduce(part)
+
+    # ---------------------------------------------------------------- adjoint
+    def _local_step(self, inv: np.ndarray, dmats: list, positions: list):
+        """Restrict a reverse step to this rank: -> (local positions, inv,
+        dmats) or None when it is the identity with no parameters."""
+        m = len(positions)
+        phys = [self.log2phys[p - 1] for p in positions]
+        fixed = {b: (self.rank >> (phys[b] - self.n_loc)) & 1
+                 for b in range(m) if phys[b] >= self.n_loc}
+
+        def sub(mat):
+            if fixed:
+                return _restrict(mat, m, fixed)
+            return np.asarray(mat).reshape(1 << m, 1 << m, order="F")
+
+        keep = [b for b in range(m) if b not in fixed]
+        inv_r = sub(inv)
+        d_r = [sub(d) for d in dmats]
+        if not keep:  # fully global diagonal: scalars on this rank (as a 1-bit op)
+            eye = np.eye(2, dtype=np.complex128)
+            return ([1], (inv_r[0, 0] * eye).reshape(-1, order="F"),
+                    [(d[0, 0] * eye).reshape(-1, order="F") for d in d_r])
+        if not d_r and np.array_equal(inv_r, np.eye(inv_r.shape[0])):
+            return None
+        return ([phys[b] + 1 for b in keep], np.ascontiguousarray(inv_r.reshape(-1, order="F")),
+                [np.ascontiguousarray(d.reshape(-1, order="F")) for d in d_r])
+
+    def gradient_pure(self, op: PauliOperator, circuit: Circuit, lookahead: int = 64):
+        """gradient_pure (autodiff.hpp:95-156) on the shard: the state held
+        now is s0; on return it holds the reverse-swept Phi (= s0 up to
+        rounding). -> (loss, grads) on every rank."""
+        import torch
+        elems = list(circuit.elements)
+        if any(isinstance(e, ChannelOp) for e in elems):
+            raise UnsupportedError("gradient_pure: noisy circuits need gradient_mixed")
+        base, total = [], 0
+        for e in elems:  # parameter order: traversal, then in-gate (circuit.hpp:149-159)
+            base.append(total)
+            total += e.num_active_params()
+        self.apply_circuit(circuit, lookahead)
+        loss = self.expectation(op).real
+        psi = torch.empty_like(self.local)
+        self.engine.local_apply_operator(self, self._local_operator(op), psi)
+        self.followers = [psi]
+        grads = np.zeros(max(total, 1), dtype=np.float64)
+        steps: list = []
+        try:
+            for i in range(len(elems) - 1, -1, -1):
+                e = elems[i]
+                inv = self.engine.gate_inverse(e)
+                dmats = [self.engine.gate_derivative(e, p)
+                         for p in range(len(e.is_param)) if e.is_param[p]]
+                m = len(e.positions)
+                mix = set(_mixing_bits(inv, m))
+                for d in dmats:
+                    mix.update(_mixing_bits(d, m))
+                phys = [self.log2phys[p - 1] for p in e.positions]
+                for b in sorted(mix):
+                    if phys[b] >= self.n_loc:
+                        self.engine.reverse_sweep(self, psi, steps, grads)
+                        steps = []
+                        soon = set()
+                        for f in elems[max(0, i - lookahead): i]:
+                            soon.update(self.log2phys[p - 1] for p in f.positions)
+                        cands = [l for l in range(self.n_loc - 1, -1, -1) if l not in phys]
+                        pick = next((l for l in cands if l not in soon), cands[0])
+                        self._swap(phys[b], pick)
+                        phys = [self.log2phys[p - 1] for p in e.positions]
+                st = self._local_step(inv, dmats, list(e.positions))
+                if st is not None:
+                    steps.append((st[0], st[1], st[2], base[i]))
+            self.engine.reverse_sweep(self, psi, steps, grads)
+        finally:
+            self.followers = []
+        if self.world > 1:
+            t = torch.from_numpy(grads).to(self.local.device)
+            self.dist.all_reduce(t)
+            grads = t.cpu().numpy()
+        return loss, grads[:total]
 
 
 class DeviceEngine:
@@ -281,3 +378,39 @@ class DeviceEngine:
         v = self.eng.expectation(op, s)
         s.free()
         return v
+
+    def gate_inverse(self, g):
+        return self.eng.gate_inverse(g)
+
+    def gate_derivative(self, g, p):
+        return self.eng.gate_derivative(g, p)
+
+    def local_apply_operator(self, st: ShardedState, op: PauliOperator, out) -> None:
+        """out <- op |shard> (apply_operator observables.hpp:216-237) on device."""
+        import torch
+        torch.cuda.current_stream().synchronize()
+        src = self._wrap(st)
+        dst = self._wrap_tensor(st, out)
+        self.eng.check(self.eng._fn("apply_operator")(src.handle, dst.handle, *op.pack()[:2]))
+        src.free()
+        dst.free()
+
+    def _wrap_tensor(self, st: ShardedState, tensor):
+        import ctypes as ct
+        from .engine import State
+        h = ct.c_void_p()
+        self.eng.check(self.eng._fn("state_wrap")(ct.c_void_p(tensor.data_ptr()), st.n_loc, 0,
+                                                  ct.c_uint64(st.rank << st.n_loc), st.g,
+                                                  ct.byref(h)))
+        return State(self.eng, h, st.n_loc, False)
+
+    def reverse_sweep(self, st: ShardedState, psi, steps, grads) -> None:
+        if not steps:
+            return
+        import torch
+        torch.cuda.current_stream().synchronize()
+        a = self._wrap(st)
+        b = self._wrap_tensor(st, psi)
+        self.eng.reverse_sweep(a, b, steps, 2.0, grads)  # grads = 2 Re(acc) (autodiff.hpp:147-149)
+        a.free()
+        b.free()

@@ -196,6 +196,30 @@ class Engine:
                                             out))
         return [complex(out[i].re, out[i].im) for i in range(len(dmats))]
 
+    def reverse_sweep(self, phi: State, psi: State, steps, scale: float, grads: np.ndarray) -> None:
+        """Batched reverse steps; steps = [(positions, inv, [dmats], grad_index)],
+        grads (float64, C-contiguous) accumulates scale * Re<psi|D|phi>."""
+        keep = []
+        arr = (abi.vqb_rev_step * max(len(steps), 1))()
+        for i, (pos, inv, dmats, gidx) in enumerate(steps):
+            st = arr[i]
+            st.num_positions = len(pos)
+            for k, q in enumerate(pos):
+                st.positions[k] = int(q)
+            iv = abi.as_c128_array(inv)
+            keep.append(iv)
+            st.inv = abi.c128_ptr(iv)
+            st.num_dmats = len(dmats)
+            if dmats:
+                dm = np.ascontiguousarray(np.concatenate([abi.as_c128_array(d) for d in dmats]))
+                keep.append(dm)
+                st.dmats = abi.c128_ptr(dm)
+            st.grad_index = int(gidx)
+        assert grads.dtype == np.float64 and grads.flags.c_contiguous
+        self.check(self._fn("reverse_sweep")(phi.handle, psi.handle, arr, len(steps), float(scale),
+                                             grads.ctypes.data_as(ct.POINTER(ct.c_double)),
+                                             grads.size))
+
     # ---- losses / gradients ----
     def loss_pure(self, op: PauliOperator, c: Circuit, s0: State) -> float:
         p = c.pack()

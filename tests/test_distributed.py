@@ -38,6 +38,25 @@ class OracleEngine:
     def local_expectation(self, st, op):
         return self.o.expectation(op, self.o.from_amplitudes(st.local.numpy()))
 
+    def gate_inverse(self, g):
+        return self.o.gate_inverse(g)
+
+    def gate_derivative(self, g, p):
+        return self.o.gate_derivative(g, p)
+
+    def local_apply_operator(self, st, op, out):
+        r = self.o.apply_operator(op, self.o.from_amplitudes(st.local.numpy()))
+        out.copy_(torch.from_numpy(self.o.download(r)))
+
+    def reverse_sweep(self, st, psi, steps, grads):
+        if not steps:
+            return
+        a = self.o.from_amplitudes(st.local.numpy())
+        b = self.o.from_amplitudes(psi.numpy())
+        self.o.reverse_sweep(a, b, steps, 2.0, grads)
+        st.local.copy_(torch.from_numpy(self.o.download(a)))
+        psi.copy_(torch.from_numpy(self.o.download(b)))
+
 
 def free_port():
     s = socket.socket()
@@ -105,6 +124,60 @@ def test_sharded_circuit_matches_unsharded(world, n):
     mgr = mp.Manager()
     failures = mgr.list()
     mp.spawn(worker, args=(world, free_port(), n, 7 + world, failures), nprocs=world, join=True)
+    assert not list(failures)
+
+
+def grad_worker(rank, world, port, n, seed, failures):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        o = oracle.restatement()
+        rng = np.random.default_rng(seed)
+        cases = []
+        # the QAOA generator (config 2 shape): H layer, CNOT.Rz.CNOT edges, Rx
+        # mixers, H = 1/2 sum (I - Z Z) incl. the identity term
+        q = circuits.config2(n=n, p=2, seed=seed)
+        cases.append((q.circuit, q.observable))
+        # random gates incl. parametric ones on the global qubits and a
+        # Heisenberg-like operator with X/Y factors
+        gates = [random_gate(n, rng) for _ in range(60)]
+        top = n
+        gates += [parametric_gate(GateKind.Ry, [top], 0.4, True),
+                  parametric_gate(GateKind.CRz, [top, 1], -0.8, True),
+                  parametric_gate(GateKind.CRx, [2, top], 1.1, True),
+                  parametric_gate(GateKind.Rz, [top], 0.9, True),
+                  parametric_gate(GateKind.Fsim, [top - 1, top], [0.3, 0.2, 0.1, 0.05, 0.4],
+                                  [True, False, True, True, False])]
+        cases.append((Circuit(gates), random_operator(n, 6, rng)))
+        for c, op in cases:
+            local = torch.zeros(1 << (n - (world.bit_length() - 1)), dtype=torch.complex128)
+            st = ShardedState(n, dist, OracleEngine(), local, rank, world, chunk_amps=32)
+            st.set_zero()
+            loss, grads = st.gradient_pure(op, c)
+            back = st.gather()
+            if rank == 0:
+                want_loss, want = o.gradient_pure(op, c, o.pure_state(n))
+                assert abs(loss - want_loss) <= 1e-10 * max(1.0, abs(want_loss))
+                assert grads.shape == want.shape
+                assert np.max(np.abs(grads - want)) <= 1e-10 * max(1.0, np.max(np.abs(want)))
+                # the reverse sweep returns Phi to s0 = |0...0>
+                e0 = np.zeros(1 << n, dtype=np.complex128)
+                e0[0] = 1
+                assert np.max(np.abs(back - e0)) <= 1e-10
+    except Exception as ex:
+        failures.append(f"rank {rank}: {type(ex).__name__}: {ex}")
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 8), (4, 10)])
+def test_sharded_gradient_matches_unsharded(world, n):
+    mgr = mp.Manager()
+    failures = mgr.list()
+    mp.spawn(grad_worker, args=(world, free_port(), n, 3 + world, failures), nprocs=world, join=True)
     assert not list(failures)
 
 
