@@ -54,6 +54,14 @@ constexpr int NW = T / 32;  // warps per block
 constexpr int K = RB + TB;  // tile bits
 constexpr int TS = 1 << K;  // tile size
 
+// adjoint gradient partials: lanes reduced by shuffles per partial sum (the
+// rest stay separate shared-memory partials, summed once per block)
+#ifndef VQB_RS_LANES_PER_PART
+#define VQB_RS_LANES_PER_PART 32
+#endif
+constexpr int LANES_PER_PART = VQB_RS_LANES_PER_PART;
+constexpr int NPART = NW * (32 / LANES_PER_PART);
+
 // register bit 3 in the dispatch tables (never selected when RB = 3)
 constexpr int B3 = RB > 3 ? 3 : 0;
 
@@ -500,13 +508,13 @@ __global__ void __launch_bounds__(T, (kBlocksPerSm<REV, WIDE>))
     double2 *stab = reinterpret_cast<double2 *>(smem_raw);
     double2 *stage_buf = stab + kMaxTab;
     double2 *xbuf = STAGED ? stage_buf + NS * TS : stage_buf;
-    double *pacc = reinterpret_cast<double *>(xbuf + TS); // [nslots][NW] (REV)
+    double *pacc = reinterpret_cast<double *>(xbuf + TS); // [nslots][NPART] (REV)
     // the stage's matrix pool, read with broadcast shared-memory loads
-    double2 *spool = REV ? reinterpret_cast<double2 *>(pacc + kMaxSlots * NW) : xbuf + TS;
+    double2 *spool = REV ? reinterpret_cast<double2 *>(pacc + kMaxSlots * NPART) : xbuf + TS;
     const int t = threadIdx.x;
     const int lane = t & 31, warp = t >> 5;
     if (REV)
-        for (int i = t; i < P.nslots * NW; i += T) pacc[i] = 0;
+        for (int i = t; i < P.nslots * NPART; i += T) pacc[i] = 0;
     for (int i = t; i < P.ntab; i += T) stab[i] = P.tab[i];
     for (int i = t; i < P.npool; i += T) spool[i] = P.pool[i];
     __syncthreads();
@@ -659,9 +667,14 @@ __global__ void __launch_bounds__(T, (kBlocksPerSm<REV, WIDE>))
                     for (int p = 0; p < VQB_MAX_PARAMS; ++p) {
                         if (p >= op.np) break;
                         double x = acc[p];
+                        // partial warp reduction: LANES_PER_PART lanes per partial
+                        // sum, each partial slot owned by one lane (deterministic)
 #pragma unroll
-                        for (int sh = 16; sh > 0; sh >>= 1) x += __shfl_down_sync(0xffffffffu, x, sh);
-                        if (lane == 0) pacc[(op.slot + p) * NW + warp] += x;
+                        for (int sh = LANES_PER_PART / 2; sh > 0; sh >>= 1)
+                            x += __shfl_down_sync(0xffffffffu, x, sh);
+                        if ((lane & (LANES_PER_PART - 1)) == 0)
+                            pacc[(op.slot + p) * NPART + warp * (32 / LANES_PER_PART) +
+                                 lane / LANES_PER_PART] += x;
                     }
                 }
             }
@@ -690,7 +703,7 @@ __global__ void __launch_bounds__(T, (kBlocksPerSm<REV, WIDE>))
         __syncthreads();
         for (int s = t; s < P.nslots; s += T) {
             double x = 0;
-            for (int w = 0; w < NW; ++w) x += pacc[s * NW + w];
+            for (int w = 0; w < NPART; ++w) x += pacc[s * NPART + w];
             partial[(size_t)blockIdx.x * P.partial_ld + P.slot_begin + s] = x;
         }
     }
@@ -1020,7 +1033,7 @@ int env_int(const char *name, int dflt) {
 template <bool REV, bool WIDE = true> size_t smem_bytes(int npool = kMaxPool) {
     const int staging = kStaged<REV, WIDE> ? (REV ? 2 : 1) : 0;
     return (size_t)kMaxTab * sizeof(double2) + (size_t)(staging + 1) * TS * sizeof(double2) +
-           (REV ? kMaxSlots * NW * 8 : 0) + (size_t)npool * sizeof(double2);
+           (REV ? kMaxSlots * NPART * 8 : 0) + (size_t)npool * sizeof(double2);
 }
 
 // resident blocks (grid = SMs x blocks per SM) for a launch with `smem` bytes
