@@ -33,6 +33,14 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cstddef>
+#include <cstdint>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+#include "jit.hpp"
 #include "plan.hpp"
 
 namespace vqb {
@@ -322,20 +330,20 @@ __device__ __forceinline__ void apply_diag(double2 (&v)[R], const ROp &op, const
 template <int NT, int P0, int P1 = 0>
 __device__ __forceinline__ void apply_hoisted(double2 (&v)[R], const double2 *M) {
     using PS = Pos<NT, P0, P1, 0, 0>;
-    constexpr int D = PS::D;
 #if !VQB_RS_HOIST
     // entries re-read per group (broadcast shared-memory loads), no register copy
 #pragma unroll
     for (int i = 0; i < R; ++i)
         if (!(i & PS::MASK)) group_mv<PS>(v, i, M);
-    return;
-#endif
+#else
+    constexpr int D = PS::D;
     double2 m[D * D];
 #pragma unroll
     for (int e = 0; e < D * D; ++e) m[e] = M[e];
 #pragma unroll
     for (int i = 0; i < R; ++i)
         if (!(i & PS::MASK)) group_mv<PS>(v, i, m);
+#endif
 }
 
 __device__ __forceinline__ void apply_fast(double2 (&v)[R], const double2 *pool, int w) {
@@ -1058,6 +1066,269 @@ template <bool REV, bool WIDE> int grid_size(unsigned long long ntiles, size_t s
     return (int)std::min<unsigned long long>((unsigned long long)nsm * per_sm[kib], ntiles);
 }
 
+
+// ---------------------------------------------------------------- specialisation
+std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *per_block);
+// Source of a kernel equivalent to k_regstage<false, false> on one lowered
+// stage program, with every structural quantity a literal: tile bits, layouts
+// (shared-memory slot XOR constants), register positions, condition bits,
+// identity masks and matrix offsets. Matrices are read from the kernel's
+// parameter block at constant offsets; sub-matrices selected by thread or
+// tile bits come from a shared-memory copy. Returns "" for programs the
+// generator does not cover (wide operations).
+std::string jit_forward_source(const RParams &P, bool *uses_spool, bool *per_block) {
+    if constexpr (RB != 4 || TB != 7) return "";
+    else return jit_forward_source_rs16(P, uses_spool, per_block);
+}
+
+std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *per_block) {
+    for (int i = 0; i < P.nsubs; ++i)
+        for (int o = 0; o < P.subs[i].op_count; ++o)
+            if (P.ops[P.subs[i].op_begin + o].nt >= 3) return "";
+    std::string src;
+    auto out = [&](const std::string &x) { src += x; };
+    auto num = [](unsigned long long v) { return std::to_string(v) + "ull"; };
+    auto thread_expr = [&](const int *lbits, bool global) {
+        // sum_b ((t >> b) & 1) << pos(b), pos = local bit or its global bit
+        std::string e = "(0";
+        for (int b = 0; b < TB; ++b) {
+            const int pos = global ? P.bits[lbits[b]] : lbits[b];
+            e += " | (" + std::string(global ? "(u64)" : "") + "((t >> " + std::to_string(b) +
+                 ") & 1) << " + std::to_string(pos) + ")";
+        }
+        return e + ")";
+    };
+    auto slot_const = [&](const RLayout &L, int i) {
+        int c = 0;
+        for (int b = 0; b < RB; ++b)
+            if ((i >> b) & 1) c ^= swz(1 << L.reg[b]);
+        return c;
+    };
+    bool spool = false;
+    // where statically indexed matrices are read from: the parameter bank
+    // (uniform-register operands; the compiler hoists them) or the
+    // shared-memory copy (VQB_JIT_POOL=smem)
+    const char *pool_env = std::getenv("VQB_JIT_POOL");
+    const bool pool_smem = pool_env && std::strcmp(pool_env, "smem") == 0;
+    const std::string MP = pool_smem ? "spool" : "P.pool";
+    const int jit_blocks = env_int("VQB_JIT_BLOCKS", 4);
+    const char *mode_env = std::getenv("VQB_JIT_MODE");
+    const bool per_block_mode = !(mode_env && std::strcmp(mode_env, "persistent") == 0);
+    std::string body;
+    auto emit = [&](const std::string &x) { body += x; };
+    static const int pair_p0[6] = {0, 0, 0, 1, 1, 2}, pair_p1[6] = {1, 2, 3, 2, 3, 3};
+    for (int sub = 0; sub < P.nsubs; ++sub) {
+        const RSub &sb = P.subs[sub];
+        if (sub > 0) {
+            const RLayout &A = P.subs[sub - 1].L;
+            for (int i = 0; i < R; ++i)
+                emit("    xbuf[st" + std::to_string(sub - 1) + " ^ " + std::to_string(slot_const(A, i)) +
+                     "] = v[" + std::to_string(i) + "];\n");
+            emit("    __syncthreads();\n");
+            for (int i = 0; i < R; ++i)
+                emit("    v[" + std::to_string(i) + "] = xbuf[st" + std::to_string(sub) + " ^ " +
+                     std::to_string(slot_const(sb.L, i)) + "];\n");
+            emit("    __syncthreads();\n");
+        }
+        for (int k = 0; k < sb.op_count; ++k) {
+            const ROp &op = P.ops[sb.op_begin + k];
+            const int dd = 1 << (2 * op.nt);
+            std::string dyn;
+            for (int q = 0; q < op.nc; ++q) {
+                if (op.ck[q] == 0)
+                    dyn += " | (int)(((base >> " + std::to_string(op.cp[q]) + ") & 1) << " +
+                           std::to_string(q) + ")";
+                else if (op.ck[q] == 1)
+                    dyn += " | (((t >> " + std::to_string(op.cp[q]) + ") & 1) << " + std::to_string(q) + ")";
+            }
+            auto cstat = [&](int i) {
+                int c = 0;
+                for (int q = 0; q < op.nc; ++q)
+                    if (op.ck[q] == 2 && ((i >> op.cp[q]) & 1)) c |= 1 << q;
+                return c;
+            };
+            std::string tmpl;
+            int mask = 0;
+            if (op.nt == 1) {
+                tmpl = "1, " + std::to_string(op.code) + ", 0, 16";
+                mask = 1 << op.code;
+            } else if (op.nt == 2) {
+                tmpl = "2, " + std::to_string(pair_p0[op.code]) + ", " + std::to_string(pair_p1[op.code]) + ", 16";
+                mask = (1 << pair_p0[op.code]) | (1 << pair_p1[op.code]);
+            }
+            const std::string ident = num(op.ident);
+            if (dyn.empty()) {
+                if (op.nt > 0 && op.nc == 0) {
+                    if (!(op.ident & 1))
+                        emit("    mv_all<" + tmpl + ">(v, " + MP + " + " + std::to_string(op.mat) + ");\n");
+                    continue;
+                }
+                for (int i = 0; i < R; ++i) {
+                    if (i & mask) continue;
+                    const int c = cstat(i);
+                    if ((op.ident >> c) & 1) continue;
+                    if (op.nt == 0)
+                        emit("    v[" + std::to_string(i) + "] = cmul(" + MP + "[" + std::to_string(op.mat + c) +
+                             "], v[" + std::to_string(i) + "]);\n");
+                    else
+                        emit("    mv_group<" + tmpl + ">(v, " + std::to_string(i) + ", " + MP + " + " +
+                             std::to_string(op.mat + c * dd) + ");\n");
+                }
+                continue;
+            }
+            spool = true;
+            emit("    {\n      const int cd = 0" + dyn + ";\n");
+            for (int i = 0; i < R; ++i) {
+                if (i & mask) continue;
+                const std::string c = "(cd | " + std::to_string(cstat(i)) + ")";
+                const std::string guard = "if (!((" + ident + " >> " + c + ") & 1)) ";
+                if (op.nt == 0)
+                    emit("      " + guard + "v[" + std::to_string(i) + "] = cmul(spool[" +
+                         std::to_string(op.mat) + " + " + c + "], v[" + std::to_string(i) + "]);\n");
+                else
+                    emit("      " + guard + "mv_group<" + tmpl + ">(v, " + std::to_string(i) + ", spool + " +
+                         std::to_string(op.mat) + " + " + c + " * " + std::to_string(dd) + ");\n");
+            }
+            emit("    }\n");
+        }
+    }
+    const RLayout &Lf = P.subs[P.nsubs - 1].L;
+    out("#include \"jit_rt.cuh\"\nusing namespace vqbjit;\n");
+    out("struct JP { double2 pool[" + std::to_string(std::max(P.npool, 1)) + "]; };\n");
+    out("extern \"C\" __global__ void __launch_bounds__(128, " + std::to_string(jit_blocks) + ")\n"
+        "vqb_stage(double2 *__restrict__ a, const __grid_constant__ JP P) {\n");
+    out(per_block_mode ? "  extern __shared__ __align__(16) double2 sm[];\n  double2 *xbuf = sm;\n"
+                       : "  extern __shared__ __align__(16) double2 sm[];\n"
+                         "  double2 *stage = sm, *xbuf = sm + 2048;\n");
+    // matrices are read from a shared-memory copy at constant offsets: loads
+    // the compiler cannot hoist out of the tile loop (parameter-bank reads
+    // would be hoisted into registers and spill)
+    spool = spool || pool_smem;
+    if (spool)
+        out(std::string("  double2 *spool = sm + ") + (per_block_mode ? "2048" : "4096") +
+            ";\n  for (int i = threadIdx.x; i < " + std::to_string(P.npool) +
+            "; i += 128) spool[i] = P.pool[i];\n  __syncthreads();\n");
+    out("  const int t = threadIdx.x;\n");
+    int nat_local[TB];
+    for (int b = 0; b < TB; ++b) nat_local[b] = b;
+    out("  const u64 glo = " + thread_expr(nat_local, true) + ";\n");
+    // thread-dependent slot bases are recomputed per tile from an opaque copy
+    // of t (cheap integer work) instead of being hoisted into registers
+    auto opaque_t = [](const char *name) {
+        return std::string("int ") + name + "; asm volatile(\"mov.b32 %0, %1;\" : \"=r\"(" + name +
+               ") : \"r\"(t));\n";
+    };
+    out("  const u64 gfin = " + thread_expr(Lf.thr, true) + ";\n");
+    out("  const u64 NT = " + num(P.ntiles) + ";\n");
+    out("  auto base_of = [&](u64 c) -> u64 {\n");
+    for (int j = 0; j < K; ++j) {
+        const int sb = P.bits[j];
+        out("    c = ((c >> " + std::to_string(sb) + ") << " + std::to_string(sb + 1) + ") | (c & " +
+            num((1ull << sb) - 1) + ");\n");
+    }
+    out("    return c;\n  };\n");
+    // per-layout slot bases, with t seen through an opaque copy (so they are
+    // recomputed per tile instead of being hoisted into registers)
+    std::string slot_bases = "    " + opaque_t("to");
+    for (int sub = 0; sub < P.nsubs; ++sub) {
+        std::string x = thread_expr(P.subs[sub].L.thr, false);
+        for (size_t pos; (pos = x.find("(t >>")) != std::string::npos;) x.replace(pos, 5, "(to >>");
+        slot_bases += "    const int st" + std::to_string(sub) + " = swz" + x + ";\n";
+    }
+    auto natural = [&](int s2, unsigned long long *g, int *sl) {
+        *g = 0;
+        *sl = 0;
+        for (int b = 0; b < RB; ++b)
+            if ((s2 >> b) & 1) {
+                *g |= 1ull << P.bits[TB + b];
+                *sl ^= swz(T << b);
+            }
+    };
+    if (per_block_mode) {
+        // one tile per block: coalesced loads straight into registers, one
+        // relayout to the first layout; other resident blocks cover latency
+        out("  {\n    const u64 tile = blockIdx.x;\n    const u64 base = base_of(tile);\n    double2 v[16];\n");
+        for (int s2 = 0; s2 < R; ++s2) {
+            unsigned long long g;
+            int sl;
+            natural(s2, &g, &sl);
+            out("    v[" + std::to_string(s2) + "] = a[base | glo | " + num(g) + "];\n");
+        }
+        out(slot_bases + "    const int nat_st = swz(to);\n");
+        for (int s2 = 0; s2 < R; ++s2) {
+            unsigned long long g;
+            int sl;
+            natural(s2, &g, &sl);
+            out("    xbuf[nat_st ^ " + std::to_string(sl) + "] = v[" + std::to_string(s2) + "];\n");
+        }
+        out("    __syncthreads();\n");
+        for (int i = 0; i < R; ++i)
+            out("    v[" + std::to_string(i) + "] = xbuf[st0 ^ " + std::to_string(slot_const(P.subs[0].L, i)) + "];\n");
+        out("    __syncthreads();\n");
+    } else {
+        out("  auto prefetch = [&](u64 tile) {\n    const u64 b = base_of(tile) | glo;\n    " + opaque_t("tn") +
+            "    const int nat_st = swz(tn);\n");
+        for (int s2 = 0; s2 < R; ++s2) {
+            unsigned long long g;
+            int sl;
+            natural(s2, &g, &sl);
+            out("    cp_async16(&stage[nat_st ^ " + std::to_string(sl) + "], a + (b | " + num(g) + "));\n");
+        }
+        out("    cp_async_commit();\n  };\n");
+        out("  u64 tile = blockIdx.x;\n  if (tile < NT) prefetch(tile);\n"
+            "  for (; tile < NT; tile += gridDim.x) {\n    const u64 base = base_of(tile);\n"
+            "    cp_async_wait_all();\n    __syncthreads();\n    double2 v[16];\n");
+        out(slot_bases);
+        for (int i = 0; i < R; ++i)
+            out("    v[" + std::to_string(i) + "] = stage[st0 ^ " + std::to_string(slot_const(P.subs[0].L, i)) + "];\n");
+        out("    __syncthreads();\n    if (tile + gridDim.x < NT) prefetch(tile + gridDim.x);\n");
+    }
+    out(body);
+    for (int i = 0; i < R; ++i) {
+        unsigned long long g = 0;
+        for (int b = 0; b < RB; ++b)
+            if ((i >> b) & 1) g |= 1ull << P.bits[Lf.reg[b]];
+        out("    a[base | gfin | " + num(g) + "] = v[" + std::to_string(i) + "];\n");
+    }
+    out(per_block_mode ? "  }\n}\n" : "  }\n  cp_async_wait_all();\n}\n");
+    if (uses_spool) *uses_spool = spool;
+    if (per_block) *per_block = per_block_mode;
+    return src;
+}
+
+// Specialised kernels by stage-program *structure*: everything in RParams but
+// the matrix values (pool, tab). A hit skips source generation entirely.
+struct JitShape {
+    std::string key;
+    jit::Kernel k;
+    bool spool = false, per_block = false;
+};
+uint64_t fnv1a(const std::string &s) {
+    uint64_t h = 1469598103934665603ull;
+    for (unsigned char c : s) h = (h ^ c) * 1099511628211ull;
+    return h;
+}
+std::string shape_key(const RParams &P) {
+    const char *b = reinterpret_cast<const char *>(&P);
+    const size_t pool_at = offsetof(RParams, pool), rest_at = offsetof(RParams, ntab);
+    std::string key(b, pool_at);
+    key.append(b + rest_at, sizeof(RParams) - rest_at);
+    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE"}) {
+        const char *v = std::getenv(e);
+        key += '|';
+        if (v) key += v;
+    }
+    return key;
+}
+std::mutex g_shape_mu;
+std::unordered_map<uint64_t, JitShape> g_shapes;
+// cached kernel for a structure, or nullptr
+const JitShape *find_shape(const std::string &key, uint64_t h) {
+    std::lock_guard<std::mutex> lk(g_shape_mu);
+    auto it = g_shapes.find(h);
+    return it != g_shapes.end() && it->second.key == key ? &it->second : nullptr;
+}
+
 // Shared driver: stage planning, block fusion, lowering, launches.
 template <bool REV, typename Fallback>
 void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, double *dgrads,
@@ -1081,10 +1352,71 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
         VQB_CUDA(cudaMemsetAsync(m_partial.p, 0, sizeof(double) * (size_t)grid * total_slots, st));
     }
     SlotMap slots;
-    static thread_local RParams P;
+    // Actions (a launch, or an unfusable op) are lowered in program order and
+    // issued as soon as their kernel is known, so the host's planning of later
+    // stages overlaps the device's work on earlier ones. The first
+    // specialisation miss switches to batch mode: the rest is lowered first,
+    // all missing kernels are compiled in parallel, then everything pending is
+    // issued in order.
+    struct Action {
+        int fallback_op = -1;
+        std::unique_ptr<RParams> P;
+        bool wide = false;
+        const JitShape *jit = nullptr;
+        std::string key;
+        uint64_t hash = 0;
+    };
+    const bool use_jit = !REV && jit::enabled(pn);
+    bool batching = false;
+    std::vector<Action> pending;
+    auto issue = [&](Action &act) {
+        if (act.fallback_op >= 0) {
+            fallback(fops[act.fallback_op]);
+            return;
+        }
+        RParams &P = *act.P;
+        const ProfMark pf_ = prof_begin(st);
+        if (act.jit) {
+            const JitShape &sh = *act.jit;
+            const size_t sm = (size_t)((sh.per_block ? 1 : 2) * TS + (sh.spool ? P.npool : 0)) * sizeof(double2);
+            static int nsm = 0;
+            if (!nsm) VQB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+            const unsigned g = sh.per_block
+                                   ? (unsigned)ntiles
+                                   : (unsigned)std::min<unsigned long long>(
+                                         (unsigned long long)nsm * jit::blocks_per_sm(sh.k, T, sm), ntiles);
+            void *amps = sphi->amps;
+            void *args[2] = {&amps, P.pool};
+            jit::launch(sh.k, g, T, sm, st, args);
+            check_launch("k_regstage_jit", pf_);
+            return;
+        }
+        if (act.wide) {
+            const size_t sm = smem_bytes<REV>(P.npool);
+            k_regstage<REV, true><<<grid_size<REV, true>(ntiles, sm), T, sm, st>>>(
+                sphi->amps, REV ? spsi->amps : nullptr, static_cast<double *>(m_partial.p), P);
+        } else {
+            const size_t sm = smem_bytes<REV, false>(P.npool);
+            k_regstage<REV, false><<<grid_size<REV, false>(ntiles, sm), T, sm, st>>>(
+                sphi->amps, REV ? spsi->amps : nullptr, static_cast<double *>(m_partial.p), P);
+        }
+        check_launch(REV ? "k_regstage_rev" : "k_regstage", pf_);
+    };
+    auto submit = [&](Action &&act) {
+        if (use_jit && act.P && !act.wide) {
+            act.key = shape_key(*act.P);
+            act.hash = fnv1a(act.key);
+            act.jit = find_shape(act.key, act.hash);
+            if (!act.jit) batching = true; // compile later, with the other misses
+        }
+        if (batching) pending.push_back(std::move(act));
+        else issue(act);
+    };
     for (const Stage &sg : stages) {
         if (!sg.fused) {
-            fallback(fops[sg.ops[0]]);
+            Action a;
+            a.fallback_op = sg.ops[0];
+            submit(std::move(a));
             continue;
         }
         std::vector<FusedOp> blocks;
@@ -1094,6 +1426,9 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
         std::vector<int> remaining(blocks.size());
         for (size_t i = 0; i < blocks.size(); ++i) remaining[i] = (int)i;
         while (!remaining.empty()) {
+            Action act;
+            act.P = std::make_unique<RParams>();
+            RParams &P = *act.P;
             lower_stage_reg(sg, blocks, remaining, pn, REV, P, slots);
             P.partial_ld = total_slots;
             if (stats) {
@@ -1118,21 +1453,47 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
                 }
                 note_flops(per_amp * double(1ull << pn));
             }
-            bool wide = REV;
+            act.wide = REV;
             for (int i = 0; i < P.nsubs; ++i)
                 for (int o = 0; o < P.subs[i].op_count; ++o)
-                    wide = wide || P.ops[P.subs[i].op_begin + o].nt >= 3;
-            const ProfMark pf_ = prof_begin(st);
-            if (wide) {
-                const size_t sm = smem_bytes<REV>(P.npool);
-                k_regstage<REV, true><<<grid_size<REV, true>(ntiles, sm), T, sm, st>>>(
-                    sphi->amps, REV ? spsi->amps : nullptr, static_cast<double *>(m_partial.p), P);
-            } else {
-                const size_t sm = smem_bytes<REV, false>(P.npool);
-                k_regstage<REV, false><<<grid_size<REV, false>(ntiles, sm), T, sm, st>>>(
-                    sphi->amps, REV ? spsi->amps : nullptr, static_cast<double *>(m_partial.p), P);
+                    act.wide = act.wide || P.ops[P.subs[i].op_begin + o].nt >= 3;
+            submit(std::move(act));
+        }
+    }
+    if (!pending.empty()) {
+        // compile the missing structures (distinct ones, in parallel), then issue
+        std::vector<std::string> srcs;
+        std::vector<size_t> which;
+        std::vector<std::pair<bool, bool>> flags;
+        std::unordered_map<uint64_t, size_t> first;
+        for (size_t i = 0; i < pending.size(); ++i) {
+            Action &act = pending[i];
+            if (!act.P || act.wide || act.hash == 0) continue;
+            if ((act.jit = find_shape(act.key, act.hash))) continue;
+            if (first.count(act.hash)) continue;
+            bool sp = false, pb = false;
+            std::string src = jit_forward_source(*act.P, &sp, &pb);
+            if (src.empty()) continue;
+            first[act.hash] = i;
+            srcs.push_back(std::move(src));
+            flags.emplace_back(sp, pb);
+            which.push_back(i);
+        }
+        if (!srcs.empty()) {
+            const auto ks = jit::get(srcs, "vqb_stage");
+            std::lock_guard<std::mutex> lk(g_shape_mu);
+            for (size_t k = 0; k < which.size(); ++k) {
+                const Action &act = pending[which[k]];
+                JitShape &sh = g_shapes[act.hash];
+                sh.key = act.key;
+                sh.k = ks[k];
+                sh.spool = flags[k].first;
+                sh.per_block = flags[k].second;
             }
-            check_launch(REV ? "k_regstage_rev" : "k_regstage", pf_);
+        }
+        for (Action &act : pending) {
+            if (act.P && !act.wide && act.hash != 0 && !act.jit) act.jit = find_shape(act.key, act.hash);
+            issue(act);
         }
     }
     if (REV && total_slots > 0) {
