@@ -720,12 +720,31 @@ __global__ void __launch_bounds__(T, (kBlocksPerSm<REV, WIDE>))
 // grads[dst[j]] = scale[j] * sum_b partial[b][j] (fixed block order)
 __global__ void k_grads(const double *__restrict__ partial, int nblocks, int ld,
                         const double *__restrict__ scale, const long long *__restrict__ dst,
-                        int ncols, double *__restrict__ grads) {
+                        int ncols, const double *__restrict__ extra, double *__restrict__ grads) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= ncols) return;
     double v = 0;
     for (int b = 0; b < nblocks; ++b) v += partial[(size_t)b * ld + j];
-    grads[dst[j]] = scale[j] * v;
+    grads[dst[j]] = scale[j] * (v + extra[j]);
+}
+
+// Specialised adjoint launches write one partial per (slot, tile); this sums a
+// slot's row in fixed order (strided per thread, then a fixed tree):
+// deterministic. One block per slot of the launch.
+__global__ void __launch_bounds__(256) k_slot_sums(const double *__restrict__ partial,
+                                                   unsigned long long ntiles,
+                                                   double *__restrict__ out) {
+    __shared__ double sh[256];
+    const double *row = partial + (size_t)blockIdx.x * ntiles;
+    double v = 0;
+    for (unsigned long long i = threadIdx.x; i < ntiles; i += 256) v += row[i];
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[blockIdx.x] = sh[0];
 }
 
 // ---------------------------------------------------------------- host planning
@@ -1296,6 +1315,217 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
     return src;
 }
 
+
+// Source of a specialised adjoint stage kernel (the REV mode of k_regstage on
+// one lowered program): Phi and Psi tiles in registers, one tile per block,
+// each parametric step's contributions reduced per warp into shared memory and
+// written as one partial per (slot, tile) for k_slot_sums. Returns "" for
+// programs with wide operations (they stay on the interpreter).
+std::string jit_reverse_source(const RParams &P, bool *uses_spool) {
+    int nops_total = 0;
+    for (int i = 0; i < P.nsubs; ++i)
+        for (int o = 0; o < P.subs[i].op_count; ++o) {
+            if (P.ops[P.subs[i].op_begin + o].nt >= 3) return "";
+            ++nops_total;
+        }
+    if (nops_total == 0) return "";
+    auto num = [](unsigned long long v) { return std::to_string(v) + "ull"; };
+    auto I = [](long long v) { return std::to_string(v); };
+    auto thread_expr = [&](const int *lbits, bool global, const char *tv) {
+        std::string e = "(0";
+        for (int b = 0; b < TB; ++b) {
+            const int pos = global ? P.bits[lbits[b]] : lbits[b];
+            e += std::string(" | (") + (global ? "(u64)" : "") + "((" + tv + " >> " + I(b) + ") & 1) << " +
+                 I(pos) + ")";
+        }
+        return e + ")";
+    };
+    auto slot_const = [&](const RLayout &L, int i) {
+        int c = 0;
+        for (int b = 0; b < RB; ++b)
+            if ((i >> b) & 1) c ^= swz(1 << L.reg[b]);
+        return c;
+    };
+    static const int pair_p0[6] = {0, 0, 0, 1, 1, 2}, pair_p1[6] = {1, 2, 3, 2, 3, 3};
+    const int jit_blocks = env_int("VQB_JIT_REV_BLOCKS", 4);
+    bool spool = false;
+    std::string body;
+    auto emit = [&](const std::string &x) { body += x; };
+    auto relayout = [&](const char *v, int from, int to) {
+        for (int i = 0; i < R; ++i)
+            emit(std::string("    xbuf[st") + I(from) + " ^ " + I(slot_const(P.subs[from].L, i)) + "] = " + v +
+                 "[" + I(i) + "];\n");
+        emit("    __syncthreads();\n");
+        for (int i = 0; i < R; ++i)
+            emit(std::string("    ") + v + "[" + I(i) + "] = xbuf[st" + I(to) + " ^ " +
+                 I(slot_const(P.subs[to].L, i)) + "];\n");
+        emit("    __syncthreads();\n");
+    };
+    for (int sub = 0; sub < P.nsubs; ++sub) {
+        const RSub &sb = P.subs[sub];
+        if (sub > 0) {
+            relayout("vf", sub - 1, sub);
+            relayout("vg", sub - 1, sub);
+        }
+        for (int k = 0; k < sb.op_count; ++k) {
+            const ROp &op = P.ops[sb.op_begin + k];
+            const int dd = 1 << (2 * op.nt), nsub = 1 << op.nc;
+            std::string dyn;
+            for (int q = 0; q < op.nc; ++q) {
+                if (op.ck[q] == 0)
+                    dyn += " | (int)(((base >> " + I(op.cp[q]) + ") & 1) << " + I(q) + ")";
+                else if (op.ck[q] == 1)
+                    dyn += " | (((to >> " + I(op.cp[q]) + ") & 1) << " + I(q) + ")";
+            }
+            const bool dynamic = !dyn.empty();
+            spool = spool || dynamic;
+            auto cstat = [&](int i) {
+                int c = 0;
+                for (int q = 0; q < op.nc; ++q)
+                    if (op.ck[q] == 2 && ((i >> op.cp[q]) & 1)) c |= 1 << q;
+                return c;
+            };
+            std::string tmpl;
+            int mask = 0;
+            if (op.nt == 1) {
+                tmpl = "1, " + I(op.code) + ", 0, " + I(R);
+                mask = 1 << op.code;
+            } else if (op.nt == 2) {
+                tmpl = "2, " + I(pair_p0[op.code]) + ", " + I(pair_p1[op.code]) + ", " + I(R);
+                mask = (1 << pair_p0[op.code]) | (1 << pair_p1[op.code]);
+            }
+            // matrix expression for sub-matrix index expression c at base offset off
+            auto mat = [&](unsigned off, const std::string &c, int cs, int stride) {
+                if (dynamic) return "spool + " + I(off) + " + (" + c + ") * " + I(stride);
+                return "P.pool + " + I(off + (unsigned)(cs * stride));
+            };
+            auto elem = [&](unsigned off, const std::string &c, int cs) {
+                if (dynamic) return "spool[" + I(off) + " + (" + c + ")]";
+                return "P.pool[" + I(off + (unsigned)cs) + "]";
+            };
+            if (dynamic) emit("    {\n      const int cd = 0" + dyn + ";\n");
+            else emit("    {\n");
+            if (op.np == 0) {
+                const unsigned mpsi = op.pair ? op.mat_psi : op.mat;
+                const unsigned long long ipsi = op.pair ? op.ident_psi : op.ident;
+                for (int st2 = 0; st2 < 2; ++st2) {
+                    const char *v = st2 ? "vg" : "vf";
+                    const unsigned m = st2 ? mpsi : op.mat;
+                    const unsigned long long id = st2 ? ipsi : op.ident;
+                    for (int i = 0; i < R; ++i) {
+                        if (i & mask) continue;
+                        const int cs = cstat(i);
+                        const std::string c = dynamic ? "(cd | " + I(cs) + ")" : I(cs);
+                        std::string guard;
+                        if (dynamic) guard = "if (!((" + num(id) + " >> " + c + ") & 1)) ";
+                        else if ((id >> cs) & 1) continue;
+                        if (op.nt == 0)
+                            emit("      " + guard + v + "[" + I(i) + "] = cmul(" + elem(m, c, cs) + ", " + v +
+                                 "[" + I(i) + "]);\n");
+                        else
+                            emit("      " + guard + "mv_group<" + tmpl + ">(" + v + ", " + I(i) + ", " +
+                                 mat(m, c, cs, dd) + ");\n");
+                    }
+                }
+            } else {
+                for (int p = 0; p < op.np; ++p) emit("      double acc" + I(p) + " = 0;\n");
+                for (int i = 0; i < R; ++i) {
+                    if (i & mask) continue;
+                    const int cs = cstat(i);
+                    const std::string c = dynamic ? "(cd | " + I(cs) + ")" : I(cs);
+                    if (op.nt == 0) {
+                        emit("      {\n        const double2 w = cmul(" + elem(op.mat, c, cs) + ", vf[" + I(i) +
+                             "]);\n        vf[" + I(i) + "] = w;\n");
+                        for (int p = 0; p < op.np; ++p)
+                            emit("        acc" + I(p) + " += re_cj(vg[" + I(i) + "], cmul(" +
+                                 elem(op.mat_d + (unsigned)(p * nsub), c, cs) + ", w));\n");
+                        emit("        vg[" + I(i) + "] = cmul(" + elem(op.mat, c, cs) + ", vg[" + I(i) +
+                             "]);\n      }\n");
+                    } else {
+                        emit("      mv_group<" + tmpl + ">(vf, " + I(i) + ", " + mat(op.mat, c, cs, dd) + ");\n");
+                        for (int p = 0; p < op.np; ++p)
+                            emit("      acc" + I(p) + " += dot_group<" + tmpl + ">(vf, vg, " + I(i) + ", " +
+                                 mat(op.mat_d + (unsigned)(p * nsub * dd), c, cs, dd) + ");\n");
+                        emit("      mv_group<" + tmpl + ">(vg, " + I(i) + ", " + mat(op.mat, c, cs, dd) + ");\n");
+                    }
+                }
+                for (int p = 0; p < op.np; ++p)
+                    emit("      { const double x = warp_sum(acc" + I(p) + "); if (lane == 0) red[" +
+                         I((op.slot + p) * NW) + " + warp] = x; }\n");
+            }
+            emit("    }\n");
+        }
+    }
+    const RLayout &Lf = P.subs[P.nsubs - 1].L;
+    std::string src;
+    auto out = [&](const std::string &x) { src += x; };
+    out("#include \"jit_rt.cuh\"\nusing namespace vqbjit;\n");
+    out("struct JP { double2 pool[" + I(std::max(P.npool, 1)) + "]; };\n");
+    out("extern \"C\" __global__ void __launch_bounds__(" + I(T) + ", " + I(jit_blocks) + ")\n"
+        "vqb_rev(double2 *__restrict__ a, double2 *__restrict__ b2, double *__restrict__ partial,\n"
+        "        const __grid_constant__ JP P) {\n");
+    out("  extern __shared__ __align__(16) double2 sm[];\n  double2 *xbuf = sm;\n");
+    const int red_at = TS + (spool ? P.npool : 0);
+    if (spool)
+        out("  double2 *spool = sm + " + I(TS) + ";\n  for (int i = threadIdx.x; i < " + I(P.npool) + "; i += " +
+            I(T) + ") spool[i] = P.pool[i];\n");
+    out("  double *red = reinterpret_cast<double *>(sm + " + I(red_at) + ");\n");
+    out("  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;\n");
+    int nat_local[TB];
+    for (int b = 0; b < TB; ++b) nat_local[b] = b;
+    out("  const u64 glo = " + thread_expr(nat_local, true, "t") + ";\n");
+    out("  const u64 gfin = " + thread_expr(Lf.thr, true, "t") + ";\n");
+    out("  auto base_of = [&](u64 c) -> u64 {\n");
+    for (int j = 0; j < K; ++j) {
+        const int sbit = P.bits[j];
+        out("    c = ((c >> " + I(sbit) + ") << " + I(sbit + 1) + ") | (c & " + num((1ull << sbit) - 1) + ");\n");
+    }
+    out("    return c;\n  };\n");
+    out("  const u64 tile = blockIdx.x;\n  const u64 base = base_of(tile);\n");
+    out("  double2 vf[" + I(R) + "], vg[" + I(R) + "];\n");
+    for (int s2 = 0; s2 < R; ++s2) {
+        unsigned long long g = 0;
+        for (int b = 0; b < RB; ++b)
+            if ((s2 >> b) & 1) g |= 1ull << P.bits[TB + b];
+        out("  vf[" + I(s2) + "] = a[base | glo | " + num(g) + "];\n  vg[" + I(s2) + "] = b2[base | glo | " + num(g) +
+            "];\n");
+    }
+    out("  int to; asm volatile(\"mov.b32 %0, %1;\" : \"=r\"(to) : \"r\"(t));\n");
+    for (int sub = 0; sub < P.nsubs; ++sub)
+        out("  const int st" + I(sub) + " = swz" + thread_expr(P.subs[sub].L.thr, false, "to") + ";\n");
+    out("  const int nat_st = swz(to);\n");
+    for (int st2 = 0; st2 < 2; ++st2) {
+        const char *v = st2 ? "vg" : "vf";
+        for (int s2 = 0; s2 < R; ++s2) {
+            int sl = 0;
+            for (int b = 0; b < RB; ++b)
+                if ((s2 >> b) & 1) sl ^= swz(T << b);
+            out(std::string("  xbuf[nat_st ^ ") + I(sl) + "] = " + v + "[" + I(s2) + "];\n");
+        }
+        out("  __syncthreads();\n");
+        for (int i = 0; i < R; ++i)
+            out(std::string("  ") + v + "[" + I(i) + "] = xbuf[st0 ^ " + I(slot_const(P.subs[0].L, i)) + "];\n");
+        out("  __syncthreads();\n");
+    }
+    out(body);
+    for (int i = 0; i < R; ++i) {
+        unsigned long long g = 0;
+        for (int b = 0; b < RB; ++b)
+            if ((i >> b) & 1) g |= 1ull << P.bits[Lf.reg[b]];
+        out("  a[base | gfin | " + num(g) + "] = vf[" + I(i) + "];\n  b2[base | gfin | " + num(g) + "] = vg[" + I(i) +
+            "];\n");
+    }
+    if (P.nslots > 0) {
+        out("  __syncthreads();\n");
+        out("  for (int s = t; s < " + I(P.nslots) + "; s += " + I(T) + ") {\n    double x = 0;\n");
+        for (int w = 0; w < NW; ++w) out("    x += red[s * " + I(NW) + " + " + I(w) + "];\n");
+        out("    partial[(size_t)s * " + num(P.ntiles) + " + tile] = x;\n  }\n");
+    }
+    out("}\n");
+    if (uses_spool) *uses_spool = spool;
+    return src;
+}
+
 // Specialised kernels by stage-program *structure*: everything in RParams but
 // the matrix values (pool, tab). A hit skips source generation entirely.
 struct JitShape {
@@ -1308,12 +1538,13 @@ uint64_t fnv1a(const std::string &s) {
     for (unsigned char c : s) h = (h ^ c) * 1099511628211ull;
     return h;
 }
-std::string shape_key(const RParams &P) {
+std::string shape_key(const RParams &P, bool rev) {
     const char *b = reinterpret_cast<const char *>(&P);
     const size_t pool_at = offsetof(RParams, pool), rest_at = offsetof(RParams, ntab);
-    std::string key(b, pool_at);
+    std::string key(rev ? "R" : "F");
+    key.append(b, pool_at);
     key.append(b + rest_at, sizeof(RParams) - rest_at);
-    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE"}) {
+    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS"}) {
         const char *v = std::getenv(e);
         key += '|';
         if (v) key += v;
@@ -1361,12 +1592,21 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
     struct Action {
         int fallback_op = -1;
         std::unique_ptr<RParams> P;
-        bool wide = false;
+        bool wide = false;     // interpreter variant with wide-op support
+        bool has_wide = false; // nt >= 3 operations (not specialised)
         const JitShape *jit = nullptr;
         std::string key;
         uint64_t hash = 0;
     };
-    const bool use_jit = !REV && jit::enabled(pn);
+    // adjoint specialisation: per-(slot, tile) partials, summed per launch
+    static thread_local DevMem m_jpartial, m_slotsum;
+    const size_t jpartial_bytes = sizeof(double) * (size_t)kMaxSlots * ntiles;
+    const bool use_jit = jit::enabled(pn) && (!REV || jpartial_bytes <= (size_t(1) << 30));
+    if (REV && total_slots > 0) {
+        m_slotsum.ensure(sizeof(double) * total_slots);
+        VQB_CUDA(cudaMemsetAsync(m_slotsum.p, 0, sizeof(double) * total_slots, st));
+        if (use_jit) m_jpartial.ensure(jpartial_bytes);
+    }
     bool batching = false;
     std::vector<Action> pending;
     auto issue = [&](Action &act) {
@@ -1376,6 +1616,22 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
         }
         RParams &P = *act.P;
         const ProfMark pf_ = prof_begin(st);
+        if (act.jit && REV) {
+            const JitShape &sh = *act.jit;
+            const size_t sm = (size_t)(TS + (sh.spool ? P.npool : 0)) * sizeof(double2) +
+                              sizeof(double) * (size_t)P.nslots * NW;
+            void *a0 = sphi->amps, *a1 = spsi->amps, *pp = m_jpartial.p;
+            void *args[4] = {&a0, &a1, &pp, P.pool};
+            jit::launch(sh.k, (unsigned)ntiles, T, sm, st, args);
+            check_launch("k_regstage_rev_jit", pf_);
+            if (P.nslots > 0) {
+                const ProfMark pf2 = prof_begin(st);
+                k_slot_sums<<<P.nslots, 256, 0, st>>>(static_cast<const double *>(m_jpartial.p), ntiles,
+                                                       static_cast<double *>(m_slotsum.p) + P.slot_begin);
+                check_launch("k_slot_sums", pf2);
+            }
+            return;
+        }
         if (act.jit) {
             const JitShape &sh = *act.jit;
             const size_t sm = (size_t)((sh.per_block ? 1 : 2) * TS + (sh.spool ? P.npool : 0)) * sizeof(double2);
@@ -1403,8 +1659,8 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
         check_launch(REV ? "k_regstage_rev" : "k_regstage", pf_);
     };
     auto submit = [&](Action &&act) {
-        if (use_jit && act.P && !act.wide) {
-            act.key = shape_key(*act.P);
+        if (use_jit && act.P && !act.has_wide) {
+            act.key = shape_key(*act.P, REV);
             act.hash = fnv1a(act.key);
             act.jit = find_shape(act.key, act.hash);
             if (!act.jit) batching = true; // compile later, with the other misses
@@ -1453,10 +1709,10 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
                 }
                 note_flops(per_amp * double(1ull << pn));
             }
-            act.wide = REV;
             for (int i = 0; i < P.nsubs; ++i)
                 for (int o = 0; o < P.subs[i].op_count; ++o)
-                    act.wide = act.wide || P.ops[P.subs[i].op_begin + o].nt >= 3;
+                    act.has_wide = act.has_wide || P.ops[P.subs[i].op_begin + o].nt >= 3;
+            act.wide = REV || act.has_wide;
             submit(std::move(act));
         }
     }
@@ -1468,11 +1724,11 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
         std::unordered_map<uint64_t, size_t> first;
         for (size_t i = 0; i < pending.size(); ++i) {
             Action &act = pending[i];
-            if (!act.P || act.wide || act.hash == 0) continue;
+            if (!act.P || act.has_wide || act.hash == 0) continue;
             if ((act.jit = find_shape(act.key, act.hash))) continue;
             if (first.count(act.hash)) continue;
-            bool sp = false, pb = false;
-            std::string src = jit_forward_source(*act.P, &sp, &pb);
+            bool sp = false, pb = REV;
+            std::string src = REV ? jit_reverse_source(*act.P, &sp) : jit_forward_source(*act.P, &sp, &pb);
             if (src.empty()) continue;
             first[act.hash] = i;
             srcs.push_back(std::move(src));
@@ -1480,7 +1736,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             which.push_back(i);
         }
         if (!srcs.empty()) {
-            const auto ks = jit::get(srcs, "vqb_stage");
+            const auto ks = jit::get(srcs, REV ? "vqb_rev" : "vqb_stage");
             std::lock_guard<std::mutex> lk(g_shape_mu);
             for (size_t k = 0; k < which.size(); ++k) {
                 const Action &act = pending[which[k]];
@@ -1492,7 +1748,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             }
         }
         for (Action &act : pending) {
-            if (act.P && !act.wide && act.hash != 0 && !act.jit) act.jit = find_shape(act.key, act.hash);
+            if (act.P && !act.has_wide && act.hash != 0 && !act.jit) act.jit = find_shape(act.key, act.hash);
             issue(act);
         }
     }
@@ -1510,7 +1766,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             static_cast<const double *>(m_slots.p),
             reinterpret_cast<const long long *>(static_cast<char *>(m_slots.p) +
                                                 sizeof(double) * total_slots),
-            total_slots, dgrads);
+            total_slots, static_cast<const double *>(m_slotsum.p), dgrads);
         check_launch("k_grads", pf_);
     }
     VQB_CUDA(cudaStreamSynchronize(st)); // host-side slot vectors outlive the copies

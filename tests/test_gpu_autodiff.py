@@ -241,3 +241,21 @@ def test_specialised_kernels_match_reference(dev, ref, monkeypatch, mode):
         r = ref.pure_state(14)
         ref.apply_circuit(w.circuit, r)
         assert np.max(np.abs(dev.download(s) - ref.download(r))) <= 1e-12
+
+
+@pytest.mark.parametrize("regs", ["8", "16"])
+def test_specialised_adjoint_matches_reference(dev, ref, monkeypatch, regs):
+    """Specialised adjoint kernels (VQB_JIT=1) for both register geometries:
+    QAOA (folded diagonal parametric steps with register conditions), the
+    hardware-efficient ansatz (1-qubit parametric steps + CNOT) and a noisy
+    circuit (its 16x16 superoperator launches stay on the interpreter)."""
+    monkeypatch.setenv("VQB_JIT", "1")
+    monkeypatch.setenv("VQB_REV_REGS", regs)
+    for w in (circuits.config2(n=14, p=2), circuits.config0(n=14, layers=3)):
+        loss, g = dev.gradient_pure(w.observable, w.circuit, dev.pure_state(14))
+        rloss, rg = ref.gradient_pure(w.observable, w.circuit, ref.pure_state(14))
+        assert abs(loss - rloss) <= RTOL * abs(rloss) and rel_err(g, rg) <= RTOL
+    w = circuits.config3(n=7, layers=2)
+    loss, g = dev.gradient_mixed(w.observable, w.circuit, dev.mixed_state(7))
+    rloss, rg = ref.gradient_mixed(w.observable, w.circuit, ref.mixed_state(7))
+    assert abs(loss - rloss) <= RTOL * abs(rloss) and rel_err(g, rg) <= RTOL
