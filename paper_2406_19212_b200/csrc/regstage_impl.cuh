@@ -1087,6 +1087,65 @@ template <bool REV, bool WIDE> int grid_size(unsigned long long ntiles, size_t s
 
 
 // ---------------------------------------------------------------- specialisation
+// Specialised code for a wide (nt >= 3) operation of sub-stage `sub` on the
+// register state `v`: through the shared-memory tile as sum_k diag(d_k)
+// P_{x_k} (smem_op), with the mixing bits, XOR patterns and slot offsets as
+// literals. Matrices come from the shared-memory pool copy (spool).
+std::string jit_wide_op(const RParams &P, int sub, const ROp &op, const char *v, unsigned mat,
+                        unsigned long long ident, const char *slot_base) {
+    auto I = [](long long x) { return std::to_string(x); };
+    const RLayout &L = P.subs[sub].L;
+    const int NT = std::min(std::max(op.nt, 1), kMaxMix), D = 1 << NT;
+    auto slot_const = [&](int i) {
+        int c = 0;
+        for (int b = 0; b < RB; ++b)
+            if ((i >> b) & 1) c ^= swz(1 << L.reg[b]);
+        return c;
+    };
+    int sorted[kMaxMix];
+    for (int q = 0; q < NT; ++q) sorted[q] = op.lb[q];
+    std::sort(sorted, sorted + NT);
+    int sw_off[16];
+    for (int r = 0; r < D; ++r) {
+        int o = 0;
+        for (int q = 0; q < NT; ++q)
+            if ((r >> q) & 1) o |= 1 << op.lb[q];
+        sw_off[r] = swz(o);
+    }
+    std::string e = "    {\n";
+    for (int i = 0; i < R; ++i)
+        e += std::string("      xbuf[") + slot_base + " ^ " + I(slot_const(i)) + "] = " + v + "[" + I(i) + "];\n";
+    e += "      __syncthreads();\n      const int cu = 0";
+    for (int q = 0; q < op.nc; ++q)
+        if (op.ck[q] == 0) e += " | (int)(((base >> " + I(op.cp[q]) + ") & 1) << " + I(q) + ")";
+    e += ";\n      for (int g = threadIdx.x; g < " + I(TS >> NT) + "; g += " + I(T) + ") {\n        int b = g;\n";
+    for (int q = 0; q < NT; ++q)
+        e += "        b = ((b >> " + I(sorted[q]) + ") << " + I(sorted[q] + 1) + ") | (b & " +
+             I((1 << sorted[q]) - 1) + ");\n";
+    e += "        const int c = cu";
+    for (int q = 0; q < op.nc; ++q) {
+        const int l = op.ck[q] == 1 ? L.thr[op.cp[q]] : (op.ck[q] == 2 ? L.reg[op.cp[q]] : -1);
+        if (l >= 0) e += " | (((b >> " + I(l) + ") & 1) << " + I(q) + ")";
+    }
+    e += ";\n";
+    if (ident) e += "        if ((" + std::to_string(ident) + "ull >> c) & 1) continue;\n";
+    e += "        const double2 *M = spool + " + I(mat) + " + c * " + I(op.nx * D) + ";\n";
+    e += "        const int sb = swz(b);\n";
+    for (int r = 0; r < D; ++r) e += "        double2 o" + I(r) + " = make_double2(0.0, 0.0);\n";
+    for (int k = 0; k < op.nx; ++k) {
+        const int x = P.xpat[op.xoff + k];
+        for (int r = 0; r < D; ++r)
+            e += "        o" + I(r) + " = cfma(M[" + I(k * D + r) + "], xbuf[sb ^ " + I(sw_off[r ^ x]) + "], o" +
+                 I(r) + ");\n";
+    }
+    for (int r = 0; r < D; ++r) e += "        xbuf[sb ^ " + I(sw_off[r]) + "] = o" + I(r) + ";\n";
+    e += "      }\n      __syncthreads();\n";
+    for (int i = 0; i < R; ++i)
+        e += std::string("      ") + v + "[" + I(i) + "] = xbuf[" + slot_base + " ^ " + I(slot_const(i)) + "];\n";
+    e += "      __syncthreads();\n    }\n";
+    return e;
+}
+
 std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *per_block);
 // Source of a kernel equivalent to k_regstage<false, false> on one lowered
 // stage program, with every structural quantity a literal: tile bits, layouts
@@ -1101,9 +1160,6 @@ std::string jit_forward_source(const RParams &P, bool *uses_spool, bool *per_blo
 }
 
 std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *per_block) {
-    for (int i = 0; i < P.nsubs; ++i)
-        for (int o = 0; o < P.subs[i].op_count; ++o)
-            if (P.ops[P.subs[i].op_begin + o].nt >= 3) return "";
     std::string src;
     auto out = [&](const std::string &x) { src += x; };
     auto num = [](unsigned long long v) { return std::to_string(v) + "ull"; };
@@ -1151,6 +1207,11 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
         }
         for (int k = 0; k < sb.op_count; ++k) {
             const ROp &op = P.ops[sb.op_begin + k];
+            if (op.nt >= 3) {
+                spool = true;
+                emit(jit_wide_op(P, sub, op, "v", op.mat, op.ident, ("st" + std::to_string(sub)).c_str()));
+                continue;
+            }
             const int dd = 1 << (2 * op.nt);
             std::string dyn;
             for (int q = 0; q < op.nc; ++q) {
@@ -1325,7 +1386,8 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool) {
     int nops_total = 0;
     for (int i = 0; i < P.nsubs; ++i)
         for (int o = 0; o < P.subs[i].op_count; ++o) {
-            if (P.ops[P.subs[i].op_begin + o].nt >= 3) return "";
+            const ROp &op = P.ops[P.subs[i].op_begin + o];
+            if (op.nt >= 3 && op.np > 0) return ""; // wide parametric steps are unfusable anyway
             ++nops_total;
         }
     if (nops_total == 0) return "";
@@ -1369,6 +1431,14 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool) {
         }
         for (int k = 0; k < sb.op_count; ++k) {
             const ROp &op = P.ops[sb.op_begin + k];
+            if (op.nt >= 3) {
+                spool = true;
+                const std::string sbase = "st" + I(sub);
+                emit(jit_wide_op(P, sub, op, "vf", op.mat, op.ident, sbase.c_str()));
+                emit(jit_wide_op(P, sub, op, "vg", op.pair ? op.mat_psi : op.mat,
+                                 op.pair ? op.ident_psi : op.ident, sbase.c_str()));
+                continue;
+            }
             const int dd = 1 << (2 * op.nt), nsub = 1 << op.nc;
             std::string dyn;
             for (int q = 0; q < op.nc; ++q) {
@@ -1616,7 +1686,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
         }
         RParams &P = *act.P;
         const ProfMark pf_ = prof_begin(st);
-        if (act.jit && REV) {
+        if (act.jit && act.jit->k.e && REV) {
             const JitShape &sh = *act.jit;
             const size_t sm = (size_t)(TS + (sh.spool ? P.npool : 0)) * sizeof(double2) +
                               sizeof(double) * (size_t)P.nslots * NW;
@@ -1632,7 +1702,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             }
             return;
         }
-        if (act.jit) {
+        if (act.jit && act.jit->k.e) {
             const JitShape &sh = *act.jit;
             const size_t sm = (size_t)((sh.per_block ? 1 : 2) * TS + (sh.spool ? P.npool : 0)) * sizeof(double2);
             static int nsm = 0;
@@ -1659,7 +1729,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
         check_launch(REV ? "k_regstage_rev" : "k_regstage", pf_);
     };
     auto submit = [&](Action &&act) {
-        if (use_jit && act.P && !act.has_wide) {
+        if (use_jit && act.P) {
             act.key = shape_key(*act.P, REV);
             act.hash = fnv1a(act.key);
             act.jit = find_shape(act.key, act.hash);
@@ -1724,12 +1794,17 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
         std::unordered_map<uint64_t, size_t> first;
         for (size_t i = 0; i < pending.size(); ++i) {
             Action &act = pending[i];
-            if (!act.P || act.has_wide || act.hash == 0) continue;
+            if (!act.P || act.hash == 0) continue;
             if ((act.jit = find_shape(act.key, act.hash))) continue;
             if (first.count(act.hash)) continue;
             bool sp = false, pb = REV;
             std::string src = REV ? jit_reverse_source(*act.P, &sp) : jit_forward_source(*act.P, &sp, &pb);
-            if (src.empty()) continue;
+            if (src.empty()) {
+                // not specialisable: remember that (no kernel), stay on the interpreter
+                std::lock_guard<std::mutex> lk(g_shape_mu);
+                g_shapes[act.hash].key = act.key;
+                continue;
+            }
             first[act.hash] = i;
             srcs.push_back(std::move(src));
             flags.emplace_back(sp, pb);
@@ -1748,7 +1823,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             }
         }
         for (Action &act : pending) {
-            if (act.P && !act.has_wide && act.hash != 0 && !act.jit) act.jit = find_shape(act.key, act.hash);
+            if (act.P && act.hash != 0 && !act.jit) act.jit = find_shape(act.key, act.hash);
             issue(act);
         }
     }
