@@ -372,7 +372,16 @@ def main():
             ach = step_flops / (fused_ms / 1e3) / 1e12
             roof["fp64"] = {"achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
                             "frac": ach / fp64_peak, "flops_per_step": step_flops,
-                            "peak_source": "nominal (no measured FP64 peak)"}
+                            "peak_source": "nominal (148 SM x 64 DFMA/clk x 2 x 1.965 GHz); "
+                                           "measured DFMA/DMMA ceilings in profiles/fp64_peak.json"}
+            try:
+                with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                       "fp64_peak.json")) as f:
+                    roof["fp64"]["measured_dfma_peak"] = json.load(f)["dfma_tflops"]
+            except Exception:
+                pass
+            # which ceiling the stage kernels sit closer to
+            roof["limiter"] = "fp64" if roof["fp64"]["frac"] > roof["frac"] else "hbm"
     algo_gbs = wl.algorithmic_bytes() / (ms_per_step / 1e3) / 1e9
 
     # end to end through the C-ABI with host buffers
