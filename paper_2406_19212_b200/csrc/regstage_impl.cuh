@@ -1498,7 +1498,9 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool) {
                     }
                 }
             } else {
-                for (int p = 0; p < op.np; ++p) emit("      double acc" + I(p) + " = 0;\n");
+                // per-slot accumulators live to the end of the tile; their warp
+                // reductions are issued together there (independent shuffle
+                // chains overlap instead of stalling each parametric step)
                 for (int i = 0; i < R; ++i) {
                     if (i & mask) continue;
                     const int cs = cstat(i);
@@ -1507,21 +1509,18 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool) {
                         emit("      {\n        const double2 w = cmul(" + elem(op.mat, c, cs) + ", vf[" + I(i) +
                              "]);\n        vf[" + I(i) + "] = w;\n");
                         for (int p = 0; p < op.np; ++p)
-                            emit("        acc" + I(p) + " += re_cj(vg[" + I(i) + "], cmul(" +
+                            emit("        acc_s" + I(op.slot + p) + " += re_cj(vg[" + I(i) + "], cmul(" +
                                  elem(op.mat_d + (unsigned)(p * nsub), c, cs) + ", w));\n");
                         emit("        vg[" + I(i) + "] = cmul(" + elem(op.mat, c, cs) + ", vg[" + I(i) +
                              "]);\n      }\n");
                     } else {
                         emit("      mv_group<" + tmpl + ">(vf, " + I(i) + ", " + mat(op.mat, c, cs, dd) + ");\n");
                         for (int p = 0; p < op.np; ++p)
-                            emit("      acc" + I(p) + " += dot_group<" + tmpl + ">(vf, vg, " + I(i) + ", " +
+                            emit("      acc_s" + I(op.slot + p) + " += dot_group<" + tmpl + ">(vf, vg, " + I(i) + ", " +
                                  mat(op.mat_d + (unsigned)(p * nsub * dd), c, cs, dd) + ");\n");
                         emit("      mv_group<" + tmpl + ">(vg, " + I(i) + ", " + mat(op.mat, c, cs, dd) + ");\n");
                     }
                 }
-                for (int p = 0; p < op.np; ++p)
-                    emit("      { const double x = warp_sum(acc" + I(p) + "); if (lane == 0) red[" +
-                         I((op.slot + p) * NW) + " + warp] = x; }\n");
             }
             emit("    }\n");
         }
@@ -1541,6 +1540,7 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool) {
             I(T) + ") spool[i] = P.pool[i];\n");
     out("  double *red = reinterpret_cast<double *>(sm + " + I(red_at) + ");\n");
     out("  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;\n");
+    for (int sl = 0; sl < P.nslots; ++sl) out("  double acc_s" + I(sl) + " = 0;\n");
     int nat_local[TB];
     for (int b = 0; b < TB; ++b) nat_local[b] = b;
     out("  const u64 glo = " + thread_expr(nat_local, true, "t") + ";\n");
@@ -1586,6 +1586,12 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool) {
             "];\n");
     }
     if (P.nslots > 0) {
+        for (int sl = 0; sl < P.nslots; ++sl)
+            out("  acc_s" + I(sl) + " = warp_sum(acc_s" + I(sl) + ");\n");
+        out("  if (lane == 0) {\n");
+        for (int sl = 0; sl < P.nslots; ++sl)
+            out("    red[" + I(sl * NW) + " + warp] = acc_s" + I(sl) + ";\n");
+        out("  }\n");
         out("  __syncthreads();\n");
         out("  for (int s = t; s < " + I(P.nslots) + "; s += " + I(T) + ") {\n    double x = 0;\n");
         for (int w = 0; w < NW; ++w) out("    x += red[s * " + I(NW) + " + " + I(w) + "];\n");
