@@ -98,6 +98,11 @@ struct ROp {
     int tab, tab_psi;     // nt = 0 with register conditions: shared-memory tables
     int xoff, nx;         // nt >= 3: XOR patterns of the diagonal-times-permutation terms
     int lb[kMaxMix];      // nt >= 3: tile-local mixing bits in matrix bit order
+    // nt = 0 adjoint steps: every phase has modulus 1 (conj(psi) phi is then
+    // invariant under the step) and, for parametric ones, the tables
+    // e_p[c] = D_p[c] * M[c] at pool offset mat_e
+    int unit;
+    unsigned mat_e;
 };
 
 struct RSub {
@@ -840,7 +845,7 @@ void lower_stage_reg(const Stage &sg, const std::vector<FusedOp> &blocks,
         if (f.nt >= 3) // XOR-term form: |X| * D entries per sub-matrix
             return (count_x(f) * (1 << f.nt) << f.nc) * (1 + (f.pair ? 1 : 0));
         const int dd = (1 << (2 * f.nt)) << f.nc;
-        return dd * (1 + (f.pair ? 1 : 0) + (rev ? f.np : 0));
+        return dd * (1 + (f.pair ? 1 : 0) + (rev ? f.np : 0)) + (rev && f.nt == 0 ? f.np << f.nc : 0);
     };
     int nops = 0, npool = 0, nslots = 0;
     while (!remaining.empty()) {
@@ -994,9 +999,22 @@ void lower_stage_reg(const Stage &sg, const std::vector<FusedOp> &blocks,
                 o.mat = push(f.sub_phi, 0, &o.ident);
                 if (f.pair) o.mat_psi = push(f.sub_psi, 0, &o.ident_psi);
             }
+            if (rev && f.nt == 0 && !f.pair) {
+                o.unit = 1;
+                for (int c = 0; c < (1 << f.nc); ++c)
+                    if (std::abs(std::abs(f.sub_phi[c]) - 1.0) > 1e-13) o.unit = 0;
+            }
             if (o.np > 0) {
                 o.mat_d = (unsigned)npool;
                 for (int p = 0; p < f.np; ++p) push(f.sub_d, size_t(p) << f.nc, nullptr);
+                if (f.nt == 0) {
+                    o.mat_e = (unsigned)npool;
+                    for (int p = 0; p < f.np; ++p)
+                        for (int c = 0; c < (1 << f.nc); ++c) {
+                            const cplx e = f.sub_d[(size_t(p) << f.nc) + c] * f.sub_phi[c];
+                            P.pool[npool++] = make_double2(e.real(), e.imag());
+                        }
+                }
                 o.ident = 0;
                 o.slot = nslots;
                 for (int p = 0; p < f.np; ++p) {
@@ -1431,6 +1449,58 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool) {
         }
         for (int k = 0; k < sb.op_count; ++k) {
             const ROp &op = P.ops[sb.op_begin + k];
+            // a run of unit-modulus diagonal steps: conj(psi) phi is invariant
+            // along it, so every contribution is Re(z e_p) with z taken once,
+            // and both states get the product of the phases at the end
+            int run_end = k;
+            while (run_end < sb.op_count && P.ops[sb.op_begin + run_end].nt == 0 &&
+                   P.ops[sb.op_begin + run_end].unit && !P.ops[sb.op_begin + run_end].pair)
+                ++run_end;
+            if (run_end - k >= 2) {
+                emit("    {\n");
+                for (int j = k; j < run_end; ++j) {
+                    const ROp &oj = P.ops[sb.op_begin + j];
+                    std::string dyn;
+                    for (int q = 0; q < oj.nc; ++q) {
+                        if (oj.ck[q] == 0)
+                            dyn += " | (int)(((base >> " + I(oj.cp[q]) + ") & 1) << " + I(q) + ")";
+                        else if (oj.ck[q] == 1)
+                            dyn += " | (((to >> " + I(oj.cp[q]) + ") & 1) << " + I(q) + ")";
+                    }
+                    emit("      const int cd" + I(j) + " = 0" + dyn + ";\n");
+                    if (!dyn.empty()) spool = true;
+                }
+                for (int i = 0; i < R; ++i) {
+                    emit("      {\n        const double2 z = make_double2(fma(vg[" + I(i) + "].x, vf[" + I(i) +
+                         "].x, vg[" + I(i) + "].y * vf[" + I(i) + "].y), fma(vg[" + I(i) + "].x, vf[" + I(i) +
+                         "].y, -vg[" + I(i) + "].y * vf[" + I(i) + "].x));\n        double2 ph = make_double2(1.0, 0.0);\n");
+                    for (int j = k; j < run_end; ++j) {
+                        const ROp &oj = P.ops[sb.op_begin + j];
+                        int cs = 0;
+                        bool dyn = false;
+                        for (int q = 0; q < oj.nc; ++q) {
+                            if (oj.ck[q] == 2 && ((i >> oj.cp[q]) & 1)) cs |= 1 << q;
+                            if (oj.ck[q] != 2) dyn = true;
+                        }
+                        const std::string c = dyn ? "(cd" + I(j) + " | " + I(cs) + ")" : I(cs);
+                        auto elem = [&](unsigned off) {
+                            return dyn ? "spool[" + I(off) + " + " + c + "]" : "P.pool[" + I(off + (unsigned)cs) + "]";
+                        };
+                        for (int p = 0; p < oj.np; ++p) {
+                            const std::string e = elem(oj.mat_e + (unsigned)(p << oj.nc));
+                            emit("        { const double2 e = " + e + "; acc_s" + I(oj.slot + p) +
+                                 " += fma(z.x, e.x, -z.y * e.y); }\n");
+                        }
+                        if (dyn || !((oj.ident >> cs) & 1))
+                            emit("        ph = cmul(" + elem(oj.mat) + ", ph);\n");
+                    }
+                    emit("        vf[" + I(i) + "] = cmul(ph, vf[" + I(i) + "]);\n        vg[" + I(i) +
+                         "] = cmul(ph, vg[" + I(i) + "]);\n      }\n");
+                }
+                emit("    }\n");
+                k = run_end - 1;
+                continue;
+            }
             if (op.nt >= 3) {
                 spool = true;
                 const std::string sbase = "st" + I(sub);
