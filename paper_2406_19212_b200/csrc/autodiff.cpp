@@ -14,10 +14,22 @@ namespace vqb {
 
 namespace {
 
+// Device buffer for the gradient vector and the loss, reused across calls
+// on a thread (grow-only): a cudaMalloc/cudaFree pair per call would cost
+// more than a small gradient (and cudaFree synchronises the device).
 struct DevBuf {
     void *p = nullptr;
-    explicit DevBuf(size_t bytes) { VQB_CUDA(cudaMalloc(&p, bytes)); }
-    ~DevBuf() { cudaFree(p); }
+    explicit DevBuf(size_t bytes) {
+        static thread_local void *cached = nullptr;
+        static thread_local size_t cap = 0;
+        if (bytes > cap) {
+            if (cached) cudaFree(cached);
+            cached = nullptr;
+            VQB_CUDA(cudaMalloc(&cached, bytes));
+            cap = bytes;
+        }
+        p = cached;
+    }
     template <typename T> T *as() { return static_cast<T *>(p); }
 };
 

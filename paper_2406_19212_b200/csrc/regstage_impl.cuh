@@ -1456,7 +1456,7 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool) {
             while (run_end < sb.op_count && P.ops[sb.op_begin + run_end].nt == 0 &&
                    P.ops[sb.op_begin + run_end].unit && !P.ops[sb.op_begin + run_end].pair)
                 ++run_end;
-            if (run_end - k >= 2) {
+            if (run_end - k >= 2 && env_int("VQB_JIT_DIAGRUN", 0)) {
                 emit("    {\n");
                 for (int j = k; j < run_end; ++j) {
                     const ROp &oj = P.ops[sb.op_begin + j];
@@ -1690,7 +1690,7 @@ std::string shape_key(const RParams &P, bool rev) {
     std::string key(rev ? "R" : "F");
     key.append(b, pool_at);
     key.append(b + rest_at, sizeof(RParams) - rest_at);
-    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS"}) {
+    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN"}) {
         const char *v = std::getenv(e);
         key += '|';
         if (v) key += v;
@@ -1920,7 +1920,9 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             total_slots, static_cast<const double *>(m_slotsum.p), dgrads);
         check_launch("k_grads", pf_);
     }
-    VQB_CUDA(cudaStreamSynchronize(st)); // host-side slot vectors outlive the copies
+    // no synchronisation: kernel parameters are copied at launch and the
+    // pageable slot vectors are staged by cudaMemcpyAsync before it returns,
+    // so the caller's next host work overlaps this program on the device
 }
 
 } // namespace
