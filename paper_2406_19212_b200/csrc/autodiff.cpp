@@ -150,7 +150,10 @@ GradientOut gradient_pure(const vqb_op *ops, int64_t count, const vqb_pauli_term
 
     DeviceState *phi = clone(s0);
     StateGuard gphi{phi};
-    run_program(phi, fwd, fused);
+    {
+        HostTimer ht("gradient_pure forward");
+        run_program(phi, fwd, fused);
+    }
 
     GradientOut out;
     out.grads.assign(total, 0.0);
@@ -168,7 +171,15 @@ GradientOut gradient_pure(const vqb_op *ops, int64_t count, const vqb_pauli_term
     double2 *dloss = reinterpret_cast<double2 *>(dbuf.as<char>() + gbytes);
     dot_async(phi, phi->amps, psi->amps, dloss); // loss = Re <phi|H phi>
 
-    run_reverse(phi, psi, pure_reverse_program(es, base), dgrads, fused);
+    {
+        HostTimer ht("gradient_pure reverse");
+        std::vector<RevOp> rprog;
+        {
+            HostTimer ht2("reverse program");
+            rprog = pure_reverse_program(es, base);
+        }
+        run_reverse(phi, psi, rprog, dgrads, fused);
+    }
 
     double2 hl;
     VQB_CUDA(cudaMemcpyAsync(out.grads.data(), dgrads, sizeof(double) * total,

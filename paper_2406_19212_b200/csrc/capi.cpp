@@ -217,8 +217,13 @@ VQB_API int vqb_apply_matrix(vqb_state *s, const int32_t *pos, int32_t m, const 
 
 static void apply_circuit_impl(vqb_state *s, const vqb_op *ops, int64_t count, bool fused) {
     DeviceState *d = ds(s);
+    HostTimer ht_call("apply_circuit (to launch end)");
     if (count > 0) need(ops, "ops");
-    const auto es = build_elements(ops, count);
+    std::vector<Element> es;
+    {
+        HostTimer ht("build_elements");
+        es = build_elements(ops, count);
+    }
     for (const auto &e : es) {
         if (e.channel) {
             if (!d->mixed)
@@ -237,6 +242,7 @@ static void apply_circuit_impl(vqb_state *s, const vqb_op *ops, int64_t count, b
         for (const auto &e : es) prog.push_back(e.gate);
         run_program(d, prog, fused);
     }
+    HostTimer ht_sync("apply_circuit sync");
     sync(d);
 }
 

@@ -1,6 +1,10 @@
 // Common host/device definitions for libvqcs_b200.
 #pragma once
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 
 #include <complex>
@@ -12,6 +16,32 @@
 #include "../../include/vqcs_b200.h"
 
 namespace vqb {
+
+// Accumulating host timer (VQB_HOST_TIMING): add the scope's time to *acc.
+struct HostAcc {
+    double *acc;
+    std::chrono::steady_clock::time_point t0;
+    explicit HostAcc(double *a) : acc(a), t0(std::chrono::steady_clock::now()) {}
+    ~HostAcc() {
+        *acc += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    }
+};
+
+// Host-side phase timing for diagnostics (VQB_HOST_TIMING=1 prints to stderr).
+struct HostTimer {
+    const char *what;
+    std::chrono::steady_clock::time_point t0;
+    bool on;
+    explicit HostTimer(const char *w) : what(w), t0(std::chrono::steady_clock::now()) {
+        static const bool enabled = std::getenv("VQB_HOST_TIMING") != nullptr;
+        on = enabled;
+    }
+    ~HostTimer() {
+        if (!on) return;
+        const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+        std::fprintf(stderr, "[host] %-28s %9.1f us\n", what, us);
+    }
+};
 
 using cplx = std::complex<double>;
 using cvec = std::vector<cplx>;

@@ -268,7 +268,11 @@ void run_reverse(DeviceState *phi, DeviceState *psi, const std::vector<RevOp> &p
         if (nf && *nf == '1') {
             run_reverse_fused(phi, psi, prog, dgrads);
         } else {
-            const std::vector<RevOp> folded = fold_reverse_program(prog);
+            std::vector<RevOp> folded;
+            {
+                HostTimer ht("fold_reverse_program");
+                folded = fold_reverse_program(prog);
+            }
             run_reverse_fused(phi, psi, folded, dgrads);
         }
         return;

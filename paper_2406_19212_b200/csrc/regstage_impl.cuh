@@ -1680,16 +1680,33 @@ struct JitShape {
     bool spool = false, per_block = false;
 };
 uint64_t fnv1a(const std::string &s) {
+    // word-wise FNV-1a variant (the key is a few KB per launch)
     uint64_t h = 1469598103934665603ull;
-    for (unsigned char c : s) h = (h ^ c) * 1099511628211ull;
+    size_t i = 0;
+    for (; i + 8 <= s.size(); i += 8) {
+        uint64_t w;
+        std::memcpy(&w, s.data() + i, 8);
+        h = (h ^ w) * 1099511628211ull;
+        h ^= h >> 29;
+    }
+    for (; i < s.size(); ++i) h = (h ^ (unsigned char)s[i]) * 1099511628211ull;
     return h;
 }
 std::string shape_key(const RParams &P, bool rev) {
-    const char *b = reinterpret_cast<const char *>(&P);
-    const size_t pool_at = offsetof(RParams, pool), rest_at = offsetof(RParams, ntab);
+    // the used parts of the structural fields (everything but the matrix
+    // values; unused array tails are zero by construction)
+    int nops = 0;
+    for (int i = 0; i < P.nsubs; ++i) nops = std::max(nops, P.subs[i].op_begin + P.subs[i].op_count);
     std::string key(rev ? "R" : "F");
-    key.append(b, pool_at);
-    key.append(b + rest_at, sizeof(RParams) - rest_at);
+    auto add = [&](const void *p, size_t n) { key.append(static_cast<const char *>(p), n); };
+    add(P.bits, sizeof P.bits);
+    add(&P.ntiles, sizeof P.ntiles);
+    add(&P.nsubs, 4 * sizeof(int)); // nsubs, nslots, slot_begin, partial_ld
+    add(P.subs, sizeof(RSub) * (size_t)P.nsubs);
+    add(P.ops, sizeof(ROp) * (size_t)nops);
+    add(&P.ntab, 3 * sizeof(int)); // ntab, nxpat, npool
+    add(P.xpat, (size_t)P.nxpat);
+    add(P.fast, sizeof(int) * (size_t)nops);
     for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN"}) {
         const char *v = std::getenv(e);
         key += '|';
@@ -1710,9 +1727,22 @@ const JitShape *find_shape(const std::string &key, uint64_t h) {
 template <bool REV, typename Fallback>
 void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, double *dgrads,
              Fallback &&fallback) {
+    HostTimer ht_all(REV ? "run_reg (rev) total" : "run_reg (fwd) total");
+    double t_fuse = 0, t_lower = 0, t_key = 0, t_issue = 0;
+    struct Report {
+        double *a, *b, *c, *d;
+        ~Report() {
+            static const bool on = std::getenv("VQB_HOST_TIMING") != nullptr;
+            if (on) std::fprintf(stderr, "[host]   fuse %.1f lower %.1f key %.1f issue %.1f us\n", *a, *b, *c, *d);
+        }
+    } report{&t_fuse, &t_lower, &t_key, &t_issue};
     const int pn = sphi->pn;
     cudaStream_t st = sphi->stream;
-    const auto stages = plan_stages(fops, pn, K);
+    std::vector<Stage> stages;
+    {
+        HostTimer ht(REV ? "plan_stages (rev)" : "plan_stages (fwd)");
+        stages = plan_stages(fops, pn, K);
+    }
     const int max_support = env_int("VQB_FUSE_QUBITS", 2);
     const bool stats = std::getenv("VQB_PLAN_STATS") != nullptr;
     const unsigned long long ntiles = 1ull << (pn - K);
@@ -1806,13 +1836,17 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
     };
     auto submit = [&](Action &&act) {
         if (use_jit && act.P) {
+            HostAcc ha(&t_key);
             act.key = shape_key(*act.P, REV);
             act.hash = fnv1a(act.key);
             act.jit = find_shape(act.key, act.hash);
             if (!act.jit) batching = true; // compile later, with the other misses
         }
         if (batching) pending.push_back(std::move(act));
-        else issue(act);
+        else {
+            HostAcc ha(&t_issue);
+            issue(act);
+        }
     };
     for (const Stage &sg : stages) {
         if (!sg.fused) {
@@ -1822,6 +1856,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             continue;
         }
         std::vector<FusedOp> blocks;
+        HostAcc ha_f(&t_fuse);
         if (max_support > 0) blocks = fuse_blocks(fops, sg.ops, max_support);
         else
             for (int idx : sg.ops) blocks.push_back(fops[idx]);
@@ -1831,7 +1866,10 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             Action act;
             act.P = std::make_unique<RParams>();
             RParams &P = *act.P;
-            lower_stage_reg(sg, blocks, remaining, pn, REV, P, slots);
+            {
+                HostAcc ha(&t_lower);
+                lower_stage_reg(sg, blocks, remaining, pn, REV, P, slots);
+            }
             P.partial_ld = total_slots;
             if (stats) {
                 int nt_hist[5] = {0, 0, 0, 0, 0}, nops = 0;
@@ -1932,7 +1970,10 @@ bool regstage_available(int pn) { return pn >= K + 2; }
 void run_program_reg(DeviceState *s, const std::vector<Gate> &prog) {
     std::vector<FusedOp> fops;
     fops.reserve(prog.size());
-    for (const auto &g : prog) fops.push_back(analyse_gate(g));
+    {
+        HostTimer ht("analyse_gate x n");
+        for (const auto &g : prog) fops.push_back(analyse_gate(g));
+    }
     run_reg<false>(s, nullptr, fops, nullptr, [&](const FusedOp &f) {
         apply_gate_fast(s->amps, s->pn, f.gate, s->stream);
     });
@@ -1940,6 +1981,7 @@ void run_program_reg(DeviceState *s, const std::vector<Gate> &prog) {
 
 void run_reverse_reg(DeviceState *phi, DeviceState *psi, const std::vector<RevOp> &prog,
                      double *dgrads) {
+    HostTimer ht("run_reverse_reg (analyse+run)");
     std::vector<FusedOp> fops;
     fops.reserve(prog.size());
     for (const auto &r : prog) {
