@@ -5,7 +5,13 @@ Default (N=1): config 1 — the 28-qubit random circuit (4x7 grid, 20 cycles,
 785 gates, complex128) — through ``vqb_apply_circuit``; metric gates/s.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                  [--config rqc28|hea20|qaoa30|noisy15] [--unfused]
+                  [--config rqc28|hea20|qaoa30|noisy15|rqc33] [--unfused]
+
+``rqc33`` is config 4: the same random-circuit family on 33 + log2(N) qubits
+(grids 3x11 / 2x17 / 5x7 / 6x6, 14 cycles), 2^33 amplitudes (128 GiB) per GPU;
+at N > 1 the top log2(N) qubits are sharded over the ranks with global<->local
+swaps over NCCL (``distributed.ShardedState``, weak scaling). ``qaoa30`` at
+N > 1 runs config 2's adjoint gradient on the sharded layout (strong scaling).
 
 A step = reset the device state to |0...0> and run the whole circuit (or one
 full adjoint gradient evaluation for hea20/qaoa30/noisy15). `value` is timed
@@ -13,7 +19,8 @@ with CUDA events on the state's stream over exactly K steps after W warm-up
 steps, max over ranks; `e2e` is the same metric through the C-ABI with the
 state round-tripping through pinned HOST memory every step (upload before,
 download after, inside the timed region). Under torchrun (N>1) each rank runs
-an independent replica (config 1 does not shard: "replicas", weak scaling).
+an independent replica for rqc28/hea20/noisy15 (single-GPU configs:
+"replicas", weak scaling); rqc33 and qaoa30 shard (see above).
 
 `--impl reference` times the reference's own CPU implementation
 (oracle/_ref/libvqcs_ref.so, compiled from /root/reference) on all host
@@ -57,10 +64,14 @@ def hbm_peak():
 class Workload:
     """metric unit per step and the per-step call."""
 
-    def __init__(self, name, args):
+    def __init__(self, name, args, world=1):
         self.name = name
         self.fused = not args.unfused
-        if name == "rqc28":
+        self.sharded = world > 1 and name in ("rqc33", "qaoa30")
+        if name == "rqc33":
+            self.w = circuits.config4(num_gpus=world)
+            self.kind = "apply"
+        elif name == "rqc28":
             self.w = circuits.config1()
             self.kind = "apply"
         elif name == "hea20":
@@ -92,9 +103,12 @@ class Workload:
         else:
             eng.gradient_mixed(self.w.observable, self.w.circuit, state)
 
-    def algorithmic_bytes(self) -> float:
-        """SURVEY.md §8(d) touched-amplitude rule over the reference schedule."""
+    def algorithmic_bytes(self, world: int = 1) -> float:
+        """SURVEY.md §8(d) touched-amplitude rule over the reference schedule
+        (per GPU: a sharded state holds 2^(n - log2 N) amplitudes per rank)."""
         pn = 2 * self.n if self.mixed else self.n
+        if self.sharded:
+            pn -= int(round(math.log2(world)))
         unit = 32.0 * (1 << pn)
         fwd = sum(circuits.touched_fraction(e) for e in self.w.circuit.elements)
         if self.kind == "apply":
@@ -206,14 +220,59 @@ def reference_engine():
 
 
 def reference_sample(wl: Workload, full: bool = False):
-    """A bounded prefix of the workload for the CPU reference (10-30 s)."""
-    if wl.kind == "apply":
+    """A bounded sample of the workload for the CPU reference (about 10-30 s of
+    host work) -> (run(eng) -> None, units of the metric the sample is worth,
+    description). Samples smaller than the workload are scaled to it by the
+    amplitude-count ratio (every reference kernel is a linear pass over the
+    state, kernels.hpp:128-176) and say so."""
+    if wl.kind == "apply" and wl.n <= 28:
         k = 160 if full else 80
-        return Circuit(wl.w.circuit.elements[:k]), k, f"first {k} of {wl.gates} gates at n={wl.n}"
+        circ = Circuit(wl.w.circuit.elements[:k])
+
+        def run(eng):
+            st = eng.create(wl.n, wl.mixed)
+            eng.apply_circuit(circ, st)
+            st.free()
+        return run, float(k), f"first {k} of {wl.gates} gates at n={wl.n}"
+    if wl.kind == "apply":
+        # config 4 (33+ qubits, 128 GiB+) does not fit the host: the config-1
+        # family at 28 qubits, gates/s scaled by 2^(28-n)
+        k = 160 if full else 80
+        w28 = circuits.config1()
+        circ = Circuit(w28.circuit.elements[:k])
+        scale = 2.0 ** (28 - wl.n)
+
+        def run(eng):
+            st = eng.create(28, False)
+            eng.apply_circuit(circ, st)
+            st.free()
+        return run, k * scale, (f"first {k} gates of the 28-qubit member of the same circuit family, "
+                                f"gates/s extrapolated to n={wl.n} by 2^(28-{wl.n}) (state does not fit the host)")
     if wl.name == "hea20":
-        return wl.w.circuit, 1, "one full gradient evaluation (20q, 600 params)"
-    # 30q QAOA / 15q noisy gradient: one layer-sized prefix at reduced size
-    return None, 0, "n/a"
+        def run(eng):
+            st = eng.create(wl.n, False)
+            eng.gradient_pure(wl.w.observable, wl.w.circuit, st)
+            st.free()
+        return run, 1.0, "one full gradient evaluation (20q, 600 params)"
+    if wl.name == "qaoa30":
+        small = circuits.config2(n=22, p=wl.w.extra["p"], seed=wl.w.seed)
+
+        def run(eng):
+            st = eng.create(small.num_qubits, False)
+            eng.gradient_pure(small.observable, small.circuit, st)
+            st.free()
+        return run, 2.0 ** (22 - wl.n), ("one gradient evaluation of the same QAOA family (3-regular, p=8) at "
+                                         f"n=22, evals/s extrapolated to n={wl.n} by 2^(22-{wl.n})")
+    if wl.name == "noisy15":
+        small = circuits.config3(n=11)
+
+        def run(eng):
+            st = eng.create(small.num_qubits, True)
+            eng.gradient_mixed(small.observable, small.circuit, st)
+            st.free()
+        return run, 4.0 ** (11 - wl.n), ("one noisy gradient evaluation of the same ansatz (6 layers) at n=11 "
+                                         f"(4^11 entries), evals/s extrapolated to n={wl.n} by 4^(11-{wl.n})")
+    return None, 0.0, "n/a"
 
 
 def run_reference_arm(args, wl, world, rank):
@@ -228,19 +287,15 @@ def run_reference_arm(args, wl, world, rank):
         line["unavailable"] = threads
         print(json.dumps(line))
         return 0
-    circ, units, sample = reference_sample(wl)
-    if circ is None:
+    run, units, sample = reference_sample(wl)
+    if run is None:
         line["unavailable"] = f"no bounded reference sample defined for {wl.name}"
         print(json.dumps(line))
         return 0
-    st = eng.create(wl.n, wl.mixed)
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        if wl.kind == "apply":
-            eng.apply_circuit(circ, st)
-        else:
-            eng.gradient_pure(wl.w.observable, circ, st)
+        run(eng)
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(dt)
@@ -259,19 +314,50 @@ def cpu_baseline(wl: Workload):
     eng, threads = reference_engine()
     if eng is None:
         return None
-    circ, units, sample = reference_sample(wl, full=True)
-    if circ is None:
+    run, units, sample = reference_sample(wl, full=True)
+    if run is None:
         return None
-    st = eng.create(wl.n, wl.mixed)
     t0 = time.perf_counter()
-    if wl.kind == "apply":
-        eng.apply_circuit(circ, st)
-    else:
-        eng.gradient_pure(wl.w.observable, circ, st)
+    run(eng)
     dt = time.perf_counter() - t0
-    st.free()
     return {"value": units / dt, "unit": wl.unit, "cores": threads, "kind": "reference",
             "sample": sample + f"; {dt:.2f} s on the GPU box host"}
+
+
+# ------------------------------------------------------------------ sharded runs (N > 1)
+class ShardedRunner:
+    """Config 4 (rqc33: 33 + log2 N qubits, 2^33 amplitudes per rank) and
+    config 2 (qaoa30 gradient, 2^(30 - log2 N) per rank) on the sharded layout
+    of distributed.ShardedState: the shard is a torch CUDA tensor, local runs
+    go through the fused executor (vqb_state_wrap), global<->local swaps and
+    reductions through torch.distributed over NCCL."""
+
+    def __init__(self, eng, wl, dist, rank, world, local):
+        import torch
+        from paper_2406_19212_b200.distributed import DeviceEngine, ShardedState
+        g = int(round(math.log2(world)))
+        self.wl = wl
+        shard = torch.zeros(1 << (wl.n - g), dtype=torch.complex128, device=f"cuda:{local}")
+        self.st = ShardedState(wl.n, dist, DeviceEngine(eng), shard, rank, world)
+        self.loss = None
+
+    def reset(self):
+        self.st.set_zero()
+
+    def step(self):
+        if self.wl.kind == "apply":
+            self.st.apply_circuit(self.wl.w.circuit)
+        else:
+            self.loss, _ = self.st.gradient_pure(self.wl.w.observable, self.wl.w.circuit)
+
+    def norm(self):
+        return self.st.norm()
+
+    def stats(self):
+        return {"swaps": self.st.swaps, "bytes_exchanged_per_rank": self.st.bytes_exchanged}
+
+    def free(self):
+        self.st.local = None
 
 
 # ------------------------------------------------------------------ main
@@ -281,7 +367,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="rqc28", choices=["rqc28", "hea20", "qaoa30", "noisy15"])
+    ap.add_argument("--config", default="rqc28", choices=["rqc28", "hea20", "qaoa30", "noisy15", "rqc33"])
     ap.add_argument("--unfused", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -289,7 +375,7 @@ def main():
     args.warmup = max(args.warmup, 3)
 
     world, rank, local, dist = dist_setup(args)
-    wl = Workload(args.config, args)
+    wl = Workload(args.config, args, world)
     if args.impl == "reference":
         return run_reference_arm(args, wl, world, rank)
 
@@ -297,16 +383,23 @@ def main():
     import paper_2406_19212_b200 as vqb
     torch.cuda.set_device(local)
     eng = vqb.device()
-    state = eng.create(wl.n, wl.mixed)
-    stream = torch.cuda.ExternalStream(eng.stream_of(state), device=torch.device("cuda", local))
+    if wl.sharded:
+        runner = ShardedRunner(eng, wl, dist, rank, world, local)
+        state = runner
+        stream = torch.cuda.current_stream()
+        reset = runner.reset
+    else:
+        state = eng.create(wl.n, wl.mixed)
+        stream = torch.cuda.ExternalStream(eng.stream_of(state), device=torch.device("cuda", local))
 
-    def reset():
-        eng.check(eng._fn("state_set_zero")(state.handle))
+        def reset():
+            eng.check(eng._fn("state_set_zero")(state.handle))
 
+    step = runner.step if wl.sharded else (lambda: wl.step(eng, state))
     # warm-up
     for _ in range(args.warmup):
         reset()
-        wl.step(eng, state)
+        step()
     torch.cuda.synchronize()
 
     # timed region
@@ -319,7 +412,7 @@ def main():
         ev0.record(stream)
         for _ in range(args.steps):
             reset()
-            wl.step(eng, state)
+            step()
         ev1.record(stream)
         ev1.synchronize()
     torch.cuda.synchronize()
@@ -333,13 +426,15 @@ def main():
     # sanity of the result
     check = {}
     if wl.kind == "apply" and not wl.mixed:
-        check["norm"] = eng.norm(state)
+        check["norm"] = state.norm() if wl.sharded else eng.norm(state)
+    if wl.sharded:
+        check.update(runner.stats())
 
     # roofline: per-kernel CUDA-event timing of one more step (untimed)
     reset()
     f0 = eng.flop_count()
     eng.profile_begin()
-    wl.step(eng, state)
+    step()
     prof = eng.profile_end()
     step_flops = eng.flop_count() - f0
     peak, peak_kind = hbm_peak()
@@ -348,7 +443,12 @@ def main():
         top = max(prof.items(), key=lambda kv: kv[1][1])
         name, (cnt, tot_ms) = top
         pn = 2 * wl.n if wl.mixed else wl.n
-        bytes_per_launch = 32.0 * (1 << pn)  # one read + one write pass of the state
+        if wl.sharded:
+            pn -= int(round(math.log2(world)))
+        # one read + one write pass of the state; the adjoint kernels stream
+        # both Phi and Psi
+        nstates = 2 if "rev" in name else 1
+        bytes_per_launch = 32.0 * nstates * (1 << pn)
         avg_s = tot_ms / cnt / 1e3
         achieved = bytes_per_launch / avg_s / 1e9
         traffic = None
@@ -382,11 +482,45 @@ def main():
                 pass
             # which ceiling the stage kernels sit closer to
             roof["limiter"] = "fp64" if roof["fp64"]["frac"] > roof["frac"] else "hbm"
-    algo_gbs = wl.algorithmic_bytes() / (ms_per_step / 1e3) / 1e9
+    algo_gbs = wl.algorithmic_bytes(world) / (ms_per_step / 1e3) / 1e9
 
     # end to end through the C-ABI with host buffers
     e2e = None
-    if not args.no_e2e:
+    state_bytes = 16 * (1 << ((2 * wl.n if wl.mixed else wl.n) - (int(round(math.log2(world))) if wl.sharded else 0)))
+    if not args.no_e2e and (wl.sharded or state_bytes > (32 << 30)):
+        # config 4: the state (128 GiB per GPU) cannot round-trip through host
+        # memory every step; the user call is vqb_state_set_zero (the
+        # reference's PureState(n) constructor) + vqb_apply_circuit with the
+        # circuit packed from host objects + the norm read back to the host
+        import ctypes as ct
+        from paper_2406_19212_b200.abi import pack_ops, vqb_op
+
+        def e2e_step():
+            if wl.sharded:
+                runner.reset()
+                runner.step()
+                return state.norm()
+            reset()
+            eng.apply_circuit(wl.w.circuit, state)
+            return eng.norm(state)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier(dist, local)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        e1.synchronize()
+        ems = max_over_ranks(dist, e0.elapsed_time(e1))
+        e2e = {"value": world * wl.units_per_step * args.steps / (ems / 1e3), "unit": wl.unit,
+               "h2d_bytes_per_step": ct.sizeof(vqb_op) * wl.gates, "d2h_bytes_per_step": 8,
+               "ms_per_step": ems / args.steps,
+               "path": "vqb_state_set_zero -> vqb_apply_circuit (ops packed from host objects) -> vqb_norm "
+                       "(the 128 GiB state does not round-trip through host memory)"}
+    elif not args.no_e2e:
         nbytes = 16 * state.size
         h_in = torch.zeros(2 * state.size, dtype=torch.float64, pin_memory=True)
         h_in[0] = 1.0
@@ -426,16 +560,20 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         state.free()
         cpu = cpu_baseline(wl)
+    if wl.sharded:
+        state.free()
 
     if rank == 0:
         line = {
             "metric": wl.metric, "value": value, "unit": wl.unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+            "higher_is_better": True, "scaling": "strong" if (wl.sharded and wl.name == "qaoa30") else "weak",
+            "vs_baseline": None, "dtype": "c128",
             "data": "synthetic (seeded SplitMix64 circuit, |0...0> start)",
             "config": {"workload": wl.w.name, "qubits": wl.n, "mixed": wl.mixed,
                        "elements": wl.gates, "seed": wl.w.seed, "fused": wl.fused,
-                       "parallelism": "replicas" if world > 1 else "single",
+                       "parallelism": (f"sharded top {int(round(math.log2(world)))} qubits over {world} ranks"
+                                       if wl.sharded else ("replicas" if world > 1 else "single")),
                        "l2": (f"state {16 * (1 << (2 * wl.n if wl.mixed else wl.n)) / 2**30:.2f} GiB"
                               " vs 126 MB L2: "
                               + ("inputs larger than L2, no flush" if wl.n + (wl.n if wl.mixed else 0) >= 24

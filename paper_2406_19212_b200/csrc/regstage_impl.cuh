@@ -1104,13 +1104,113 @@ template <bool REV, bool WIDE> int grid_size(unsigned long long ntiles, size_t s
 }
 
 
+
+// ---------------------------------------------------------------- structure-aware emission
+// The specialised kernels read matrix values at run time, but which entries
+// are exactly zero, purely real or purely imaginary is structure: channel
+// superoperators are real and sparse (a depolarizing channel is
+// (1-p) I + p * trace-and-replace), rotations about X/Y and their derivatives
+// have purely real / imaginary entries, controlled blocks are mostly zero.
+// That class (bit 0: some real part nonzero, bit 1: some imaginary part
+// nonzero, over every sub-matrix the code may select) is part of the kernel
+// key, and each term is emitted with only the FMAs its class needs. Dropped
+// terms are exact zeros, so the result equals the dense product (up to the
+// sign of zero).
+int pool_cls(const RParams &P, unsigned off, int count, int stride) {
+    int c = 0;
+    for (int k = 0; k < count; ++k) {
+        const double2 v = P.pool[off + (unsigned)(k * stride)];
+        if (v.x != 0.0 || v.x != v.x) c |= 1;
+        if (v.y != 0.0 || v.y != v.y) c |= 2;
+    }
+    return c;
+}
+
+// acc (=|+=) m * x for an entry of class cls; adds the FP64 flops per thread
+std::string cterm(const std::string &m, const std::string &x, const std::string &acc, int cls, bool first,
+                  double &fl) {
+    switch (cls) {
+    case 0:
+        return "";
+    case 1:
+        fl += 4;
+        return first ? "        " + acc + " = make_double2(" + m + ".x * " + x + ".x, " + m + ".x * " + x + ".y);\n"
+                     : "        " + acc + ".x = fma(" + m + ".x, " + x + ".x, " + acc + ".x); " + acc + ".y = fma(" + m +
+                           ".x, " + x + ".y, " + acc + ".y);\n";
+    case 2:
+        fl += 4;
+        return first ? "        " + acc + " = make_double2(-" + m + ".y * " + x + ".y, " + m + ".y * " + x + ".x);\n"
+                     : "        " + acc + ".x = fma(-" + m + ".y, " + x + ".y, " + acc + ".x); " + acc + ".y = fma(" +
+                           m + ".y, " + x + ".x, " + acc + ".y);\n";
+    default:
+        fl += 8;
+        return first ? "        " + acc + " = cmul(" + m + ", " + x + ");\n"
+                     : "        " + acc + " = cfma(" + m + ", " + x + ", " + acc + ");\n";
+    }
+}
+
+// v[idx[r]] <- sum_s M[r + s D] v[idx[s]] for one group; M entry k is the
+// expression mat(k) of class cls(k)
+template <typename MatF, typename ClsF>
+std::string mv_code(const std::string &v, const int *idx, int D, MatF mat, ClsF cls, double &fl) {
+    std::string e = "      {\n";
+    for (int s = 0; s < D; ++s)
+        e += "        const double2 x" + std::to_string(s) + " = " + v + "[" + std::to_string(idx[s]) + "];\n";
+    for (int r = 0; r < D; ++r) {
+        e += "        double2 o" + std::to_string(r) + ";\n";
+        bool first = true;
+        for (int s = 0; s < D; ++s) {
+            const int c = cls(r + s * D);
+            if (!c) continue;
+            e += cterm(mat(r + s * D), "x" + std::to_string(s), "o" + std::to_string(r), c, first, fl);
+            first = false;
+        }
+        if (first) e += "        o" + std::to_string(r) + " = make_double2(0.0, 0.0);\n";
+    }
+    for (int r = 0; r < D; ++r)
+        e += "        " + v + "[" + std::to_string(idx[r]) + "] = o" + std::to_string(r) + ";\n";
+    return e + "      }\n";
+}
+
+// acc += Re <vg | Dm | vf> over one group (dot_group with structure)
+template <typename MatF, typename ClsF>
+std::string dot_code(const std::string &acc, const int *idx, int D, MatF mat, ClsF cls, double &fl) {
+    std::string e = "      {\n        double a = 0.0;\n";
+    bool any = false;
+    for (int r = 0; r < D; ++r) {
+        std::string row;
+        bool first = true;
+        for (int s = 0; s < D; ++s) {
+            const int c = cls(r + s * D);
+            if (!c) continue;
+            row += cterm(mat(r + s * D), "vf[" + std::to_string(idx[s]) + "]", "y", c, first, fl);
+            first = false;
+        }
+        if (first) continue;
+        any = true;
+        fl += 4;
+        e += "        {\n          double2 y;\n" + row + "          a += re_cj(vg[" + std::to_string(idx[r]) +
+             "], y);\n        }\n";
+    }
+    if (!any) return "";
+    return e + "        " + acc + " += a;\n      }\n";
+}
+
+// register indices of the matrix rows of group i (Pos<NT, P0, P1>::off)
+void group_idx(int nt, int code, int i, int *idx) {
+    static const int p0[6] = {0, 0, 0, 1, 1, 2}, p1[6] = {1, 2, 3, 2, 3, 3};
+    const int P0 = nt == 1 ? code : p0[code], P1 = nt == 2 ? p1[code] : 0;
+    for (int r = 0; r < (1 << nt); ++r)
+        idx[r] = i | ((r & 1) ? 1 << P0 : 0) | ((nt > 1 && (r & 2)) ? 1 << P1 : 0);
+}
+
 // ---------------------------------------------------------------- specialisation
 // Specialised code for a wide (nt >= 3) operation of sub-stage `sub` on the
 // register state `v`: through the shared-memory tile as sum_k diag(d_k)
 // P_{x_k} (smem_op), with the mixing bits, XOR patterns and slot offsets as
 // literals. Matrices come from the shared-memory pool copy (spool).
 std::string jit_wide_op(const RParams &P, int sub, const ROp &op, const char *v, unsigned mat,
-                        unsigned long long ident, const char *slot_base) {
+                        unsigned long long ident, const char *slot_base, double *wide_fl) {
     auto I = [](long long x) { return std::to_string(x); };
     const RLayout &L = P.subs[sub].L;
     const int NT = std::min(std::max(op.nt, 1), kMaxMix), D = 1 << NT;
@@ -1149,12 +1249,20 @@ std::string jit_wide_op(const RParams &P, int sub, const ROp &op, const char *v,
     if (ident) e += "        if ((" + std::to_string(ident) + "ull >> c) & 1) continue;\n";
     e += "        const double2 *M = spool + " + I(mat) + " + c * " + I(op.nx * D) + ";\n";
     e += "        const int sb = swz(b);\n";
-    for (int r = 0; r < D; ++r) e += "        double2 o" + I(r) + " = make_double2(0.0, 0.0);\n";
-    for (int k = 0; k < op.nx; ++k) {
-        const int x = P.xpat[op.xoff + k];
-        for (int r = 0; r < D; ++r)
-            e += "        o" + I(r) + " = cfma(M[" + I(k * D + r) + "], xbuf[sb ^ " + I(sw_off[r ^ x]) + "], o" +
-                 I(r) + ");\n";
+    // per-entry structure over every selectable sub-matrix (pool_cls)
+    const int nsubm = 1 << op.nc;
+    for (int r = 0; r < D; ++r) {
+        bool first = true;
+        e += "        double2 o" + I(r) + ";\n";
+        for (int k = 0; k < op.nx; ++k) {
+            const int x = P.xpat[op.xoff + k];
+            const int c = pool_cls(P, mat + (unsigned)(k * D + r), nsubm, op.nx * D);
+            if (!c) continue;
+            e += cterm("M[" + I(k * D + r) + "]", "xbuf[sb ^ " + I(sw_off[r ^ x]) + "]", "o" + I(r), c, first,
+                       *wide_fl);
+            first = false;
+        }
+        if (first) e += "        o" + I(r) + " = make_double2(0.0, 0.0);\n";
     }
     for (int r = 0; r < D; ++r) e += "        xbuf[sb ^ " + I(sw_off[r]) + "] = o" + I(r) + ";\n";
     e += "      }\n      __syncthreads();\n";
@@ -1164,7 +1272,7 @@ std::string jit_wide_op(const RParams &P, int sub, const ROp &op, const char *v,
     return e;
 }
 
-std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *per_block);
+std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *per_block, double *flops);
 // Source of a kernel equivalent to k_regstage<false, false> on one lowered
 // stage program, with every structural quantity a literal: tile bits, layouts
 // (shared-memory slot XOR constants), register positions, condition bits,
@@ -1172,12 +1280,12 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
 // parameter block at constant offsets; sub-matrices selected by thread or
 // tile bits come from a shared-memory copy. Returns "" for programs the
 // generator does not cover (wide operations).
-std::string jit_forward_source(const RParams &P, bool *uses_spool, bool *per_block) {
+std::string jit_forward_source(const RParams &P, bool *uses_spool, bool *per_block, double *flops) {
     if constexpr (RB != 4 || TB != 7) return "";
-    else return jit_forward_source_rs16(P, uses_spool, per_block);
+    else return jit_forward_source_rs16(P, uses_spool, per_block, flops);
 }
 
-std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *per_block) {
+std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *per_block, double *flops) {
     std::string src;
     auto out = [&](const std::string &x) { src += x; };
     auto num = [](unsigned long long v) { return std::to_string(v) + "ull"; };
@@ -1210,6 +1318,7 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
     std::string body;
     auto emit = [&](const std::string &x) { body += x; };
     static const int pair_p0[6] = {0, 0, 0, 1, 1, 2}, pair_p1[6] = {1, 2, 3, 2, 3, 3};
+    double fl = 0, wfl = 0; // FP64 flops per thread (register code) / per wide-op group
     for (int sub = 0; sub < P.nsubs; ++sub) {
         const RSub &sb = P.subs[sub];
         if (sub > 0) {
@@ -1227,7 +1336,9 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
             const ROp &op = P.ops[sb.op_begin + k];
             if (op.nt >= 3) {
                 spool = true;
-                emit(jit_wide_op(P, sub, op, "v", op.mat, op.ident, ("st" + std::to_string(sub)).c_str()));
+                double w = 0;
+                emit(jit_wide_op(P, sub, op, "v", op.mat, op.ident, ("st" + std::to_string(sub)).c_str(), &w));
+                wfl += w * (TS >> std::min(std::max(op.nt, 1), kMaxMix)); // per tile
                 continue;
             }
             const int dd = 1 << (2 * op.nt);
@@ -1255,22 +1366,29 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
                 mask = (1 << pair_p0[op.code]) | (1 << pair_p1[op.code]);
             }
             const std::string ident = num(op.ident);
+            // register-condition bits are fixed per group; the others select
+            // the sub-matrix at run time (class = union over those)
+            int rmask = 0;
+            for (int q = 0; q < op.nc; ++q)
+                if (op.ck[q] == 2) rmask |= 1 << q;
+            auto ecls = [&](unsigned off, int cs, int k) {
+                int c = 0;
+                for (int cc = 0; cc < (1 << op.nc); ++cc)
+                    if ((cc & rmask) == cs) c |= pool_cls(P, off + (unsigned)(cc * dd + k), 1, 0);
+                return c;
+            };
+            const int D = 1 << op.nt;
             if (dyn.empty()) {
-                if (op.nt > 0 && op.nc == 0) {
-                    if (!(op.ident & 1))
-                        emit("    mv_all<" + tmpl + ">(v, " + MP + " + " + std::to_string(op.mat) + ");\n");
-                    continue;
-                }
                 for (int i = 0; i < R; ++i) {
                     if (i & mask) continue;
                     const int c = cstat(i);
                     if ((op.ident >> c) & 1) continue;
-                    if (op.nt == 0)
-                        emit("    v[" + std::to_string(i) + "] = cmul(" + MP + "[" + std::to_string(op.mat + c) +
-                             "], v[" + std::to_string(i) + "]);\n");
-                    else
-                        emit("    mv_group<" + tmpl + ">(v, " + std::to_string(i) + ", " + MP + " + " +
-                             std::to_string(op.mat + c * dd) + ");\n");
+                    int idx[4];
+                    group_idx(op.nt, op.code, i, idx);
+                    const unsigned base_off = op.mat + (unsigned)(c * dd);
+                    emit(mv_code(
+                        "v", idx, D, [&](int k) { return MP + "[" + std::to_string(base_off + (unsigned)k) + "]"; },
+                        [&](int k) { return pool_cls(P, base_off + (unsigned)k, 1, 0); }, fl));
                 }
                 continue;
             }
@@ -1278,14 +1396,16 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
             emit("    {\n      const int cd = 0" + dyn + ";\n");
             for (int i = 0; i < R; ++i) {
                 if (i & mask) continue;
-                const std::string c = "(cd | " + std::to_string(cstat(i)) + ")";
-                const std::string guard = "if (!((" + ident + " >> " + c + ") & 1)) ";
-                if (op.nt == 0)
-                    emit("      " + guard + "v[" + std::to_string(i) + "] = cmul(spool[" +
-                         std::to_string(op.mat) + " + " + c + "], v[" + std::to_string(i) + "]);\n");
-                else
-                    emit("      " + guard + "mv_group<" + tmpl + ">(v, " + std::to_string(i) + ", spool + " +
-                         std::to_string(op.mat) + " + " + c + " * " + std::to_string(dd) + ");\n");
+                const int cs = cstat(i);
+                const std::string c = "(cd | " + std::to_string(cs) + ")";
+                int idx[4];
+                group_idx(op.nt, op.code, i, idx);
+                emit("      if (!((" + ident + " >> " + c + ") & 1)) {\n        const double2 *M = spool + " +
+                     std::to_string(op.mat) + " + " + c + " * " + std::to_string(dd) + ";\n");
+                emit(mv_code(
+                    "v", idx, D, [&](int k) { return "M[" + std::to_string(k) + "]"; },
+                    [&](int k) { return ecls(op.mat, cs, k); }, fl));
+                emit("      }\n");
             }
             emit("    }\n");
         }
@@ -1391,6 +1511,7 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
     out(per_block_mode ? "  }\n}\n" : "  }\n  cp_async_wait_all();\n}\n");
     if (uses_spool) *uses_spool = spool;
     if (per_block) *per_block = per_block_mode;
+    if (flops) *flops = (fl * T + wfl) / TS; // executed FP64 flops per amplitude
     return src;
 }
 
@@ -1400,7 +1521,7 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
 // each parametric step's contributions reduced per warp into shared memory and
 // written as one partial per (slot, tile) for k_slot_sums. Returns "" for
 // programs with wide operations (they stay on the interpreter).
-std::string jit_reverse_source(const RParams &P, bool *uses_spool) {
+std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops) {
     int nops_total = 0;
     for (int i = 0; i < P.nsubs; ++i)
         for (int o = 0; o < P.subs[i].op_count; ++o) {
@@ -1429,6 +1550,7 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool) {
     static const int pair_p0[6] = {0, 0, 0, 1, 1, 2}, pair_p1[6] = {1, 2, 3, 2, 3, 3};
     const int jit_blocks = env_int("VQB_JIT_REV_BLOCKS", 4);
     bool spool = false;
+    double fl = 0, wfl = 0; // FP64 flops per thread (register code) / per tile (wide ops)
     std::string body;
     auto emit = [&](const std::string &x) { body += x; };
     auto relayout = [&](const char *v, int from, int to) {
@@ -1504,9 +1626,11 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool) {
             if (op.nt >= 3) {
                 spool = true;
                 const std::string sbase = "st" + I(sub);
-                emit(jit_wide_op(P, sub, op, "vf", op.mat, op.ident, sbase.c_str()));
+                double w = 0;
+                emit(jit_wide_op(P, sub, op, "vf", op.mat, op.ident, sbase.c_str(), &w));
                 emit(jit_wide_op(P, sub, op, "vg", op.pair ? op.mat_psi : op.mat,
-                                 op.pair ? op.ident_psi : op.ident, sbase.c_str()));
+                                 op.pair ? op.ident_psi : op.ident, sbase.c_str(), &w));
+                wfl += w * (TS >> std::min(std::max(op.nt, 1), kMaxMix));
                 continue;
             }
             const int dd = 1 << (2 * op.nt), nsub = 1 << op.nc;
@@ -1534,14 +1658,27 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool) {
                 tmpl = "2, " + I(pair_p0[op.code]) + ", " + I(pair_p1[op.code]) + ", " + I(R);
                 mask = (1 << pair_p0[op.code]) | (1 << pair_p1[op.code]);
             }
-            // matrix expression for sub-matrix index expression c at base offset off
-            auto mat = [&](unsigned off, const std::string &c, int cs, int stride) {
-                if (dynamic) return "spool + " + I(off) + " + (" + c + ") * " + I(stride);
-                return "P.pool + " + I(off + (unsigned)(cs * stride));
+            int rmask = 0;
+            for (int q = 0; q < op.nc; ++q)
+                if (op.ck[q] == 2) rmask |= 1 << q;
+            const int D = 1 << op.nt;
+            // entry k of the sub-matrix selected by (cd | cs) of the matrix
+            // array at `off` (sub-matrix stride dd): expression and class (the
+            // union over the run-time selectable sub-matrices)
+            auto mexpr = [&](unsigned off, int cs) {
+                return [=](int k) {
+                    if (dynamic) return "spool[" + I(off) + " + (cd | " + I(cs) + ") * " + I(dd) + " + " + I(k) + "]";
+                    return "P.pool[" + I(off + (unsigned)(cs * dd + k)) + "]";
+                };
             };
-            auto elem = [&](unsigned off, const std::string &c, int cs) {
-                if (dynamic) return "spool[" + I(off) + " + (" + c + ")]";
-                return "P.pool[" + I(off + (unsigned)cs) + "]";
+            auto mcls = [&](unsigned off, int cs) {
+                return [=, &P](int k) {
+                    int c = 0;
+                    for (int cc = 0; cc < nsub; ++cc)
+                        if (dynamic ? (cc & rmask) == cs : cc == cs)
+                            c |= pool_cls(P, off + (unsigned)(cc * dd + k), 1, 0);
+                    return c;
+                };
             };
             if (dynamic) emit("    {\n      const int cd = 0" + dyn + ";\n");
             else emit("    {\n");
@@ -1555,16 +1692,11 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool) {
                     for (int i = 0; i < R; ++i) {
                         if (i & mask) continue;
                         const int cs = cstat(i);
-                        const std::string c = dynamic ? "(cd | " + I(cs) + ")" : I(cs);
-                        std::string guard;
-                        if (dynamic) guard = "if (!((" + num(id) + " >> " + c + ") & 1)) ";
-                        else if ((id >> cs) & 1) continue;
-                        if (op.nt == 0)
-                            emit("      " + guard + v + "[" + I(i) + "] = cmul(" + elem(m, c, cs) + ", " + v +
-                                 "[" + I(i) + "]);\n");
-                        else
-                            emit("      " + guard + "mv_group<" + tmpl + ">(" + v + ", " + I(i) + ", " +
-                                 mat(m, c, cs, dd) + ");\n");
+                        int idx[4];
+                        group_idx(op.nt, op.code, i, idx);
+                        if (!dynamic && ((id >> cs) & 1)) continue;
+                        if (dynamic) emit("      if (!((" + num(id) + " >> (cd | " + I(cs) + ")) & 1))\n");
+                        emit(mv_code(v, idx, D, mexpr(m, cs), mcls(m, cs), fl));
                     }
                 }
             } else {
@@ -1574,22 +1706,14 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool) {
                 for (int i = 0; i < R; ++i) {
                     if (i & mask) continue;
                     const int cs = cstat(i);
-                    const std::string c = dynamic ? "(cd | " + I(cs) + ")" : I(cs);
-                    if (op.nt == 0) {
-                        emit("      {\n        const double2 w = cmul(" + elem(op.mat, c, cs) + ", vf[" + I(i) +
-                             "]);\n        vf[" + I(i) + "] = w;\n");
-                        for (int p = 0; p < op.np; ++p)
-                            emit("        acc_s" + I(op.slot + p) + " += re_cj(vg[" + I(i) + "], cmul(" +
-                                 elem(op.mat_d + (unsigned)(p * nsub), c, cs) + ", w));\n");
-                        emit("        vg[" + I(i) + "] = cmul(" + elem(op.mat, c, cs) + ", vg[" + I(i) +
-                             "]);\n      }\n");
-                    } else {
-                        emit("      mv_group<" + tmpl + ">(vf, " + I(i) + ", " + mat(op.mat, c, cs, dd) + ");\n");
-                        for (int p = 0; p < op.np; ++p)
-                            emit("      acc_s" + I(op.slot + p) + " += dot_group<" + tmpl + ">(vf, vg, " + I(i) + ", " +
-                                 mat(op.mat_d + (unsigned)(p * nsub * dd), c, cs, dd) + ");\n");
-                        emit("      mv_group<" + tmpl + ">(vg, " + I(i) + ", " + mat(op.mat, c, cs, dd) + ");\n");
+                    int idx[4];
+                    group_idx(op.nt, op.code, i, idx);
+                    emit(mv_code("vf", idx, D, mexpr(op.mat, cs), mcls(op.mat, cs), fl));
+                    for (int p = 0; p < op.np; ++p) {
+                        const unsigned dof = op.mat_d + (unsigned)(p * nsub * dd);
+                        emit(dot_code("acc_s" + I(op.slot + p), idx, D, mexpr(dof, cs), mcls(dof, cs), fl));
                     }
+                    emit(mv_code("vg", idx, D, mexpr(op.mat, cs), mcls(op.mat, cs), fl));
                 }
             }
             emit("    }\n");
@@ -1669,6 +1793,7 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool) {
     }
     out("}\n");
     if (uses_spool) *uses_spool = spool;
+    if (flops) *flops = (fl * T + wfl) / TS; // executed FP64 flops per amplitude (both states)
     return src;
 }
 
@@ -1678,6 +1803,7 @@ struct JitShape {
     std::string key;
     jit::Kernel k;
     bool spool = false, per_block = false;
+    double flops_per_amp = 0; // executed FP64 flops (structure-aware code)
 };
 uint64_t fnv1a(const std::string &s) {
     // word-wise FNV-1a variant (the key is a few KB per launch)
@@ -1707,6 +1833,14 @@ std::string shape_key(const RParams &P, bool rev) {
     add(&P.ntab, 3 * sizeof(int)); // ntab, nxpat, npool
     add(P.xpat, (size_t)P.nxpat);
     add(P.fast, sizeof(int) * (size_t)nops);
+    // per-entry structure of the matrices (zero / real / imaginary / complex,
+    // pool_cls): the generated code depends on it, the values themselves not
+    {
+        std::string cls((size_t)(P.npool + 3) / 4, '\0');
+        for (int i = 0; i < P.npool; ++i)
+            cls[(size_t)i >> 2] = (char)(cls[(size_t)i >> 2] | (pool_cls(P, (unsigned)i, 1, 0) << (2 * (i & 3))));
+        key += cls;
+    }
     for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN"}) {
         const char *v = std::getenv(e);
         key += '|';
@@ -1773,6 +1907,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
         const JitShape *jit = nullptr;
         std::string key;
         uint64_t hash = 0;
+        double dense_flops_per_amp = 0; // interpreter: dense matrices
     };
     // adjoint specialisation: per-(slot, tile) partials, summed per launch
     static thread_local DevMem m_jpartial, m_slotsum;
@@ -1791,6 +1926,8 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             return;
         }
         RParams &P = *act.P;
+        note_flops((act.jit && act.jit->k.e ? act.jit->flops_per_amp : act.dense_flops_per_amp) *
+                   double(1ull << pn));
         const ProfMark pf_ = prof_begin(st);
         if (act.jit && act.jit->k.e && REV) {
             const JitShape &sh = *act.jit;
@@ -1891,7 +2028,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
                     const double mv = o.nt == 0 ? 6.0 : 8.0 * (1 << o.nt);
                     per_amp += (REV ? 2.0 : 1.0) * mv + (REV ? o.np * (mv + 2.0) : 0.0);
                 }
-                note_flops(per_amp * double(1ull << pn));
+                act.dense_flops_per_amp = per_amp;
             }
             for (int i = 0; i < P.nsubs; ++i)
                 for (int o = 0; o < P.subs[i].op_count; ++o)
@@ -1905,6 +2042,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
         std::vector<std::string> srcs;
         std::vector<size_t> which;
         std::vector<std::pair<bool, bool>> flags;
+        std::vector<double> fpas;
         std::unordered_map<uint64_t, size_t> first;
         for (size_t i = 0; i < pending.size(); ++i) {
             Action &act = pending[i];
@@ -1912,7 +2050,8 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             if ((act.jit = find_shape(act.key, act.hash))) continue;
             if (first.count(act.hash)) continue;
             bool sp = false, pb = REV;
-            std::string src = REV ? jit_reverse_source(*act.P, &sp) : jit_forward_source(*act.P, &sp, &pb);
+            double fpa = 0;
+            std::string src = REV ? jit_reverse_source(*act.P, &sp, &fpa) : jit_forward_source(*act.P, &sp, &pb, &fpa);
             if (src.empty()) {
                 // not specialisable: remember that (no kernel), stay on the interpreter
                 std::lock_guard<std::mutex> lk(g_shape_mu);
@@ -1922,6 +2061,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             first[act.hash] = i;
             srcs.push_back(std::move(src));
             flags.emplace_back(sp, pb);
+            fpas.push_back(fpa);
             which.push_back(i);
         }
         if (!srcs.empty()) {
@@ -1934,6 +2074,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
                 sh.k = ks[k];
                 sh.spool = flags[k].first;
                 sh.per_block = flags[k].second;
+                sh.flops_per_amp = fpas[k];
             }
         }
         for (Action &act : pending) {

@@ -17,6 +17,9 @@
     } while (0)
 
 constexpr int kChains = 8;
+#ifndef MIXR
+#define MIXR 4
+#endif
 
 __global__ void k_dfma(double *out, int iters, double a, double b) {
     double x[kChains];
@@ -52,6 +55,37 @@ __global__ void k_dmma(double *out, int iters, double a) {
     if (s == 1234.5) out[0] = s;
 }
 
+// both pipes at once: each warp interleaves DMMA chains with DFMA chains, to
+// learn whether the FP64 tensor path and the DFMA pipe issue concurrently
+__global__ void k_mixed(double *out, int iters, double a, double b) {
+    const int lane = threadIdx.x & 31;
+    double av = a + lane * 1e-3, bv = a - lane * 1e-3;
+    double d[4][2];
+    double x[kChains];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) d[c][0] = d[c][1] = c;
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) x[c] = threadIdx.x * 1e-9 + c;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, "
+                         "{%0,%1};\n"
+                         : "+d"(d[c][0]), "+d"(d[c][1])
+                         : "d"(av), "d"(bv));
+#pragma unroll
+        for (int r = 0; r < MIXR; ++r)
+#pragma unroll
+            for (int c = 0; c < kChains; ++c) x[c] = fma(x[c], a, b);
+    }
+    double s = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) s += d[c][0] + d[c][1];
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) s += x[c];
+    if (s == 1234.5) out[0] = s;
+}
+
 int main() {
     int dev = 0, nsm = 0, clk = 0;
     CK(cudaGetDevice(&dev));
@@ -82,8 +116,22 @@ int main() {
             2.0 * 256 * kChains * (iters / 4) * double(blocks) * (threads / 32) / (ms * 1e-3) / 1e12;
         if (rep > 0 && f2 > best_dmma) best_dmma = f2;
     }
+    double best_mixed = 0;
+    for (int rep = 0; rep < 6; ++rep) {
+        float ms;
+        const int it = iters / 8;
+        CK(cudaEventRecord(e0));
+        k_mixed<<<blocks, threads>>>(out, it, 0.999999, 1e-7);
+        CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1));
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        // per iteration per warp: 4 DMMA (256 FMA each) + MIXR*kChains*32 DFMA
+        const double fl = 2.0 * (4.0 * 256 + MIXR * kChains * 32.0) * it * double(blocks) * (threads / 32);
+        const double f3 = fl / (ms * 1e-3) / 1e12;
+        if (rep > 0 && f3 > best_mixed) best_mixed = f3;
+    }
     CK(cudaGetLastError());
-    std::printf("{\"dfma_tflops\": %.3f, \"dmma_tflops\": %.3f, \"sms\": %d, \"clock_mhz\": %d}\n",
-                best_dfma, best_dmma, nsm, clk / 1000);
+    std::printf("{\"dfma_tflops\": %.3f, \"dmma_tflops\": %.3f, \"mixed_tflops\": %.3f, \"mixr\": %d, \"sms\": %d, \"clock_mhz\": %d}\n",
+                best_dfma, best_dmma, best_mixed, MIXR, nsm, clk / 1000);
     return 0;
 }
