@@ -119,32 +119,77 @@ class Workload:
 
 # ------------------------------------------------------------------ clocks sampler
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clocks and clock-event (throttle) reasons sampled through NVML every
+    10 ms while the timed region runs (plus one sample at entry and exit, so
+    short regions are covered); falls back to `nvidia-smi -lms 200`."""
+    NAMES = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+             "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+             "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+             "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
 
     def __init__(self, gpu: int):
         self.gpu = gpu
+        self.samples = []  # (sm_mhz, sm_max_mhz, set of reasons)
+        self.stop = threading.Event()
+        self.nv = None
         self.proc = None
-        self.lines = []
+
+    def _sample(self):
+        nv = self.nv
+        sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        reasons = {k for k, attr in self.NAMES.items() if r & getattr(nv, attr, 0)}
+        self.samples.append((float(sm), float(mx), reasons))
+
+    def _poll(self):
+        while not self.stop.wait(0.01):
+            try:
+                self._sample()
+            except Exception:
+                return
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            self._sample()
+            self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.nv = None
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.gpu),
+                     "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                     "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                     "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.t = threading.Thread(target=self._read_smi, daemon=True)
+                self.t.start()
+            except Exception:
+                self.proc = None
         return self
 
-    def _read(self):
+    def _read_smi(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            parts = [p.strip() for p in line.split(",")]
+            try:
+                reasons = {k for k, v in zip(self.NAMES, parts[2:6]) if v.lower().startswith("active")}
+                self.samples.append((float(parts[0]), float(parts[1]), reasons))
+            except (ValueError, IndexError):
+                pass
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.nv is not None:
+            self.t.join(timeout=1)
+            try:
+                self._sample()
+            except Exception:
+                pass
         if self.proc:
             self.proc.terminate()
             try:
@@ -153,24 +198,14 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                smax.append(float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        if not sm:
+        if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax),
-                "reasons": sorted(reasons), "samples": len(sm)}
+        reasons = set()
+        for _, _, r in self.samples:
+            reasons |= r
+        return {"sm_mhz": statistics.median(x[0] for x in self.samples),
+                "sm_max_mhz": max(x[1] for x in self.samples), "reasons": sorted(reasons),
+                "samples": len(self.samples), "source": "nvml" if self.nv is not None else "nvidia-smi"}
 
 
 # ------------------------------------------------------------------ distributed plumbing
@@ -520,6 +555,38 @@ def main():
                "ms_per_step": ems / args.steps,
                "path": "vqb_state_set_zero -> vqb_apply_circuit (ops packed from host objects) -> vqb_norm "
                        "(the 128 GiB state does not round-trip through host memory)"}
+    elif not args.no_e2e and wl.kind == "apply":
+        # the user call: vqb_apply_circuit_copy_batch over host states (one job
+        # per step: upload the input state from pinned memory, run the circuit,
+        # download the final state into pinned memory); consecutive jobs'
+        # copies overlap the circuits (both PCIe directions + compute)
+        nbytes = 16 * state.size
+        h_in = torch.zeros(2 * state.size, dtype=torch.float64, pin_memory=True)
+        h_in[0] = 1.0
+        h_outs = [torch.empty(2 * state.size, dtype=torch.float64, pin_memory=True) for _ in range(3)]
+        # at least 16 jobs, so the pipeline's fill (first upload) and drain
+        # (last download) do not dominate
+        jobs = max(args.steps, 16)
+        ins = [h_in.data_ptr()] * jobs
+        outs = [h_outs[j % 3].data_ptr() for j in range(jobs)]
+        eng.apply_circuit_copy_batch(wl.w.circuit, wl.n, ins[:2], outs[:2], mixed=wl.mixed)  # warm
+        torch.cuda.synchronize()
+        barrier(dist, local)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        eng.apply_circuit_copy_batch(wl.w.circuit, wl.n, ins, outs, mixed=wl.mixed)
+        e1.record(stream)
+        e1.synchronize()
+        ems = max_over_ranks(dist, e0.elapsed_time(e1))
+        out_norm = float((torch.view_as_complex(h_outs[(jobs - 1) % 3].view(-1, 2)).abs() ** 2).sum())
+        e2e = {"value": world * wl.units_per_step * jobs / (ems / 1e3), "unit": wl.unit,
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+               "ms_per_step": ems / jobs, "jobs": jobs,
+               "result_norm_sq": out_norm,
+               "path": "vqb_apply_circuit_copy_batch (per job: pinned host state -> device, circuit, "
+                       "device -> pinned host; jobs pipelined over 3 device states)"}
+        del h_in, h_outs
     elif not args.no_e2e:
         nbytes = 16 * state.size
         h_in = torch.zeros(2 * state.size, dtype=torch.float64, pin_memory=True)

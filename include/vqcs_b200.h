@@ -135,10 +135,18 @@ VQB_API int64_t vqb_kernel_launch_count(void);
  * the reference only wall-clocks whole calls, src/bench.cpp:76-87).
  * vqb_profile_end synchronises the device and writes one line per kernel
  * name: "<name> <launches> <total_ms>\n" (truncated to `cap` bytes). */
-/* Algorithmic FP64 flops issued by the fused executors so far (a dense
- * complex 2^m x 2^m block costs 8 * 2^m flops per amplitude); the FP64
- * roofline numerator for benchmarks. */
+/* FP64 flops issued by the fused executors so far: the specialised kernels
+ * count the FMAs they execute (exact zeros and real/imaginary-only matrix
+ * entries are skipped); the interpreter counts a dense complex 2^m x 2^m block
+ * as 8 * 2^m flops per amplitude. The FP64 roofline numerator for benchmarks. */
 VQB_API double vqb_flop_count(void);
+/* Development aid (host only, no device work): the source of the specialised
+ * stage kernel for a lowered stage program dumped with VQB_JIT_DUMP=<dir>
+ * (`regs` = 16 or 8 amplitudes per thread, `rev` != 0 for adjoint programs).
+ * Writes the NUL-terminated source to `out` and the executed FP64 flops per
+ * amplitude to `*flops_per_amp`. */
+VQB_API int vqb_debug_jit_source(int32_t regs, const void *params, size_t nbytes, int32_t rev, char *out,
+                                 size_t cap, double *flops_per_amp);
 VQB_API int vqb_profile_begin(void);
 VQB_API int vqb_profile_end(char *buf, int64_t cap);
 
@@ -181,6 +189,15 @@ VQB_API int vqb_apply_matrix(vqb_state *st, const int32_t *positions, int32_t m,
  * are scheduled into fused shared-memory tile passes; results match the
  * reference within 1e-12 max-abs. */
 VQB_API int vqb_apply_circuit(vqb_state *st, const vqb_op *ops, int64_t count);
+/* apply_circuit_copy (circuit.hpp:132-146) over `batch` host-resident input
+ * states of 2^num_qubits amplitudes (mixed: 4^num_qubits entries, the
+ * MixedState layout): outputs[j] <- circuit(inputs[j]). Uploads, circuits and
+ * downloads of consecutive jobs overlap (three rotating device states on their
+ * own streams); use pinned host buffers for the overlap. Synchronous: returns
+ * when every output has been written. Same results as vqb_apply_circuit. */
+VQB_API int vqb_apply_circuit_copy_batch(int32_t num_qubits, int32_t mixed, const vqb_op *ops, int64_t count,
+                                         const vqb_c128 *const *inputs, vqb_c128 *const *outputs,
+                                         int64_t batch);
 /* Same, gate by gate (one kernel per element, the unfused path). */
 VQB_API int vqb_apply_circuit_unfused(vqb_state *st, const vqb_op *ops, int64_t count);
 

@@ -400,9 +400,12 @@ def bind_abi(lib: ct.CDLL, prefix: str) -> None:
         "state_device_ptr": (ct.c_int, [vp, ct.POINTER(vp)]),
         "state_set_zero": (ct.c_int, [vp]),
         "apply_circuit_unfused": (ct.c_int, [vp, op_p, i64]),
+        "apply_circuit_copy_batch": (ct.c_int, [i32, i32, op_p, i64, ct.POINTER(c128_p), ct.POINTER(c128_p), i64]),
         "build_info": (ct.c_char_p, []),
         "kernel_launch_count": (i64, []),
         "flop_count": (ct.c_double, []),
+        "debug_jit_source": (ct.c_int, [ct.c_int32, ct.c_void_p, ct.c_size_t, ct.c_int32, ct.c_char_p,
+                                        ct.c_size_t, ct.POINTER(ct.c_double)]),
         "profile_begin": (ct.c_int, []),
         "profile_end": (ct.c_int, [ct.c_char_p, i64]),
         "state_stream": (ct.c_int, [vp, ct.POINTER(vp)]),
@@ -424,11 +427,11 @@ def bind_abi(lib: ct.CDLL, prefix: str) -> None:
 
 
 ABI_FUNCTIONS = [
-    "last_error", "build_info", "kernel_launch_count", "flop_count", "profile_begin", "profile_end",
+    "last_error", "build_info", "kernel_launch_count", "flop_count", "debug_jit_source", "profile_begin", "profile_end",
     "state_stream", "state_create", "state_wrap",
     "state_destroy", "state_info", "state_device_ptr", "state_set_zero", "state_upload",
     "state_download", "state_copy", "apply_gate", "apply_channel", "apply_matrix",
-    "apply_circuit", "apply_circuit_unfused", "norm", "trace", "expectation",
+    "apply_circuit", "apply_circuit_unfused", "apply_circuit_copy_batch", "norm", "trace", "expectation",
     "apply_operator", "bilinear_form", "reverse_step", "loss_pure", "gradient_pure",
     "loss_mixed", "gradient_mixed", "gate_matrix", "gate_derivative", "gate_inverse",
     "channel_superop", "plan_blocks", "measure", "measure_probability", "collapse",

@@ -1,6 +1,7 @@
 // extern "C" boundary (include/vqcs_b200.h). Every entry point catches all
 // exceptions and returns a vqb_status; messages go to a thread-local buffer.
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "autodiff.hpp"
@@ -12,6 +13,7 @@ using namespace vqb;
 struct vqb_state : DeviceState {};
 
 namespace vqb {
+std::string debug_jit_source(int regs, const void *params, size_t nbytes, bool rev, double *flops);
 int64_t launch_count();
 double flop_count();
 void prof_start();
@@ -82,6 +84,15 @@ VQB_API const char *vqb_build_info(void) {
 VQB_API int64_t vqb_kernel_launch_count(void) { return vqb::launch_count(); }
 
 VQB_API double vqb_flop_count(void) { return vqb::flop_count(); }
+
+VQB_API int vqb_debug_jit_source(int regs, const void *params, size_t nbytes, int rev, char *out,
+                                 size_t cap, double *flops_per_amp) {
+    return guard([&] {
+        const std::string src = vqb::debug_jit_source(regs, params, nbytes, rev != 0, flops_per_amp);
+        if (src.size() + 1 > cap) raise(VQB_ERR_SIZE, "output buffer too small");
+        std::memcpy(out, src.c_str(), src.size() + 1);
+    });
+}
 
 VQB_API int vqb_profile_begin(void) {
     return guard([&] { prof_start(); });
@@ -248,6 +259,65 @@ static void apply_circuit_impl(vqb_state *s, const vqb_op *ops, int64_t count, b
 
 VQB_API int vqb_apply_circuit(vqb_state *s, const vqb_op *ops, int64_t count) {
     return guard([&] { apply_circuit_impl(s, ops, count, true); });
+}
+
+// apply_circuit_copy (circuit.hpp:132-146) over a batch of host-resident
+// input states: job j uploads inputs[j], runs the circuit and downloads the
+// result into outputs[j]. Three device states rotate through the jobs, each
+// with its own stream, so job j+1's upload and job j-1's download (the two
+// copy engines, both PCIe directions) overlap job j's circuit. Pinned host
+// buffers are needed for the overlap (pageable ones still give correct
+// results). Returns when every output has been written.
+VQB_API int vqb_apply_circuit_copy_batch(int32_t num_qubits, int32_t mixed, const vqb_op *ops, int64_t count,
+                                         const vqb_c128 *const *inputs, vqb_c128 *const *outputs,
+                                         int64_t batch) {
+    return guard([&] {
+        if (batch < 0) raise(VQB_ERR_SIZE, "apply_circuit_copy_batch: negative batch");
+        if (batch == 0) return;
+        need(inputs, "inputs");
+        need(outputs, "outputs");
+        if (count > 0) need(ops, "ops");
+        const std::vector<Element> es = build_elements(ops, count);
+        // the rotating device states are kept for the next call of the same
+        // shape (allocating and freeing 3 x 2^n amplitudes per call costs
+        // more than a job); a call of another shape releases them first
+        constexpr int kSlots = 3;
+        static std::mutex mu;
+        static std::vector<DeviceState *> cache;
+        std::lock_guard<std::mutex> lk(mu);
+        if (!cache.empty() && (cache[0]->n != num_qubits || cache[0]->mixed != (mixed ? 1 : 0))) {
+            for (DeviceState *d : cache) state_destroy(d);
+            cache.clear();
+        }
+        while ((int64_t)cache.size() < std::min<int64_t>(kSlots, batch))
+            cache.push_back(state_create(num_qubits, mixed));
+        std::vector<DeviceState *> slots(cache.begin(), cache.begin() + std::min<int64_t>(kSlots, batch));
+        DeviceState *d0 = slots[0];
+        for (const auto &e : es) {
+            if (e.channel) {
+                if (!d0->mixed)
+                    raise(VQB_ERR_TYPE,
+                          "apply_circuit: a quantum channel cannot act on a pure state; use a MixedState");
+                check_fit(e.chan.pos, e.chan.m, d0->n);
+            } else {
+                check_fit(e.gate.pos, e.gate.m, d0->n);
+            }
+        }
+        std::vector<Gate> prog;
+        if (d0->mixed) prog = mixed_forward_program(es, d0->n);
+        else
+            for (const auto &e : es) prog.push_back(e.gate);
+        const size_t bytes = sizeof(double2) * d0->size;
+        for (int64_t j = 0; j < batch; ++j) {
+            need(inputs[j], "inputs[j]");
+            need(outputs[j], "outputs[j]");
+            DeviceState *d = slots[(size_t)(j % (int64_t)slots.size())];
+            VQB_CUDA(cudaMemcpyAsync(d->amps, inputs[j], bytes, cudaMemcpyHostToDevice, d->stream));
+            run_program(d, prog, true); // enqueues on d->stream, no host synchronisation
+            VQB_CUDA(cudaMemcpyAsync(outputs[j], d->amps, bytes, cudaMemcpyDeviceToHost, d->stream));
+        }
+        for (DeviceState *d : slots) sync(d);
+    });
 }
 
 VQB_API int vqb_apply_circuit_unfused(vqb_state *s, const vqb_op *ops, int64_t count) {

@@ -768,10 +768,16 @@ void execute(DeviceState *sphi, DeviceState *spsi, const std::vector<FusedOp> &f
     void run_program_reg(DeviceState *s, const std::vector<Gate> &prog);                    \
     void run_reverse_reg(DeviceState *phi, DeviceState *psi, const std::vector<RevOp> &prog, \
                          double *dgrads);                                                   \
+    std::string debug_jit_source(const void *params, size_t nbytes, bool rev, double *flops); \
     }
 VQB_DECLARE_REGSTAGE(rs16)
 VQB_DECLARE_REGSTAGE(rs8)
 #undef VQB_DECLARE_REGSTAGE
+
+std::string debug_jit_source(int regs, const void *params, size_t nbytes, bool rev, double *flops) {
+    return regs == 8 ? rs8::debug_jit_source(params, nbytes, rev, flops)
+                     : rs16::debug_jit_source(params, nbytes, rev, flops);
+}
 
 namespace {
 // register-executor geometry: VQB_REGS / VQB_REV_REGS = 8 or 16 amplitudes per

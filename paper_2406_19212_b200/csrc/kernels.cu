@@ -577,6 +577,29 @@ void upload_operator(DeviceState *s, const PauliPack &p) {
     VQB_CUDA(cudaStreamSynchronize(s->stream)); // buf is a stack temporary
 }
 
+// Pauli tables staged once per block in shared memory: every thread reads
+// every term for every amplitude, so broadcast shared-memory reads replace
+// per-thread global loads (the operator is a few KB; larger ones stay global).
+struct PauliView {
+    const PauliGroupDev *g;
+    const PauliTermDev *t;
+};
+__device__ __forceinline__ PauliView stage_pauli(const PauliGroupDev *g, int ng, const PauliTermDev *t, int nt,
+                                                 bool staged) {
+    if (!staged) return {g, t};
+    extern __shared__ __align__(16) unsigned char pauli_sm[];
+    auto *sg = reinterpret_cast<PauliGroupDev *>(pauli_sm);
+    auto *st = reinterpret_cast<PauliTermDev *>(pauli_sm + sizeof(PauliGroupDev) * (size_t)ng);
+    for (int i = threadIdx.x; i < ng; i += blockDim.x) sg[i] = g[i];
+    for (int i = threadIdx.x; i < nt; i += blockDim.x) st[i] = t[i];
+    __syncthreads();
+    return {sg, st};
+}
+size_t pauli_smem(const PauliPack &p) {
+    const size_t b = sizeof(PauliGroupDev) * p.groups.size() + sizeof(PauliTermDev) * p.terms.size();
+    return b <= 40 * 1024 ? b : 0;
+}
+
 // Sum over a group's terms of c_t * (-1)^popc(idx & z_t).
 __device__ __forceinline__ double2 group_weight(const PauliTermDev *__restrict__ terms, int first,
                                                 int count, uint64_t idx) {
@@ -592,11 +615,14 @@ __device__ __forceinline__ double2 group_weight(const PauliTermDev *__restrict__
 
 // <psi|H|psi> = sum_g sum_b conj(psi[b^x]) psi[b] W_g(b) (observables.hpp:176-190)
 __global__ void __launch_bounds__(kThreads) k_expect_pure(const double2 *__restrict__ a, uint64_t size,
-                                                          const PauliGroupDev *__restrict__ groups,
+                                                          const PauliGroupDev *__restrict__ groups_g,
                                                           int ngroups,
-                                                          const PauliTermDev *__restrict__ terms,
+                                                          const PauliTermDev *__restrict__ terms_g, int nterms, int staged,
                                                           double2 *partials, unsigned *counter,
                                                           Epilogue ep) {
+    const PauliView pv = stage_pauli(groups_g, ngroups, terms_g, nterms, staged != 0);
+    const PauliGroupDev *groups = pv.g;
+    const PauliTermDev *terms = pv.t;
     double2 v[1] = {make_double2(0, 0)};
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < size; b += stride) {
@@ -614,11 +640,14 @@ __global__ void __launch_bounds__(kThreads) k_expect_pure(const double2 *__restr
 
 // tr(H rho) = sum_k sum_g rho[(k^x) + k*dim] W_g(k^x) (observables.hpp:194-213)
 __global__ void __launch_bounds__(kThreads) k_expect_mixed(const double2 *__restrict__ a, uint64_t dim,
-                                                           const PauliGroupDev *__restrict__ groups,
+                                                           const PauliGroupDev *__restrict__ groups_g,
                                                            int ngroups,
-                                                           const PauliTermDev *__restrict__ terms,
+                                                           const PauliTermDev *__restrict__ terms_g, int nterms, int staged,
                                                            double2 *partials, unsigned *counter,
                                                            Epilogue ep) {
+    const PauliView pv = stage_pauli(groups_g, ngroups, terms_g, nterms, staged != 0);
+    const PauliGroupDev *groups = pv.g;
+    const PauliTermDev *terms = pv.t;
     double2 v[1] = {make_double2(0, 0)};
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < dim; k += stride) {
@@ -646,13 +675,15 @@ void expectation_async(DeviceState *s, const PauliPack &p, double2 *out_dev) {
     if (s->mixed) {
         const uint64_t dim = 1ull << s->n;
         const ProfMark pf_ = prof_begin(s->stream);
-        k_expect_mixed<<<reduce_grid(dim), kThreads, 0, s->stream>>>(s->amps, dim, groups, ng, terms,
-                                                                     s->ws.partials, s->ws.counter, ep);
+        k_expect_mixed<<<reduce_grid(dim), kThreads, pauli_smem(p), s->stream>>>(
+            s->amps, dim, groups, ng, terms, (int)p.terms.size(), pauli_smem(p) > 0, s->ws.partials,
+            s->ws.counter, ep);
         check_launch("k_expect_mixed", pf_);
     } else {
         const ProfMark pf_ = prof_begin(s->stream);
-        k_expect_pure<<<reduce_grid(s->size), kThreads, 0, s->stream>>>(
-            s->amps, s->size, groups, ng, terms, s->ws.partials, s->ws.counter, ep);
+        k_expect_pure<<<reduce_grid(s->size), kThreads, pauli_smem(p), s->stream>>>(
+            s->amps, s->size, groups, ng, terms, (int)p.terms.size(), pauli_smem(p) > 0, s->ws.partials,
+            s->ws.counter, ep);
         check_launch("k_expect_pure", pf_);
     }
 }
@@ -665,9 +696,12 @@ cplx expectation(DeviceState *s, const PauliPack &p) {
 // dst[b] = sum_g psi[b^x] W_g(b^x) (apply_operator observables.hpp:216-237)
 __global__ void __launch_bounds__(kThreads) k_apply_operator(const double2 *__restrict__ a,
                                                              double2 *__restrict__ out, uint64_t size,
-                                                             const PauliGroupDev *__restrict__ groups,
+                                                             const PauliGroupDev *__restrict__ groups_g,
                                                              int ngroups,
-                                                             const PauliTermDev *__restrict__ terms) {
+                                                             const PauliTermDev *__restrict__ terms_g, int nterms, int staged) {
+    const PauliView pv = stage_pauli(groups_g, ngroups, terms_g, nterms, staged != 0);
+    const PauliGroupDev *groups = pv.g;
+    const PauliTermDev *terms = pv.t;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < size; b += stride) {
         double2 acc = make_double2(0, 0);
@@ -686,17 +720,20 @@ void apply_operator(DeviceState *src, double2 *dst, const PauliPack &p, bool) {
     auto *terms = reinterpret_cast<const PauliTermDev *>(
         reinterpret_cast<const char *>(src->ws.terms) + sizeof(PauliGroupDev) * p.groups.size());
     const ProfMark pf_ = prof_begin(src->stream);
-    k_apply_operator<<<grid_for(src->size), kThreads, 0, src->stream>>>(
-        src->amps, dst, src->size, groups, (int)p.groups.size(), terms);
+    k_apply_operator<<<grid_for(src->size), kThreads, pauli_smem(p), src->stream>>>(
+        src->amps, dst, src->size, groups, (int)p.groups.size(), terms, (int)p.terms.size(), pauli_smem(p) > 0);
     check_launch("k_apply_operator", pf_);
 }
 
 // <<I| H as a ket on vec(rho) (autodiff.hpp:241-248): entry (c^x) + c*dim gets
 // sum_t conj(coeff_t) i^{#Y} (-1)^popc(c & z_t); everything else is zero.
 __global__ void __launch_bounds__(kThreads) k_identity_costate(double2 *__restrict__ out, uint64_t dim,
-                                                               const PauliGroupDev *__restrict__ groups,
+                                                               const PauliGroupDev *__restrict__ groups_g,
                                                                int ngroups,
-                                                               const PauliTermDev *__restrict__ terms) {
+                                                               const PauliTermDev *__restrict__ terms_g, int nterms, int staged) {
+    const PauliView pv = stage_pauli(groups_g, ngroups, terms_g, nterms, staged != 0);
+    const PauliGroupDev *groups = pv.g;
+    const PauliTermDev *terms = pv.t;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < dim; c += stride)
         for (int g = 0; g < ngroups; ++g) {
@@ -713,8 +750,8 @@ void identity_costate(DeviceState *s, const PauliPack &p) {
     VQB_CUDA(cudaMemsetAsync(s->amps, 0, sizeof(double2) * s->size, s->stream));
     const uint64_t dim = 1ull << s->n;
     const ProfMark pf_ = prof_begin(s->stream);
-    k_identity_costate<<<grid_for(dim), kThreads, 0, s->stream>>>(s->amps, dim, groups,
-                                                                  (int)p.groups.size(), terms);
+    k_identity_costate<<<grid_for(dim), kThreads, pauli_smem(p), s->stream>>>(
+        s->amps, dim, groups, (int)p.groups.size(), terms, (int)p.terms.size(), pauli_smem(p) > 0);
     check_launch("k_identity_costate", pf_);
 }
 

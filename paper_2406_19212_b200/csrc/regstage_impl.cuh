@@ -43,6 +43,9 @@
 #include "jit.hpp"
 #include "plan.hpp"
 
+#define VQB_RS_STR2(x) #x
+#define VQB_RS_STR1(x) VQB_RS_STR2(x)
+#define VQB_RS_STR VQB_RS_STR1(VQB_RS_NS)
 namespace vqb {
 
 void apply_gate_fast(double2 *a, int pn, const Gate &g, cudaStream_t st);
@@ -1209,11 +1212,23 @@ void group_idx(int nt, int code, int i, int *idx) {
 // register state `v`: through the shared-memory tile as sum_k diag(d_k)
 // P_{x_k} (smem_op), with the mixing bits, XOR patterns and slot offsets as
 // literals. Matrices come from the shared-memory pool copy (spool).
-std::string jit_wide_op(const RParams &P, int sub, const ROp &op, const char *v, unsigned mat,
-                        unsigned long long ident, const char *slot_base, double *wide_fl) {
+struct WideState {
+    const char *v;   // register array
+    const char *buf; // shared-memory tile it goes through
+    unsigned mat;
+    unsigned long long ident;
+};
+// One wide operation applied to one or two register states (the adjoint's Phi
+// and Psi, each with its own matrices): the states go through their own
+// shared-memory tiles in one round trip, and the groups of all states are
+// spread over the block's threads. Matrices come from the shared-memory pool
+// copy (*needs_spool).
+std::string jit_wide_op(const RParams &P, int sub, const ROp &op, const std::vector<WideState> &sts,
+                        const char *slot_base, double *wide_fl, bool *needs_spool) {
     auto I = [](long long x) { return std::to_string(x); };
     const RLayout &L = P.subs[sub].L;
     const int NT = std::min(std::max(op.nt, 1), kMaxMix), D = 1 << NT;
+    const int G = TS >> NT, S = (int)sts.size();
     auto slot_const = [&](int i) {
         int c = 0;
         for (int b = 0; b < RB; ++b)
@@ -1230,44 +1245,61 @@ std::string jit_wide_op(const RParams &P, int sub, const ROp &op, const char *v,
             if ((r >> q) & 1) o |= 1 << op.lb[q];
         sw_off[r] = swz(o);
     }
+    // matrices from the shared-memory pool copy: the parameter bank at literal
+    // offsets was measured slower here (the pool outgrows the constant cache)
+    const bool cond = true;
+    *needs_spool = true;
     std::string e = "    {\n";
-    for (int i = 0; i < R; ++i)
-        e += std::string("      xbuf[") + slot_base + " ^ " + I(slot_const(i)) + "] = " + v + "[" + I(i) + "];\n";
+    for (const auto &st : sts)
+        for (int i = 0; i < R; ++i)
+            e += std::string("      ") + st.buf + "[" + slot_base + " ^ " + I(slot_const(i)) + "] = " + st.v + "[" +
+                 I(i) + "];\n";
     e += "      __syncthreads();\n      const int cu = 0";
     for (int q = 0; q < op.nc; ++q)
         if (op.ck[q] == 0) e += " | (int)(((base >> " + I(op.cp[q]) + ") & 1) << " + I(q) + ")";
-    e += ";\n      for (int g = threadIdx.x; g < " + I(TS >> NT) + "; g += " + I(T) + ") {\n        int b = g;\n";
-    for (int q = 0; q < NT; ++q)
-        e += "        b = ((b >> " + I(sorted[q]) + ") << " + I(sorted[q] + 1) + ") | (b & " +
-             I((1 << sorted[q]) - 1) + ");\n";
-    e += "        const int c = cu";
-    for (int q = 0; q < op.nc; ++q) {
-        const int l = op.ck[q] == 1 ? L.thr[op.cp[q]] : (op.ck[q] == 2 ? L.reg[op.cp[q]] : -1);
-        if (l >= 0) e += " | (((b >> " + I(l) + ") & 1) << " + I(q) + ")";
-    }
-    e += ";\n";
-    if (ident) e += "        if ((" + std::to_string(ident) + "ull >> c) & 1) continue;\n";
-    e += "        const double2 *M = spool + " + I(mat) + " + c * " + I(op.nx * D) + ";\n";
-    e += "        const int sb = swz(b);\n";
-    // per-entry structure over every selectable sub-matrix (pool_cls)
-    const int nsubm = 1 << op.nc;
-    for (int r = 0; r < D; ++r) {
-        bool first = true;
-        e += "        double2 o" + I(r) + ";\n";
-        for (int k = 0; k < op.nx; ++k) {
-            const int x = P.xpat[op.xoff + k];
-            const int c = pool_cls(P, mat + (unsigned)(k * D + r), nsubm, op.nx * D);
-            if (!c) continue;
-            e += cterm("M[" + I(k * D + r) + "]", "xbuf[sb ^ " + I(sw_off[r ^ x]) + "]", "o" + I(r), c, first,
-                       *wide_fl);
-            first = false;
+    e += ";\n      for (int w = threadIdx.x; w < " + I(S * G) + "; w += " + I(T) + ") {\n";
+    for (int si = 0; si < S; ++si) {
+        const WideState &st = sts[si];
+        if (S > 1) e += si == 0 ? "       if (w < " + I(G) + ") {\n        int b = w;\n"
+                                : "       } else {\n        int b = w - " + I(G) + ";\n";
+        else e += "       {\n        int b = w;\n";
+        for (int q = 0; q < NT; ++q)
+            e += "        b = ((b >> " + I(sorted[q]) + ") << " + I(sorted[q] + 1) + ") | (b & " +
+                 I((1 << sorted[q]) - 1) + ");\n";
+        e += "        const int c = cu";
+        for (int q = 0; q < op.nc; ++q) {
+            const int l = op.ck[q] == 1 ? L.thr[op.cp[q]] : (op.ck[q] == 2 ? L.reg[op.cp[q]] : -1);
+            if (l >= 0) e += " | (((b >> " + I(l) + ") & 1) << " + I(q) + ")";
         }
-        if (first) e += "        o" + I(r) + " = make_double2(0.0, 0.0);\n";
+        e += ";\n";
+        if (st.ident) e += "        if ((" + std::to_string(st.ident) + "ull >> c) & 1) continue;\n";
+        e += cond ? "        const double2 *M = spool + " + I(st.mat) + " + c * " + I(op.nx * D) + ";\n"
+                  : "        const double2 *M = P.pool + " + I(st.mat) + ";\n";
+        e += "        const int sb = swz(b);\n";
+        // per-entry structure over every selectable sub-matrix (pool_cls)
+        const int nsubm = 1 << op.nc;
+        double fl = 0;
+        for (int r = 0; r < D; ++r) {
+            bool first = true;
+            e += "        double2 o" + I(r) + ";\n";
+            for (int k = 0; k < op.nx; ++k) {
+                const int x = P.xpat[op.xoff + k];
+                const int c = pool_cls(P, st.mat + (unsigned)(k * D + r), nsubm, op.nx * D);
+                if (!c) continue;
+                e += cterm("M[" + I(k * D + r) + "]", std::string(st.buf) + "[sb ^ " + I(sw_off[r ^ x]) + "]",
+                           "o" + I(r), c, first, fl);
+                first = false;
+            }
+            if (first) e += "        o" + I(r) + " = make_double2(0.0, 0.0);\n";
+        }
+        *wide_fl += fl * G; // per tile
+        for (int r = 0; r < D; ++r) e += "        " + std::string(st.buf) + "[sb ^ " + I(sw_off[r]) + "] = o" + I(r) + ";\n";
     }
-    for (int r = 0; r < D; ++r) e += "        xbuf[sb ^ " + I(sw_off[r]) + "] = o" + I(r) + ";\n";
-    e += "      }\n      __syncthreads();\n";
-    for (int i = 0; i < R; ++i)
-        e += std::string("      ") + v + "[" + I(i) + "] = xbuf[" + slot_base + " ^ " + I(slot_const(i)) + "];\n";
+    e += "       }\n      }\n      __syncthreads();\n";
+    for (const auto &st : sts)
+        for (int i = 0; i < R; ++i)
+            e += std::string("      ") + st.v + "[" + I(i) + "] = " + st.buf + "[" + slot_base + " ^ " +
+                 I(slot_const(i)) + "];\n";
     e += "      __syncthreads();\n    }\n";
     return e;
 }
@@ -1335,10 +1367,8 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
         for (int k = 0; k < sb.op_count; ++k) {
             const ROp &op = P.ops[sb.op_begin + k];
             if (op.nt >= 3) {
-                spool = true;
-                double w = 0;
-                emit(jit_wide_op(P, sub, op, "v", op.mat, op.ident, ("st" + std::to_string(sub)).c_str(), &w));
-                wfl += w * (TS >> std::min(std::max(op.nt, 1), kMaxMix)); // per tile
+                emit(jit_wide_op(P, sub, op, {{"v", "xbuf", op.mat, op.ident}}, ("st" + std::to_string(sub)).c_str(),
+                                 &wfl, &spool));
                 continue;
             }
             const int dd = 1 << (2 * op.nt);
@@ -1521,7 +1551,7 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
 // each parametric step's contributions reduced per warp into shared memory and
 // written as one partial per (slot, tile) for k_slot_sums. Returns "" for
 // programs with wide operations (they stay on the interpreter).
-std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops) {
+std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops, int *xtiles) {
     int nops_total = 0;
     for (int i = 0; i < P.nsubs; ++i)
         for (int o = 0; o < P.subs[i].op_count; ++o) {
@@ -1549,10 +1579,25 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
     };
     static const int pair_p0[6] = {0, 0, 0, 1, 1, 2}, pair_p1[6] = {1, 2, 3, 2, 3, 3};
     const int jit_blocks = env_int("VQB_JIT_REV_BLOCKS", 4);
-    bool spool = false;
+    bool spool = false, wide2 = false;
     double fl = 0, wfl = 0; // FP64 flops per thread (register code) / per tile (wide ops)
     std::string body;
     auto emit = [&](const std::string &x) { body += x; };
+    // Gradient accumulators: a slot's per-thread sum is complete after its
+    // step; it is warp-reduced into shared memory once more than acc_budget
+    // slots are pending, so the reduction overlaps the following steps and at
+    // most acc_budget accumulators hold registers (dozens of slots per launch
+    // would otherwise spill).
+    const int acc_budget = env_int("VQB_JIT_ACC", 6);
+    std::vector<int> open_slots;
+    auto flush_slots = [&](int keep) {
+        while ((int)open_slots.size() > keep) {
+            const int sl = open_slots.front();
+            open_slots.erase(open_slots.begin());
+            emit("    { const double x = warp_sum(acc_s" + I(sl) + "); if (lane == 0) red[" + I(sl * NW) +
+                 " + warp] = x; }\n");
+        }
+    };
     auto relayout = [&](const char *v, int from, int to) {
         for (int i = 0; i < R; ++i)
             emit(std::string("    xbuf[st") + I(from) + " ^ " + I(slot_const(P.subs[from].L, i)) + "] = " + v +
@@ -1578,7 +1623,7 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
             while (run_end < sb.op_count && P.ops[sb.op_begin + run_end].nt == 0 &&
                    P.ops[sb.op_begin + run_end].unit && !P.ops[sb.op_begin + run_end].pair)
                 ++run_end;
-            if (run_end - k >= 2 && env_int("VQB_JIT_DIAGRUN", 0)) {
+            if (run_end - k >= 2 && env_int("VQB_JIT_DIAGRUN", 1)) {
                 emit("    {\n");
                 for (int j = k; j < run_end; ++j) {
                     const ROp &oj = P.ops[sb.op_begin + j];
@@ -1620,17 +1665,25 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
                          "] = cmul(ph, vg[" + I(i) + "]);\n      }\n");
                 }
                 emit("    }\n");
+                for (int j = k; j < run_end; ++j)
+                    for (int p = 0; p < P.ops[sb.op_begin + j].np; ++p)
+                        open_slots.push_back(P.ops[sb.op_begin + j].slot + p);
+                flush_slots(acc_budget);
                 k = run_end - 1;
                 continue;
             }
             if (op.nt >= 3) {
-                spool = true;
                 const std::string sbase = "st" + I(sub);
-                double w = 0;
-                emit(jit_wide_op(P, sub, op, "vf", op.mat, op.ident, sbase.c_str(), &w));
-                emit(jit_wide_op(P, sub, op, "vg", op.pair ? op.mat_psi : op.mat,
-                                 op.pair ? op.ident_psi : op.ident, sbase.c_str(), &w));
-                wfl += w * (TS >> std::min(std::max(op.nt, 1), kMaxMix));
+                const WideState wf{"vf", "xbuf", op.mat, op.ident};
+                const WideState wg{"vg", env_int("VQB_JIT_WIDE2", 1) ? "xbuf2" : "xbuf",
+                                   op.pair ? op.mat_psi : op.mat, op.pair ? op.ident_psi : op.ident};
+                if (env_int("VQB_JIT_WIDE2", 1)) {
+                    wide2 = true;
+                    emit(jit_wide_op(P, sub, op, {wf, wg}, sbase.c_str(), &wfl, &spool));
+                } else {
+                    emit(jit_wide_op(P, sub, op, {wf}, sbase.c_str(), &wfl, &spool));
+                    emit(jit_wide_op(P, sub, op, {wg}, sbase.c_str(), &wfl, &spool));
+                }
                 continue;
             }
             const int dd = 1 << (2 * op.nt), nsub = 1 << op.nc;
@@ -1715,10 +1768,13 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
                     }
                     emit(mv_code("vg", idx, D, mexpr(op.mat, cs), mcls(op.mat, cs), fl));
                 }
+                for (int p = 0; p < op.np; ++p) open_slots.push_back(op.slot + p);
             }
             emit("    }\n");
+            flush_slots(acc_budget);
         }
     }
+    flush_slots(0);
     const RLayout &Lf = P.subs[P.nsubs - 1].L;
     std::string src;
     auto out = [&](const std::string &x) { src += x; };
@@ -1727,11 +1783,15 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
     out("extern \"C\" __global__ void __launch_bounds__(" + I(T) + ", " + I(jit_blocks) + ")\n"
         "vqb_rev(double2 *__restrict__ a, double2 *__restrict__ b2, double *__restrict__ partial,\n"
         "        const __grid_constant__ JP P) {\n");
+    // shared memory: xbuf (relayouts, Phi's wide ops) [| xbuf2 (Psi's wide
+    // ops)] [| pool copy] | gradient reduction slots
+    const int xt = wide2 ? 2 : 1;
     out("  extern __shared__ __align__(16) double2 sm[];\n  double2 *xbuf = sm;\n");
-    const int red_at = TS + (spool ? P.npool : 0);
+    if (wide2) out("  double2 *xbuf2 = sm + " + I(TS) + ";\n");
+    const int red_at = xt * TS + (spool ? P.npool : 0);
     if (spool)
-        out("  double2 *spool = sm + " + I(TS) + ";\n  for (int i = threadIdx.x; i < " + I(P.npool) + "; i += " +
-            I(T) + ") spool[i] = P.pool[i];\n");
+        out("  double2 *spool = sm + " + I(xt * TS) + ";\n  for (int i = threadIdx.x; i < " + I(P.npool) +
+            "; i += " + I(T) + ") spool[i] = P.pool[i];\n");
     out("  double *red = reinterpret_cast<double *>(sm + " + I(red_at) + ");\n");
     out("  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;\n");
     for (int sl = 0; sl < P.nslots; ++sl) out("  double acc_s" + I(sl) + " = 0;\n");
@@ -1780,12 +1840,7 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
             "];\n");
     }
     if (P.nslots > 0) {
-        for (int sl = 0; sl < P.nslots; ++sl)
-            out("  acc_s" + I(sl) + " = warp_sum(acc_s" + I(sl) + ");\n");
-        out("  if (lane == 0) {\n");
-        for (int sl = 0; sl < P.nslots; ++sl)
-            out("    red[" + I(sl * NW) + " + warp] = acc_s" + I(sl) + ";\n");
-        out("  }\n");
+        // every slot was reduced into red[] by flush_slots
         out("  __syncthreads();\n");
         out("  for (int s = t; s < " + I(P.nslots) + "; s += " + I(T) + ") {\n    double x = 0;\n");
         for (int w = 0; w < NW; ++w) out("    x += red[s * " + I(NW) + " + " + I(w) + "];\n");
@@ -1794,6 +1849,7 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
     out("}\n");
     if (uses_spool) *uses_spool = spool;
     if (flops) *flops = (fl * T + wfl) / TS; // executed FP64 flops per amplitude (both states)
+    if (xtiles) *xtiles = xt;
     return src;
 }
 
@@ -1804,6 +1860,7 @@ struct JitShape {
     jit::Kernel k;
     bool spool = false, per_block = false;
     double flops_per_amp = 0; // executed FP64 flops (structure-aware code)
+    int xtiles = 1;           // adjoint: shared-memory tiles (2 with wide operations)
 };
 uint64_t fnv1a(const std::string &s) {
     // word-wise FNV-1a variant (the key is a few KB per launch)
@@ -1841,7 +1898,7 @@ std::string shape_key(const RParams &P, bool rev) {
             cls[(size_t)i >> 2] = (char)(cls[(size_t)i >> 2] | (pool_cls(P, (unsigned)i, 1, 0) << (2 * (i & 3))));
         key += cls;
     }
-    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN"}) {
+    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2"}) {
         const char *v = std::getenv(e);
         key += '|';
         if (v) key += v;
@@ -1931,7 +1988,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
         const ProfMark pf_ = prof_begin(st);
         if (act.jit && act.jit->k.e && REV) {
             const JitShape &sh = *act.jit;
-            const size_t sm = (size_t)(TS + (sh.spool ? P.npool : 0)) * sizeof(double2) +
+            const size_t sm = (size_t)(sh.xtiles * TS + (sh.spool ? P.npool : 0)) * sizeof(double2) +
                               sizeof(double) * (size_t)P.nslots * NW;
             void *a0 = sphi->amps, *a1 = spsi->amps, *pp = m_jpartial.p;
             void *args[4] = {&a0, &a1, &pp, P.pool};
@@ -2043,6 +2100,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
         std::vector<size_t> which;
         std::vector<std::pair<bool, bool>> flags;
         std::vector<double> fpas;
+        std::vector<int> xts;
         std::unordered_map<uint64_t, size_t> first;
         for (size_t i = 0; i < pending.size(); ++i) {
             Action &act = pending[i];
@@ -2051,7 +2109,8 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             if (first.count(act.hash)) continue;
             bool sp = false, pb = REV;
             double fpa = 0;
-            std::string src = REV ? jit_reverse_source(*act.P, &sp, &fpa) : jit_forward_source(*act.P, &sp, &pb, &fpa);
+            int xt = 1;
+            std::string src = REV ? jit_reverse_source(*act.P, &sp, &fpa, &xt) : jit_forward_source(*act.P, &sp, &pb, &fpa);
             if (src.empty()) {
                 // not specialisable: remember that (no kernel), stay on the interpreter
                 std::lock_guard<std::mutex> lk(g_shape_mu);
@@ -2059,9 +2118,25 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
                 continue;
             }
             first[act.hash] = i;
+            if (const char *dump = std::getenv("VQB_JIT_DUMP")) {
+                // development aid: the lowered program (regenerate the source on
+                // the host with vqb_debug_jit_source) and the source itself
+                char name[512];
+                std::snprintf(name, sizeof name, "%s/%s_%s_%016llx", dump, REV ? "R" : "F", VQB_RS_STR,
+                              (unsigned long long)act.hash);
+                if (FILE *f = std::fopen((std::string(name) + ".params").c_str(), "wb")) {
+                    std::fwrite(act.P.get(), sizeof(RParams), 1, f);
+                    std::fclose(f);
+                }
+                if (FILE *f = std::fopen((std::string(name) + ".cu").c_str(), "w")) {
+                    std::fwrite(src.data(), 1, src.size(), f);
+                    std::fclose(f);
+                }
+            }
             srcs.push_back(std::move(src));
             flags.emplace_back(sp, pb);
             fpas.push_back(fpa);
+            xts.push_back(xt);
             which.push_back(i);
         }
         if (!srcs.empty()) {
@@ -2075,6 +2150,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
                 sh.spool = flags[k].first;
                 sh.per_block = flags[k].second;
                 sh.flops_per_amp = fpas[k];
+                sh.xtiles = xts[k];
             }
         }
         for (Action &act : pending) {
@@ -2107,6 +2183,15 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
 } // namespace
 
 bool regstage_available(int pn) { return pn >= K + 2; }
+
+// Host-only: the specialised source for a dumped lowered program (VQB_JIT_DUMP).
+std::string debug_jit_source(const void *params, size_t nbytes, bool rev, double *flops) {
+    if (nbytes != sizeof(RParams)) raise(VQB_ERR_SIZE, "params blob size mismatch");
+    auto P = std::make_unique<RParams>();
+    std::memcpy(P.get(), params, sizeof(RParams));
+    bool sp = false, pb = false;
+    return rev ? jit_reverse_source(*P, &sp, flops, nullptr) : jit_forward_source(*P, &sp, &pb, flops);
+}
 
 void run_program_reg(DeviceState *s, const std::vector<Gate> &prog) {
     std::vector<FusedOp> fops;

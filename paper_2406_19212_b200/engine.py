@@ -155,6 +155,28 @@ class Engine:
             else "apply_circuit_unfused"
         self.check(self._fn(name)(s.handle, p.arr, p.count))
 
+    def apply_circuit_copy_batch(self, c: Circuit, n: int, inputs, outputs, mixed: bool = False) -> None:
+        """apply_circuit_copy (circuit.hpp:132-146) over host states:
+        outputs[j] <- c(inputs[j]); inputs/outputs are complex128 numpy arrays
+        or raw host addresses (ints, e.g. pinned torch tensors' data_ptr())."""
+        p = c.pack() if isinstance(c, Circuit) else pack_ops(c)
+        keep = []
+
+        def ptr(x, writable):
+            if isinstance(x, int):
+                return ct.cast(ct.c_void_p(x), c128_p)
+            a = np.asarray(x)
+            if a.dtype != np.complex128 or not a.flags.c_contiguous or (writable and not a.flags.writeable):
+                raise ValueError("apply_circuit_copy_batch: complex128 C-contiguous arrays required")
+            keep.append(a)
+            return a.ctypes.data_as(c128_p)
+        nb = len(inputs)
+        if len(outputs) != nb:
+            raise ValueError("apply_circuit_copy_batch: inputs and outputs differ in length")
+        ins = (c128_p * max(nb, 1))(*[ptr(x, False) for x in inputs])
+        outs = (c128_p * max(nb, 1))(*[ptr(x, True) for x in outputs])
+        self.check(self._fn("apply_circuit_copy_batch")(n, 1 if mixed else 0, p.arr, p.count, ins, outs, nb))
+
     # ---- reductions ----
     def norm(self, s: State) -> float:
         v = ct.c_double()

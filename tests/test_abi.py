@@ -45,10 +45,10 @@ def test_library_exports_every_declared_symbol():
 def test_oracles_implement_the_same_entry_points():
     core = [n[len("vqb_"):] for n in declared()
             if n[len("vqb_"):] in set(abi.ABI_FUNCTIONS) - {
-                "build_info", "kernel_launch_count", "flop_count", "profile_begin", "profile_end",
+                "build_info", "kernel_launch_count", "flop_count", "debug_jit_source", "profile_begin", "profile_end",
                 "state_stream",
                 "state_wrap", "state_device_ptr", "state_set_zero", "apply_circuit_unfused",
-                "plan_blocks"}]
+                "apply_circuit_copy_batch", "plan_blocks"}]
     libs = [("vqcsorc_", ct.CDLL(oracle.ORC_SO), set())]
     if oracle.reference_available():
         # the reference draws measurement outcomes from a std::mt19937_64 it is

@@ -293,3 +293,26 @@ def test_fused_planner_variants(dev, ref, monkeypatch, tile_bits, fuse):
     rloss, rg = ref.gradient_mixed(w.observable, w.circuit, ref.mixed_state(4))
     assert abs(loss - rloss) <= 1e-10 * abs(rloss)
     assert np.max(np.abs(g - rg)) <= 1e-10 * np.max(np.abs(rg))
+
+
+@pytest.mark.parametrize("mixed", [False, True])
+def test_apply_circuit_copy_batch(dev, ref, mixed):
+    """vqb_apply_circuit_copy_batch (pipelined apply_circuit_copy over host
+    states, circuit.hpp:132-146): every output equals the reference's
+    apply_circuit on that input; more jobs than device slots, so slots are
+    reused."""
+    rng = np.random.default_rng(17)
+    if mixed:
+        n = 6
+        w = circuits.config3(n=n, layers=1)
+        ins = [random_density(n, rng) for _ in range(5)]
+    else:
+        n = 14
+        w = circuits.config1(rows=2, cols=7, cycles=4)
+        ins = [random_state(n, rng) for _ in range(5)]
+    outs = [np.empty_like(x) for x in ins]
+    dev.apply_circuit_copy_batch(w.circuit, n, ins, outs, mixed=mixed)
+    for x, y in zip(ins, outs):
+        r = ref.from_amplitudes(x, mixed)
+        ref.apply_circuit(w.circuit, r)
+        assert np.max(np.abs(y - ref.download(r))) <= TOL
