@@ -591,19 +591,26 @@ def main():
         nbytes = 16 * state.size
         h_in = torch.zeros(2 * state.size, dtype=torch.float64, pin_memory=True)
         h_in[0] = 1.0
-        h_out = torch.empty(2 * state.size, dtype=torch.float64, pin_memory=True)
         import ctypes as ct
         from paper_2406_19212_b200.abi import c128_p
         pin = ct.cast(ct.c_void_p(h_in.data_ptr()), c128_p)
-        pout = ct.cast(ct.c_void_p(h_out.data_ptr()), c128_p)
         up = eng._fn("state_upload")
-        down = eng._fn("state_download")
+
+        # gradient_pure / gradient_mixed (autodiff.hpp:95-98,184-188): the
+        # input is s0 (uploaded from pinned host memory every step), the
+        # result is the loss and the gradient vector, read back to the host by
+        # the call itself; s0 is const in the reference API, nothing else
+        # comes back
+        nparams = wl.w.circuit.num_active_params()
+        last = {}
 
         def e2e_step():
             eng.check(up(state.handle, pin, ct.c_uint64(state.size)))
-            wl.step(eng, state)
-            eng.check(down(state.handle, pout, ct.c_uint64(state.size)))
-            return float(h_out[0])
+            if wl.kind == "grad_pure":
+                last["loss"], last["grads"] = eng.gradient_pure(wl.w.observable, wl.w.circuit, state)
+            else:
+                last["loss"], last["grads"] = eng.gradient_mixed(wl.w.observable, wl.w.circuit, state)
+            return last["loss"]
 
         e2e_step()
         torch.cuda.synchronize()
@@ -617,11 +624,11 @@ def main():
         e1.synchronize()
         ems = max_over_ranks(dist, e0.elapsed_time(e1))
         e2e = {"value": world * wl.units_per_step * args.steps / (ems / 1e3), "unit": wl.unit,
-               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
-               "ms_per_step": ems / args.steps,
-               "path": "vqb_state_upload -> " + ("vqb_apply_circuit" if wl.kind == "apply"
-                                                   else "vqb_gradient_*") + " -> vqb_state_download"}
-        del h_in, h_out
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": 8 * (1 + nparams),
+               "ms_per_step": ems / args.steps, "loss": last["loss"],
+               "path": "vqb_state_upload (s0 from pinned host memory) -> vqb_gradient_"
+                       + ("pure" if wl.kind == "grad_pure" else "mixed") + " (loss + gradients to host)"}
+        del h_in
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

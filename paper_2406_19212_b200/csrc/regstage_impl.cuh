@@ -1624,51 +1624,93 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
                    P.ops[sb.op_begin + run_end].unit && !P.ops[sb.op_begin + run_end].pair)
                 ++run_end;
             if (run_end - k >= 2 && env_int("VQB_JIT_DIAGRUN", 1)) {
-                emit("    {\n");
+                // step-major: Phi and Psi wait in thread-private shared-memory
+                // slots (their registers are free during the run); z =
+                // conj(psi) phi and the running phase product ph stay in
+                // registers; each step's accumulator lives for that step only
+                wide2 = true;
+                emit("    {\n      double2 z[" + I(R) + "], ph[" + I(R) + "];\n");
+                for (int i = 0; i < R; ++i)
+                    emit("      xbuf[" + I(i * T) + " + t] = vf[" + I(i) + "]; xbuf2[" + I(i * T) + " + t] = vg[" + I(i) +
+                         "];\n      z[" + I(i) + "] = make_double2(fma(vg[" + I(i) + "].x, vf[" + I(i) + "].x, vg[" + I(i) +
+                         "].y * vf[" + I(i) + "].y), fma(vg[" + I(i) + "].x, vf[" + I(i) + "].y, -vg[" + I(i) + "].y * vf[" +
+                         I(i) + "].x));\n");
+                fl += 4.0 * R;
+                std::vector<bool> ph_set(R, false);
                 for (int j = k; j < run_end; ++j) {
                     const ROp &oj = P.ops[sb.op_begin + j];
-                    std::string dyn;
+                    std::string dynx;
+                    int rmask = 0;
                     for (int q = 0; q < oj.nc; ++q) {
                         if (oj.ck[q] == 0)
-                            dyn += " | (int)(((base >> " + I(oj.cp[q]) + ") & 1) << " + I(q) + ")";
+                            dynx += " | (int)(((base >> " + I(oj.cp[q]) + ") & 1) << " + I(q) + ")";
                         else if (oj.ck[q] == 1)
-                            dyn += " | (((to >> " + I(oj.cp[q]) + ") & 1) << " + I(q) + ")";
+                            dynx += " | (((to >> " + I(oj.cp[q]) + ") & 1) << " + I(q) + ")";
+                        if (oj.ck[q] == 2) rmask |= 1 << q;
                     }
-                    emit("      const int cd" + I(j) + " = 0" + dyn + ";\n");
-                    if (!dyn.empty()) spool = true;
+                    const bool dyn = !dynx.empty();
+                    if (dyn) spool = true;
+                    emit("      {\n");
+                    if (dyn) emit("        const int cd = 0" + dynx + ";\n");
+                    const int nsubj = 1 << oj.nc;
+                    auto ucls = [&](unsigned off, int cs) {
+                        int c = 0;
+                        for (int cc = 0; cc < nsubj; ++cc)
+                            if (dyn ? (cc & rmask) == cs : cc == cs) c |= pool_cls(P, off + (unsigned)cc, 1, 0);
+                        return c;
+                    };
+                    for (int i = 0; i < R; ++i) {
+                        int cs = 0;
+                        for (int q = 0; q < oj.nc; ++q)
+                            if (oj.ck[q] == 2 && ((i >> oj.cp[q]) & 1)) cs |= 1 << q;
+                        auto elem = [&](unsigned off) {
+                            return dyn ? "spool[" + I(off) + " + (cd | " + I(cs) + ")]" : "P.pool[" + I(off + (unsigned)cs) + "]";
+                        };
+                        const std::string zi = "z[" + I(i) + "]", pi = "ph[" + I(i) + "]";
+                        for (int p = 0; p < oj.np; ++p) {
+                            const unsigned eo = oj.mat_e + (unsigned)(p << oj.nc);
+                            const int c = ucls(eo, cs);
+                            const std::string acc = "acc_s" + I(oj.slot + p), e = elem(eo);
+                            if (c == 1) { emit("        " + acc + " = fma(" + zi + ".x, " + e + ".x, " + acc + ");\n"); fl += 2; }
+                            else if (c == 2) { emit("        " + acc + " = fma(-" + zi + ".y, " + e + ".y, " + acc + ");\n"); fl += 2; }
+                            else if (c == 3) {
+                                emit("        " + acc + " = fma(" + zi + ".x, " + e + ".x, fma(-" + zi + ".y, " + e + ".y, " + acc + "));\n");
+                                fl += 4;
+                            }
+                        }
+                        if (!dyn && ((oj.ident >> cs) & 1)) continue;
+                        const std::string m = elem(oj.mat);
+                        const int c = ucls(oj.mat, cs);
+                        if (!ph_set[i]) {
+                            emit("        " + pi + " = " + m + ";\n");
+                            ph_set[i] = true;
+                        } else if (c == 1) {
+                            emit("        " + pi + ".x *= " + m + ".x; " + pi + ".y *= " + m + ".x;\n");
+                            fl += 2;
+                        } else if (c == 2) {
+                            emit("        " + pi + " = make_double2(-" + m + ".y * " + pi + ".y, " + m + ".y * " + pi + ".x);\n");
+                            fl += 2;
+                        } else {
+                            emit("        " + pi + " = cmul(" + m + ", " + pi + ");\n");
+                            fl += 6;
+                        }
+                    }
+                    emit("      }\n");
+                    for (int p = 0; p < oj.np; ++p) open_slots.push_back(oj.slot + p);
+                    flush_slots(acc_budget);
                 }
                 for (int i = 0; i < R; ++i) {
-                    emit("      {\n        const double2 z = make_double2(fma(vg[" + I(i) + "].x, vf[" + I(i) +
-                         "].x, vg[" + I(i) + "].y * vf[" + I(i) + "].y), fma(vg[" + I(i) + "].x, vf[" + I(i) +
-                         "].y, -vg[" + I(i) + "].y * vf[" + I(i) + "].x));\n        double2 ph = make_double2(1.0, 0.0);\n");
-                    for (int j = k; j < run_end; ++j) {
-                        const ROp &oj = P.ops[sb.op_begin + j];
-                        int cs = 0;
-                        bool dyn = false;
-                        for (int q = 0; q < oj.nc; ++q) {
-                            if (oj.ck[q] == 2 && ((i >> oj.cp[q]) & 1)) cs |= 1 << q;
-                            if (oj.ck[q] != 2) dyn = true;
-                        }
-                        const std::string c = dyn ? "(cd" + I(j) + " | " + I(cs) + ")" : I(cs);
-                        auto elem = [&](unsigned off) {
-                            return dyn ? "spool[" + I(off) + " + " + c + "]" : "P.pool[" + I(off + (unsigned)cs) + "]";
-                        };
-                        for (int p = 0; p < oj.np; ++p) {
-                            const std::string e = elem(oj.mat_e + (unsigned)(p << oj.nc));
-                            emit("        { const double2 e = " + e + "; acc_s" + I(oj.slot + p) +
-                                 " += fma(z.x, e.x, -z.y * e.y); }\n");
-                        }
-                        if (dyn || !((oj.ident >> cs) & 1))
-                            emit("        ph = cmul(" + elem(oj.mat) + ", ph);\n");
+                    if (!ph_set[i]) {
+                        emit("      vf[" + I(i) + "] = xbuf[" + I(i * T) + " + t]; vg[" + I(i) + "] = xbuf2[" + I(i * T) +
+                             " + t];\n");
+                        continue;
                     }
-                    emit("        vf[" + I(i) + "] = cmul(ph, vf[" + I(i) + "]);\n        vg[" + I(i) +
-                         "] = cmul(ph, vg[" + I(i) + "]);\n      }\n");
+                    emit("      vf[" + I(i) + "] = cmul(ph[" + I(i) + "], xbuf[" + I(i * T) + " + t]); vg[" + I(i) +
+                         "] = cmul(ph[" + I(i) + "], xbuf2[" + I(i * T) + " + t]);\n");
+                    fl += 12;
                 }
-                emit("    }\n");
-                for (int j = k; j < run_end; ++j)
-                    for (int p = 0; p < P.ops[sb.op_begin + j].np; ++p)
-                        open_slots.push_back(P.ops[sb.op_begin + j].slot + p);
-                flush_slots(acc_budget);
+                // other threads' later relayout / wide-op writes reuse these slots
+                emit("      __syncthreads();\n    }\n");
                 k = run_end - 1;
                 continue;
             }
