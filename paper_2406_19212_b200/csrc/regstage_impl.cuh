@@ -1224,7 +1224,7 @@ struct WideState {
 // spread over the block's threads. Matrices come from the shared-memory pool
 // copy (*needs_spool).
 std::string jit_wide_op(const RParams &P, int sub, const ROp &op, const std::vector<WideState> &sts,
-                        const char *slot_base, double *wide_fl, bool *needs_spool) {
+                        const char *slot_base, double *wide_fl, bool *needs_spool, bool inplace = false) {
     auto I = [](long long x) { return std::to_string(x); };
     const RLayout &L = P.subs[sub].L;
     const int NT = std::min(std::max(op.nt, 1), kMaxMix), D = 1 << NT;
@@ -1250,11 +1250,14 @@ std::string jit_wide_op(const RParams &P, int sub, const ROp &op, const std::vec
     const bool cond = true;
     *needs_spool = true;
     std::string e = "    {\n";
-    for (const auto &st : sts)
-        for (int i = 0; i < R; ++i)
-            e += std::string("      ") + st.buf + "[" + slot_base + " ^ " + I(slot_const(i)) + "] = " + st.v + "[" +
-                 I(i) + "];\n";
-    e += "      __syncthreads();\n      const int cu = 0";
+    if (!inplace) {
+        for (const auto &st : sts)
+            for (int i = 0; i < R; ++i)
+                e += std::string("      ") + st.buf + "[" + slot_base + " ^ " + I(slot_const(i)) + "] = " + st.v +
+                     "[" + I(i) + "];\n";
+        e += "      __syncthreads();\n";
+    }
+    e += "      const int cu = 0";
     for (int q = 0; q < op.nc; ++q)
         if (op.ck[q] == 0) e += " | (int)(((base >> " + I(op.cp[q]) + ") & 1) << " + I(q) + ")";
     e += ";\n      for (int w = threadIdx.x; w < " + I(S * G) + "; w += " + I(T) + ") {\n";
@@ -1296,11 +1299,14 @@ std::string jit_wide_op(const RParams &P, int sub, const ROp &op, const std::vec
         for (int r = 0; r < D; ++r) e += "        " + std::string(st.buf) + "[sb ^ " + I(sw_off[r]) + "] = o" + I(r) + ";\n";
     }
     e += "       }\n      }\n      __syncthreads();\n";
-    for (const auto &st : sts)
-        for (int i = 0; i < R; ++i)
-            e += std::string("      ") + st.v + "[" + I(i) + "] = " + st.buf + "[" + slot_base + " ^ " +
-                 I(slot_const(i)) + "];\n";
-    e += "      __syncthreads();\n    }\n";
+    if (!inplace) {
+        for (const auto &st : sts)
+            for (int i = 0; i < R; ++i)
+                e += std::string("      ") + st.v + "[" + I(i) + "] = " + st.buf + "[" + slot_base + " ^ " +
+                     I(slot_const(i)) + "];\n";
+        e += "      __syncthreads();\n";
+    }
+    e += "    }\n";
     return e;
 }
 
@@ -1351,26 +1357,41 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
     auto emit = [&](const std::string &x) { body += x; };
     static const int pair_p0[6] = {0, 0, 0, 1, 1, 2}, pair_p1[6] = {1, 2, 3, 2, 3, 3};
     double fl = 0, wfl = 0; // FP64 flops per thread (register code) / per wide-op group
+    // lazy residency (as in the adjoint generator): the tile is in registers
+    // in the layout of cur_sub, or in xbuf in tile-index space; wide ops work
+    // on xbuf in place, so they share the round trip of a neighbouring
+    // relayout. The one-tile-per-block prologue leaves the tile in xbuf.
+    bool in_smem = per_block_mode;
+    int cur_sub = per_block_mode ? -1 : 0;
+    auto to_smem = [&]() {
+        if (in_smem) return;
+        for (int i = 0; i < R; ++i)
+            emit("    xbuf[st" + std::to_string(cur_sub) + " ^ " + std::to_string(slot_const(P.subs[cur_sub].L, i)) +
+                 "] = v[" + std::to_string(i) + "];\n");
+        emit("    __syncthreads();\n");
+        in_smem = true;
+    };
+    auto to_regs = [&](int sub) {
+        if (!in_smem && cur_sub == sub) return;
+        to_smem();
+        for (int i = 0; i < R; ++i)
+            emit("    v[" + std::to_string(i) + "] = xbuf[st" + std::to_string(sub) + " ^ " +
+                 std::to_string(slot_const(P.subs[sub].L, i)) + "];\n");
+        emit("    __syncthreads();\n");
+        in_smem = false;
+        cur_sub = sub;
+    };
     for (int sub = 0; sub < P.nsubs; ++sub) {
         const RSub &sb = P.subs[sub];
-        if (sub > 0) {
-            const RLayout &A = P.subs[sub - 1].L;
-            for (int i = 0; i < R; ++i)
-                emit("    xbuf[st" + std::to_string(sub - 1) + " ^ " + std::to_string(slot_const(A, i)) +
-                     "] = v[" + std::to_string(i) + "];\n");
-            emit("    __syncthreads();\n");
-            for (int i = 0; i < R; ++i)
-                emit("    v[" + std::to_string(i) + "] = xbuf[st" + std::to_string(sub) + " ^ " +
-                     std::to_string(slot_const(sb.L, i)) + "];\n");
-            emit("    __syncthreads();\n");
-        }
         for (int k = 0; k < sb.op_count; ++k) {
             const ROp &op = P.ops[sb.op_begin + k];
             if (op.nt >= 3) {
+                to_smem();
                 emit(jit_wide_op(P, sub, op, {{"v", "xbuf", op.mat, op.ident}}, ("st" + std::to_string(sub)).c_str(),
-                                 &wfl, &spool));
+                                 &wfl, &spool, true));
                 continue;
             }
+            to_regs(sub);
             const int dd = 1 << (2 * op.nt);
             std::string dyn;
             for (int q = 0; q < op.nc; ++q) {
@@ -1440,6 +1461,7 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
             emit("    }\n");
         }
     }
+    to_regs(P.nsubs - 1);
     const RLayout &Lf = P.subs[P.nsubs - 1].L;
     out("#include \"jit_rt.cuh\"\nusing namespace vqbjit;\n");
     out("struct JP { double2 pool[" + std::to_string(std::max(P.npool, 1)) + "]; };\n");
@@ -1509,10 +1531,7 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
             natural(s2, &g, &sl);
             out("    xbuf[nat_st ^ " + std::to_string(sl) + "] = v[" + std::to_string(s2) + "];\n");
         }
-        out("    __syncthreads();\n");
-        for (int i = 0; i < R; ++i)
-            out("    v[" + std::to_string(i) + "] = xbuf[st0 ^ " + std::to_string(slot_const(P.subs[0].L, i)) + "];\n");
-        out("    __syncthreads();\n");
+        out("    __syncthreads();\n"); // the body starts with the tile in xbuf (lazy residency)
     } else {
         out("  auto prefetch = [&](u64 tile) {\n    const u64 b = base_of(tile) | glo;\n    " + opaque_t("tn") +
             "    const int nat_st = swz(tn);\n");
@@ -1598,23 +1617,38 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
                  " + warp] = x; }\n");
         }
     };
-    auto relayout = [&](const char *v, int from, int to) {
-        for (int i = 0; i < R; ++i)
-            emit(std::string("    xbuf[st") + I(from) + " ^ " + I(slot_const(P.subs[from].L, i)) + "] = " + v +
-                 "[" + I(i) + "];\n");
+    // Where Phi and Psi live: in registers in the layout of sub-stage cur_sub,
+    // or in the shared-memory tiles xbuf / xbuf2 in tile-index space (any
+    // layout writes and reads the same slots). Register ops pull them into the
+    // registers of their layout, wide ops push them to the tiles, so a
+    // relayout next to a wide operation shares its shared-memory round trip
+    // and sub-stages without register work cost no relayout.
+    bool in_smem = true; // the prologue leaves both states in the tiles
+    int cur_sub = -1;
+    auto to_smem = [&]() {
+        if (in_smem) return;
+        for (int i = 0; i < R; ++i) {
+            const std::string sl = "st" + I(cur_sub) + " ^ " + I(slot_const(P.subs[cur_sub].L, i));
+            emit("    xbuf[" + sl + "] = vf[" + I(i) + "]; xbuf2[" + sl + "] = vg[" + I(i) + "];\n");
+        }
         emit("    __syncthreads();\n");
-        for (int i = 0; i < R; ++i)
-            emit(std::string("    ") + v + "[" + I(i) + "] = xbuf[st" + I(to) + " ^ " +
-                 I(slot_const(P.subs[to].L, i)) + "];\n");
+        in_smem = true;
+    };
+    auto to_regs = [&](int sub) {
+        if (!in_smem && cur_sub == sub) return;
+        to_smem();
+        for (int i = 0; i < R; ++i) {
+            const std::string sl = "st" + I(sub) + " ^ " + I(slot_const(P.subs[sub].L, i));
+            emit("    vf[" + I(i) + "] = xbuf[" + sl + "]; vg[" + I(i) + "] = xbuf2[" + sl + "];\n");
+        }
         emit("    __syncthreads();\n");
+        in_smem = false;
+        cur_sub = sub;
     };
     for (int sub = 0; sub < P.nsubs; ++sub) {
         const RSub &sb = P.subs[sub];
-        if (sub > 0) {
-            relayout("vf", sub - 1, sub);
-            relayout("vg", sub - 1, sub);
-        }
         for (int k = 0; k < sb.op_count; ++k) {
+            if (P.ops[sb.op_begin + k].nt < 3) to_regs(sub);
             const ROp &op = P.ops[sb.op_begin + k];
             // a run of unit-modulus diagonal steps: conj(psi) phi is invariant
             // along it, so every contribution is Re(z e_p) with z taken once,
@@ -1717,15 +1751,9 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
             if (op.nt >= 3) {
                 const std::string sbase = "st" + I(sub);
                 const WideState wf{"vf", "xbuf", op.mat, op.ident};
-                const WideState wg{"vg", env_int("VQB_JIT_WIDE2", 1) ? "xbuf2" : "xbuf",
-                                   op.pair ? op.mat_psi : op.mat, op.pair ? op.ident_psi : op.ident};
-                if (env_int("VQB_JIT_WIDE2", 1)) {
-                    wide2 = true;
-                    emit(jit_wide_op(P, sub, op, {wf, wg}, sbase.c_str(), &wfl, &spool));
-                } else {
-                    emit(jit_wide_op(P, sub, op, {wf}, sbase.c_str(), &wfl, &spool));
-                    emit(jit_wide_op(P, sub, op, {wg}, sbase.c_str(), &wfl, &spool));
-                }
+                const WideState wg{"vg", "xbuf2", op.pair ? op.mat_psi : op.mat, op.pair ? op.ident_psi : op.ident};
+                to_smem();
+                emit(jit_wide_op(P, sub, op, {wf, wg}, sbase.c_str(), &wfl, &spool, true));
                 continue;
             }
             const int dd = 1 << (2 * op.nt), nsub = 1 << op.nc;
@@ -1817,6 +1845,7 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
         }
     }
     flush_slots(0);
+    to_regs(P.nsubs - 1);
     const RLayout &Lf = P.subs[P.nsubs - 1].L;
     std::string src;
     auto out = [&](const std::string &x) { src += x; };
@@ -1827,9 +1856,10 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
         "        const __grid_constant__ JP P) {\n");
     // shared memory: xbuf (relayouts, Phi's wide ops) [| xbuf2 (Psi's wide
     // ops)] [| pool copy] | gradient reduction slots
-    const int xt = wide2 ? 2 : 1;
+    (void)wide2;
+    const int xt = 2; // xbuf (Phi) and xbuf2 (Psi)
     out("  extern __shared__ __align__(16) double2 sm[];\n  double2 *xbuf = sm;\n");
-    if (wide2) out("  double2 *xbuf2 = sm + " + I(TS) + ";\n");
+    out("  double2 *xbuf2 = sm + " + I(TS) + ";\n");
     const int red_at = xt * TS + (spool ? P.npool : 0);
     if (spool)
         out("  double2 *spool = sm + " + I(xt * TS) + ";\n  for (int i = threadIdx.x; i < " + I(P.npool) +
@@ -1860,19 +1890,13 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
     for (int sub = 0; sub < P.nsubs; ++sub)
         out("  const int st" + I(sub) + " = swz" + thread_expr(P.subs[sub].L.thr, false, "to") + ";\n");
     out("  const int nat_st = swz(to);\n");
-    for (int st2 = 0; st2 < 2; ++st2) {
-        const char *v = st2 ? "vg" : "vf";
-        for (int s2 = 0; s2 < R; ++s2) {
-            int sl = 0;
-            for (int b = 0; b < RB; ++b)
-                if ((s2 >> b) & 1) sl ^= swz(T << b);
-            out(std::string("  xbuf[nat_st ^ ") + I(sl) + "] = " + v + "[" + I(s2) + "];\n");
-        }
-        out("  __syncthreads();\n");
-        for (int i = 0; i < R; ++i)
-            out(std::string("  ") + v + "[" + I(i) + "] = xbuf[st0 ^ " + I(slot_const(P.subs[0].L, i)) + "];\n");
-        out("  __syncthreads();\n");
+    for (int s2 = 0; s2 < R; ++s2) {
+        int sl = 0;
+        for (int b = 0; b < RB; ++b)
+            if ((s2 >> b) & 1) sl ^= swz(T << b);
+        out("  xbuf[nat_st ^ " + I(sl) + "] = vf[" + I(s2) + "]; xbuf2[nat_st ^ " + I(sl) + "] = vg[" + I(s2) + "];\n");
     }
+    out("  __syncthreads();\n");
     out(body);
     for (int i = 0; i < R; ++i) {
         unsigned long long g = 0;
