@@ -464,6 +464,27 @@ def main():
         check["norm"] = state.norm() if wl.sharded else eng.norm(state)
     if wl.sharded:
         check.update(runner.stats())
+    noisy_fwd = None
+    if wl.kind == "grad_mixed":
+        # BASELINE.json's "noisy DM gates/s": the circuit's elements (gates and
+        # channels) per second of forward evolution of the density matrix
+        reset()
+        wl.step_forward = lambda: eng.apply_circuit(wl.w.circuit, state)
+        wl.step_forward()
+        torch.cuda.synchronize()
+        f0e = torch.cuda.Event(enable_timing=True)
+        f1e = torch.cuda.Event(enable_timing=True)
+        f0e.record(stream)
+        for _ in range(args.steps):
+            reset()
+            wl.step_forward()
+        f1e.record(stream)
+        f1e.synchronize()
+        fms = max_over_ranks(dist, f0e.elapsed_time(f1e)) / args.steps
+        noisy_fwd = {"value": world * wl.gates / (fms / 1e3), "unit": "DM gates/s",
+                     "ms_per_forward": fms, "elements": wl.gates,
+                     "what": "vqb_apply_circuit on the 2^30-entry vec(rho) (gates as superoperators + channels), "
+                             "state reset included"}
 
     # roofline: per-kernel CUDA-event timing of one more step (untimed)
     reset()
@@ -657,6 +678,7 @@ def main():
             "hbm_gbs_algorithmic": algo_gbs,
             "hbm_frac_algorithmic": algo_gbs / peak,
             "gpu_launches": launches,
+            "noisy_dm_gates": noisy_fwd,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),

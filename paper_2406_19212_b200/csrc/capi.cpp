@@ -682,14 +682,16 @@ VQB_API int vqb_plan_blocks(const vqb_op *ops, int64_t count, int32_t n, int32_t
         for (const auto &g : prog) fops.push_back(analyse_gate(g));
         const auto stages = plan_stages(fops, pn, tile_bits);
         int64_t nb = 0;
+        std::deque<FusedOp> store;
         for (const auto &sg : stages) {
-            std::vector<FusedOp> blocks;
+            std::vector<const FusedOp *> blocks;
             if (sg.fused && max_support > 0) {
-                blocks = fuse_blocks(fops, sg.ops, max_support);
+                blocks = fuse_blocks_ref(fops, sg.ops, max_support, store);
             } else {
-                for (int i : sg.ops) blocks.push_back(fops[i]);
+                for (int i : sg.ops) blocks.push_back(&fops[i]);
             }
-            for (const auto &b : blocks) {
+            for (const FusedOp *bp : blocks) {
+                const FusedOp &b = *bp;
                 if (nb < cap) {
                     const Gate &g = b.gate;
                     if (g.m > 4) raise(VQB_ERR_UNSUPPORTED, "plan_blocks: block wider than 4 positions");

@@ -2,6 +2,7 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <deque>
 
 namespace vqb {
 
@@ -103,146 +104,195 @@ FusedOp analyse_rev(const RevOp &r) {
 
 namespace {
 
-// Embed matrix M over positions P (global bits) into the space of U (global
-// bits, local order = listed order); identity on U \ P.
-cvec embed(const cvec &M, const std::vector<int> &P, const std::vector<int> &U) {
-    const int u = (int)U.size(), du = 1 << u, dp = 1 << (int)P.size();
-    std::vector<int> where(P.size());
-    for (size_t i = 0; i < P.size(); ++i)
-        where[i] = (int)(std::find(U.begin(), U.end(), P[i]) - U.begin());
-    int pmask = 0;
-    for (int w : where) pmask |= 1 << w;
-    cvec out(size_t(du) * du);
-    for (int c = 0; c < du; ++c)
-        for (int r = 0; r < du; ++r) {
-            if ((r & ~pmask) != (c & ~pmask)) continue;
-            int rp = 0, cp = 0;
-            for (size_t i = 0; i < P.size(); ++i) {
-                rp |= ((r >> where[i]) & 1) << i;
-                cp |= ((c >> where[i]) & 1) << i;
+constexpr int kMaxFuse = 4;                  // qubits (pseudo bits) per fused block
+constexpr int kMaxFuseDim = 1 << kMaxFuse;   // 16
+constexpr int kMaxFuseEnt = kMaxFuseDim * kMaxFuseDim;
+
+// out = embed(M over P into U) * acc, all du x du column-major (du = 2^|U|);
+// embed is the identity on U \ P. No temporaries.
+void embed_mul(const cplx *M, const int *P, int np, const int *U, int nu, const cplx *acc, cplx *out) {
+    const int du = 1 << nu;
+    int where[kMaxFuse], pmask = 0;
+    for (int i = 0; i < np; ++i) {
+        where[i] = 0;
+        for (int j = 0; j < nu; ++j)
+            if (U[j] == P[i]) where[i] = j;
+        pmask |= 1 << where[i];
+    }
+    const int dp = 1 << np;
+    for (int i = 0; i < du * du; ++i) out[i] = cplx(0);
+    // (E acc)[r, j] = sum_c E[r, c] acc[c, j]; E[r, c] != 0 only if r, c agree off P
+    for (int j = 0; j < du; ++j)
+        for (int c = 0; c < du; ++c) {
+            const cplx a = acc[c + j * du];
+            if (a == cplx(0)) continue;
+            int cp = 0;
+            for (int i = 0; i < np; ++i) cp |= ((c >> where[i]) & 1) << i;
+            const int rest = c & ~pmask;
+            for (int rp = 0; rp < dp; ++rp) {
+                int r = rest;
+                for (int i = 0; i < np; ++i) r |= ((rp >> i) & 1) << where[i];
+                out[r + j * du] += M[rp + cp * dp] * a;
             }
-            out[r + size_t(c) * du] = M[rp + size_t(cp) * dp];
         }
-    return out;
 }
 
 struct Block {
-    std::vector<int> U;  // global bits
-    cvec phi, psi;       // psi empty unless a pair block
+    int U[kMaxFuse];     // global bits
+    int nu = 0;
+    cplx phi[kMaxFuseEnt], psi[kMaxFuseEnt]; // psi unused unless a pair block
     bool pair = false;
     bool alive = true;
     bool frozen = false; // parametric or too wide: never merged into
-    int src = -1;        // original op index when frozen
+    int src = -1;        // original op index (frozen, or a single unmerged op)
+    bool merged = false;
 };
-
-std::vector<int> gate_bits(const Gate &g) {
-    std::vector<int> b(g.m);
-    for (int i = 0; i < g.m; ++i) b[i] = g.pos[i] - 1;
-    return b;
-}
 
 } // namespace
 
-std::vector<FusedOp> fuse_blocks(const std::vector<FusedOp> &ops, const std::vector<int> &order,
-                                 int max_support) {
+std::vector<const FusedOp *> fuse_blocks_ref(const std::vector<FusedOp> &ops, const std::vector<int> &order,
+                                             int max_support, std::deque<FusedOp> &store) {
+    max_support = std::min(max_support, kMaxFuse);
     std::vector<Block> blocks;
-    std::vector<int> last(64, -1); // last block per qubit
+    blocks.reserve(order.size());
+    int last[64];
+    for (int &x : last) x = -1;
     for (int idx : order) {
         const FusedOp &f = ops[idx];
         const Gate &g = f.gate;
-        const std::vector<int> P = gate_bits(g);
+        const int np = g.m;
+        int P[VQB_MAX_POSITIONS];
+        for (int i = 0; i < np; ++i) P[i] = g.pos[i] - 1;
         const bool param = f.rev && !f.rev->dmats.empty();
         const bool pair = f.rev && f.rev->psi_op.mat != f.rev->phi_op.mat;
-        if (param || (int)P.size() > max_support || !f.fusable) {
-            Block b;
-            b.U = P;
-            b.frozen = true;
+        auto fresh = [&](bool frozen) {
+            blocks.emplace_back();
+            Block &b = blocks.back();
+            b.frozen = frozen;
             b.src = idx;
-            blocks.push_back(b);
-            for (int q : P) last[q] = (int)blocks.size() - 1;
+            b.nu = std::min(np, kMaxFuse);
+            for (int i = 0; i < b.nu; ++i) b.U[i] = P[i];
+            for (int i = 0; i < np; ++i) last[P[i]] = (int)blocks.size() - 1;
+        };
+        if (param || np > max_support || !f.fusable) {
+            fresh(true);
             continue;
         }
         // candidate blocks: the latest block on each touched qubit
-        std::vector<int> cands;
-        for (int q : P)
-            if (last[q] >= 0 && std::find(cands.begin(), cands.end(), last[q]) == cands.end())
-                cands.push_back(last[q]);
-        std::vector<int> U = P;
-        bool ok = !cands.empty();
-        for (int c : cands) {
-            if (blocks[c].frozen) ok = false;
-            for (int q : blocks[c].U)
-                if (std::find(U.begin(), U.end(), q) == U.end()) U.push_back(q);
+        int cands[kMaxFuse], nc = 0;
+        for (int i = 0; i < np; ++i) {
+            const int c = last[P[i]];
+            if (c < 0) continue;
+            bool seen = false;
+            for (int k = 0; k < nc; ++k) seen |= cands[k] == c;
+            if (!seen) cands[nc++] = c;
         }
-        if (ok && (int)U.size() > max_support) ok = false;
+        int U[2 * kMaxFuse], nu = 0;
+        for (int i = 0; i < np; ++i) U[nu++] = P[i];
+        bool ok = nc > 0;
+        for (int k = 0; k < nc && ok; ++k) {
+            const Block &c = blocks[cands[k]];
+            if (c.frozen) ok = false;
+            for (int i = 0; i < c.nu && ok; ++i) {
+                bool in = false;
+                for (int j = 0; j < nu; ++j) in |= U[j] == c.U[i];
+                if (!in) {
+                    if (nu >= max_support) ok = false;
+                    else U[nu++] = c.U[i];
+                }
+            }
+        }
         // every candidate must be the latest block on all of its qubits, so
         // nothing after it acts on them: it can move forward to the merge
         // point, and the candidates have disjoint supports (they commute)
-        if (ok)
-            for (int c : cands)
-                for (int q : blocks[c].U)
-                    if (last[q] != c) ok = false;
+        for (int k = 0; k < nc && ok; ++k)
+            for (int i = 0; i < blocks[cands[k]].nu; ++i)
+                if (last[blocks[cands[k]].U[i]] != cands[k]) ok = false;
         if (!ok) {
-            Block b;
-            b.U = P;
-            b.phi = g.mat;
-            if (pair) {
-                b.pair = true;
-                b.psi = f.rev->psi_op.mat;
-            }
-            blocks.push_back(b);
-            for (int q : P) last[q] = (int)blocks.size() - 1;
+            fresh(false);
             continue;
         }
         // product of the candidates (disjoint supports, commuting), then op
-        std::sort(U.begin(), U.end());
-        const int du = 1 << (int)U.size();
-        cvec acc_phi(size_t(du) * du), acc_psi;
-        for (int i = 0; i < du; ++i) acc_phi[i + size_t(i) * du] = 1.0;
+        std::sort(U, U + nu);
+        const int du = 1 << nu;
+        cplx acc_phi[kMaxFuseEnt], acc_psi[kMaxFuseEnt], tmp[kMaxFuseEnt];
+        for (int i = 0; i < du * du; ++i) acc_phi[i] = cplx(0);
+        for (int i = 0; i < du; ++i) acc_phi[i + i * du] = 1.0;
         bool any_pair = pair;
-        for (int c : cands) any_pair |= blocks[c].pair;
-        if (any_pair) acc_psi = acc_phi;
-        for (int c : cands) {
-            const Block &b = blocks[c];
-            acc_phi = matmul(embed(b.phi, b.U, U), acc_phi, du);
-            if (any_pair) acc_psi = matmul(embed(b.pair ? b.psi : b.phi, b.U, U), acc_psi, du);
+        for (int k = 0; k < nc; ++k) any_pair |= blocks[cands[k]].pair;
+        if (any_pair) std::copy(acc_phi, acc_phi + du * du, acc_psi);
+        auto src_mat = [&](const Block &b, bool psi) -> const cplx * {
+            if (b.merged) return psi && b.pair ? b.psi : b.phi;
+            const FusedOp &o = ops[b.src];
+            if (psi && o.rev && o.rev->psi_op.mat != o.rev->phi_op.mat) return o.rev->psi_op.mat.data();
+            return o.gate.mat.data();
+        };
+        for (int k = 0; k < nc; ++k) {
+            const Block &b = blocks[cands[k]];
+            embed_mul(src_mat(b, false), b.U, b.nu, U, nu, acc_phi, tmp);
+            std::copy(tmp, tmp + du * du, acc_phi);
+            if (any_pair) {
+                embed_mul(src_mat(b, true), b.U, b.nu, U, nu, acc_psi, tmp);
+                std::copy(tmp, tmp + du * du, acc_psi);
+            }
         }
-        acc_phi = matmul(embed(g.mat, P, U), acc_phi, du);
-        if (any_pair) acc_psi = matmul(embed(pair ? f.rev->psi_op.mat : g.mat, P, U), acc_psi, du);
-        const int keep = *std::max_element(cands.begin(), cands.end());
-        for (int c : cands)
-            if (c != keep) blocks[c].alive = false;
-        Block &k = blocks[keep];
-        k.U = U;
-        k.phi = std::move(acc_phi);
-        k.pair = any_pair;
-        k.psi = std::move(acc_psi);
-        for (int q : U) last[q] = keep;
+        embed_mul(g.mat.data(), P, np, U, nu, acc_phi, tmp);
+        std::copy(tmp, tmp + du * du, acc_phi);
+        if (any_pair) {
+            embed_mul(pair ? f.rev->psi_op.mat.data() : g.mat.data(), P, np, U, nu, acc_psi, tmp);
+            std::copy(tmp, tmp + du * du, acc_psi);
+        }
+        const int keep = *std::max_element(cands, cands + nc);
+        for (int k = 0; k < nc; ++k)
+            if (cands[k] != keep) blocks[cands[k]].alive = false;
+        Block &kb = blocks[keep];
+        kb.nu = nu;
+        std::copy(U, U + nu, kb.U);
+        std::copy(acc_phi, acc_phi + du * du, kb.phi);
+        kb.pair = any_pair;
+        if (any_pair) std::copy(acc_psi, acc_psi + du * du, kb.psi);
+        kb.merged = true;
+        for (int i = 0; i < nu; ++i) last[U[i]] = keep;
     }
-    std::vector<FusedOp> out;
+    std::vector<const FusedOp *> out;
+    out.reserve(blocks.size());
     for (const Block &b : blocks) {
         if (!b.alive) continue;
-        if (b.frozen) {
-            out.push_back(ops[b.src]);
+        if (!b.merged) { // frozen or never merged into: the analysed op as is
+            out.push_back(&ops[b.src]);
             continue;
         }
+        const int du = 1 << b.nu;
         int pos1[VQB_MAX_POSITIONS];
-        for (size_t i = 0; i < b.U.size(); ++i) pos1[i] = b.U[i] + 1;
-        std::vector<const cvec *> mats{&b.phi};
-        if (b.pair) mats.push_back(&b.psi);
-        FusedOp f = analyse(pos1, (int)b.U.size(), mats);
+        for (int i = 0; i < b.nu; ++i) pos1[i] = b.U[i] + 1;
+        cvec phi(b.phi, b.phi + du * du), psi;
+        std::vector<const cvec *> mats{&phi};
+        if (b.pair) {
+            psi.assign(b.psi, b.psi + du * du);
+            mats.push_back(&psi);
+        }
+        FusedOp f = analyse(pos1, b.nu, mats);
         std::vector<int> mix, cnd;
-        split_bits(mats, (int)b.U.size(), mix, cnd);
+        split_bits(mats, b.nu, mix, cnd);
         if (b.pair) {
             f.pair = true;
-            f.sub_psi = sub_blocks(b.psi, (int)b.U.size(), mix, cnd);
+            f.sub_psi = sub_blocks(psi, b.nu, mix, cnd);
         }
         f.gate.kind = VQB_GATE_GENERIC;
-        f.gate.m = (int)b.U.size();
-        for (size_t i = 0; i < b.U.size(); ++i) f.gate.pos[i] = pos1[i];
-        f.gate.mat = b.phi;
-        out.push_back(std::move(f));
+        f.gate.m = b.nu;
+        for (int i = 0; i < b.nu; ++i) f.gate.pos[i] = pos1[i];
+        f.gate.mat = std::move(phi);
+        store.push_back(std::move(f));
+        out.push_back(&store.back());
     }
+    return out;
+}
+
+std::vector<FusedOp> fuse_blocks(const std::vector<FusedOp> &ops, const std::vector<int> &order,
+                                 int max_support) {
+    std::deque<FusedOp> store;
+    std::vector<FusedOp> out;
+    for (const FusedOp *f : fuse_blocks_ref(ops, order, max_support, store)) out.push_back(*f);
     return out;
 }
 

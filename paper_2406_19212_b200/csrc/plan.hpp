@@ -12,6 +12,7 @@
 // a later operation may overtake a deferred one only if their supports are
 // disjoint (they commute), so the stage order reproduces the program exactly.
 #pragma once
+#include <deque>
 
 #include "engine.hpp"
 
@@ -56,5 +57,9 @@ std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k);
 // are. Returns the stage's new operation list (re-analysed).
 std::vector<FusedOp> fuse_blocks(const std::vector<FusedOp> &ops, const std::vector<int> &order,
                                  int max_support);
+// The same without copying: unmerged operations are returned as pointers into
+// `ops`, merged blocks are stored in `store` (stable addresses).
+std::vector<const FusedOp *> fuse_blocks_ref(const std::vector<FusedOp> &ops, const std::vector<int> &order,
+                                             int max_support, std::deque<FusedOp> &store);
 
 } // namespace vqb

@@ -811,7 +811,7 @@ struct SlotMap {
 // Lower as much of a stage's block list as fits one parameter block.
 // `remaining` (block indices, in a valid order) is consumed; what is left
 // must run in a following launch with the same tile bits.
-void lower_stage_reg(const Stage &sg, const std::vector<FusedOp> &blocks,
+void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks,
                      std::vector<int> &remaining, int pn, bool rev, RParams &P, SlotMap &slots) {
     std::memset(&P, 0, sizeof P);
     for (int j = 0; j < K; ++j) P.bits[j] = sg.bits[j];
@@ -858,7 +858,7 @@ void lower_stage_reg(const Stage &sg, const std::vector<FusedOp> &blocks,
         std::vector<int> taken, deferred;
         int pool_used = 0, ops_used = 0, slots_used = 0, xp_used = 0;
         for (int i : remaining) {
-            const FusedOp &f = blocks[i];
+            const FusedOp &f = *blocks[i];
             const unsigned mix = mixmask(f);
             const int nx = count_x(f);
             const bool fits_res = nops + ops_used < kMaxOps &&
@@ -879,7 +879,7 @@ void lower_stage_reg(const Stage &sg, const std::vector<FusedOp> &blocks,
         }
         if (taken.empty()) break; // parameter block full: continue in the next launch
         for (int i : deferred) {
-            const unsigned mix = mixmask(blocks[i]);
+            const unsigned mix = mixmask(*blocks[i]);
             if (__builtin_popcount(rset | mix) <= RB) rset |= mix;
         }
         for (int j = K - 1; j >= 0 && __builtin_popcount(rset) < RB; --j) rset |= 1u << j;
@@ -903,7 +903,7 @@ void lower_stage_reg(const Stage &sg, const std::vector<FusedOp> &blocks,
         };
         sb.op_begin = nops;
         for (int i : taken) {
-            const FusedOp &f = blocks[i];
+            const FusedOp &f = *blocks[i];
             ROp &o = P.ops[nops++];
             o.nt = f.nt;
             o.nc = f.nc;
@@ -1381,14 +1381,17 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
         in_smem = false;
         cur_sub = sub;
     };
+    const bool lazy = env_int("VQB_JIT_LAZY", 1) != 0;
     for (int sub = 0; sub < P.nsubs; ++sub) {
         const RSub &sb = P.subs[sub];
+        if (!lazy) to_regs(sub);
         for (int k = 0; k < sb.op_count; ++k) {
             const ROp &op = P.ops[sb.op_begin + k];
             if (op.nt >= 3) {
                 to_smem();
                 emit(jit_wide_op(P, sub, op, {{"v", "xbuf", op.mat, op.ident}}, ("st" + std::to_string(sub)).c_str(),
                                  &wfl, &spool, true));
+                if (!lazy) to_regs(sub);
                 continue;
             }
             to_regs(sub);
@@ -1645,8 +1648,10 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
         in_smem = false;
         cur_sub = sub;
     };
+    const bool lazy = env_int("VQB_JIT_LAZY", 1) != 0;
     for (int sub = 0; sub < P.nsubs; ++sub) {
         const RSub &sb = P.subs[sub];
+        if (!lazy) to_regs(sub);
         for (int k = 0; k < sb.op_count; ++k) {
             if (P.ops[sb.op_begin + k].nt < 3) to_regs(sub);
             const ROp &op = P.ops[sb.op_begin + k];
@@ -1754,6 +1759,7 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
                 const WideState wg{"vg", "xbuf2", op.pair ? op.mat_psi : op.mat, op.pair ? op.ident_psi : op.ident};
                 to_smem();
                 emit(jit_wide_op(P, sub, op, {wf, wg}, sbase.c_str(), &wfl, &spool, true));
+                if (!lazy) to_regs(sub);
                 continue;
             }
             const int dd = 1 << (2 * op.nt), nsub = 1 << op.nc;
@@ -1964,7 +1970,7 @@ std::string shape_key(const RParams &P, bool rev) {
             cls[(size_t)i >> 2] = (char)(cls[(size_t)i >> 2] | (pool_cls(P, (unsigned)i, 1, 0) << (2 * (i & 3))));
         key += cls;
     }
-    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2"}) {
+    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY"}) {
         const char *v = std::getenv(e);
         key += '|';
         if (v) key += v;
@@ -2016,6 +2022,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
         VQB_CUDA(cudaMemsetAsync(m_partial.p, 0, sizeof(double) * (size_t)grid * total_slots, st));
     }
     SlotMap slots;
+    std::deque<FusedOp> fused_store; // merged blocks of every stage (stable addresses)
     // Actions (a launch, or an unfusable op) are lowered in program order and
     // issued as soon as their kernel is known, so the host's planning of later
     // stages overlaps the device's work on earlier ones. The first
@@ -2115,11 +2122,11 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             submit(std::move(a));
             continue;
         }
-        std::vector<FusedOp> blocks;
+        std::vector<const FusedOp *> blocks;
         HostAcc ha_f(&t_fuse);
-        if (max_support > 0) blocks = fuse_blocks(fops, sg.ops, max_support);
+        if (max_support > 0) blocks = fuse_blocks_ref(fops, sg.ops, max_support, fused_store);
         else
-            for (int idx : sg.ops) blocks.push_back(fops[idx]);
+            for (int idx : sg.ops) blocks.push_back(&fops[idx]);
         std::vector<int> remaining(blocks.size());
         for (size_t i = 0; i < blocks.size(); ++i) remaining[i] = (int)i;
         while (!remaining.empty()) {
