@@ -41,6 +41,7 @@
 #include <unordered_map>
 
 #include "jit.hpp"
+#include <map>
 #include "plan.hpp"
 
 #define VQB_RS_STR2(x) #x
@@ -1663,74 +1664,121 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
                    P.ops[sb.op_begin + run_end].unit && !P.ops[sb.op_begin + run_end].pair)
                 ++run_end;
             if (run_end - k >= 2 && env_int("VQB_JIT_DIAGRUN", 1)) {
-                // step-major: Phi and Psi wait in thread-private shared-memory
-                // slots (their registers are free during the run); z =
-                // conj(psi) phi and the running phase product ph stay in
-                // registers; each step's accumulator lives for that step only
+                // Step-major, factored by register conditions. A step's
+                // matrix element depends on a register element i only through
+                // the register bits among its condition bits (mask rm, usually
+                // none or one bit). So its contribution sum_i Re(z_i e(c(i)))
+                // = sum_g Re(S_rm[g] e(g)) with S_rm[g] the sum of z over the
+                // elements whose rm-bits are g (taken once per run), and its
+                // phase multiplies one of 2^|rm| running products PH_rm[g];
+                // each element gets the product of its PH's at the end. Phi
+                // and Psi wait in thread-private shared-memory slots meanwhile.
                 wide2 = true;
-                emit("    {\n      double2 z[" + I(R) + "], ph[" + I(R) + "];\n");
+                auto rmask_of = [&](const ROp &o) {
+                    int m = 0;
+                    for (int q = 0; q < o.nc; ++q)
+                        if (o.ck[q] == 2) m |= 1 << o.cp[q];
+                    return m;
+                };
+                auto extract = [](int i, int m) { // bits of i under mask m, compressed
+                    int g = 0, k2 = 0;
+                    for (int b = 0; b < RB; ++b)
+                        if ((m >> b) & 1) g |= ((i >> b) & 1) << k2++;
+                    return g;
+                };
+                std::vector<int> masks;
+                for (int j = k; j < run_end; ++j) {
+                    const int m = rmask_of(P.ops[sb.op_begin + j]);
+                    if (std::find(masks.begin(), masks.end(), m) == masks.end()) masks.push_back(m);
+                }
+                emit("    {\n");
                 for (int i = 0; i < R; ++i)
                     emit("      xbuf[" + I(i * T) + " + t] = vf[" + I(i) + "]; xbuf2[" + I(i * T) + " + t] = vg[" + I(i) +
-                         "];\n      z[" + I(i) + "] = make_double2(fma(vg[" + I(i) + "].x, vf[" + I(i) + "].x, vg[" + I(i) +
-                         "].y * vf[" + I(i) + "].y), fma(vg[" + I(i) + "].x, vf[" + I(i) + "].y, -vg[" + I(i) + "].y * vf[" +
-                         I(i) + "].x));\n");
+                         "];\n");
+                emit("      double2 z[" + I(R) + "];\n");
+                for (int i = 0; i < R; ++i)
+                    emit("      z[" + I(i) + "] = make_double2(fma(vg[" + I(i) + "].x, vf[" + I(i) + "].x, vg[" + I(i) +
+                         "].y * vf[" + I(i) + "].y), fma(vg[" + I(i) + "].x, vf[" + I(i) + "].y, -vg[" + I(i) +
+                         "].y * vf[" + I(i) + "].x));\n");
                 fl += 4.0 * R;
-                std::vector<bool> ph_set(R, false);
+                // class sums S_m_g, phase products PH_m_g
+                for (int m : masks) {
+                    const int ng = 1 << __builtin_popcount(m);
+                    for (int g = 0; g < ng; ++g) {
+                        std::string e = "      const double2 S" + I(m) + "_" + I(g) + " = make_double2(0.0";
+                        std::string ex, ey;
+                        for (int i = 0; i < R; ++i)
+                            if (extract(i, m) == g) {
+                                ex += " + z[" + I(i) + "].x";
+                                ey += " + z[" + I(i) + "].y";
+                                fl += 2;
+                            }
+                        emit(e + ex + ", 0.0" + ey + ");\n      double2 PH" + I(m) + "_" + I(g) + ";\n");
+                    }
+                }
+                std::map<std::pair<int, int>, bool> ph_set;
                 for (int j = k; j < run_end; ++j) {
                     const ROp &oj = P.ops[sb.op_begin + j];
                     std::string dynx;
-                    int rmask = 0;
+                    int rmq = 0;
                     for (int q = 0; q < oj.nc; ++q) {
                         if (oj.ck[q] == 0)
                             dynx += " | (int)(((base >> " + I(oj.cp[q]) + ") & 1) << " + I(q) + ")";
                         else if (oj.ck[q] == 1)
                             dynx += " | (((to >> " + I(oj.cp[q]) + ") & 1) << " + I(q) + ")";
-                        if (oj.ck[q] == 2) rmask |= 1 << q;
+                        else
+                            rmq |= 1 << q;
                     }
                     const bool dyn = !dynx.empty();
                     if (dyn) spool = true;
+                    const int m = rmask_of(oj);
+                    const int ng = 1 << __builtin_popcount(m);
+                    const int nsubj = 1 << oj.nc;
                     emit("      {\n");
                     if (dyn) emit("        const int cd = 0" + dynx + ";\n");
-                    const int nsubj = 1 << oj.nc;
-                    auto ucls = [&](unsigned off, int cs) {
-                        int c = 0;
-                        for (int cc = 0; cc < nsubj; ++cc)
-                            if (dyn ? (cc & rmask) == cs : cc == cs) c |= pool_cls(P, off + (unsigned)cc, 1, 0);
-                        return c;
-                    };
-                    for (int i = 0; i < R; ++i) {
-                        int cs = 0;
+                    for (int g = 0; g < ng; ++g) {
+                        // condition index bits contributed by the register bits g
+                        int cs = 0, k2 = 0, full = 0;
+                        for (int b = 0; b < RB; ++b)
+                            if ((m >> b) & 1) full |= ((g >> k2++) & 1) << b;
                         for (int q = 0; q < oj.nc; ++q)
-                            if (oj.ck[q] == 2 && ((i >> oj.cp[q]) & 1)) cs |= 1 << q;
+                            if (oj.ck[q] == 2 && ((full >> oj.cp[q]) & 1)) cs |= 1 << q;
                         auto elem = [&](unsigned off) {
                             return dyn ? "spool[" + I(off) + " + (cd | " + I(cs) + ")]" : "P.pool[" + I(off + (unsigned)cs) + "]";
                         };
-                        const std::string zi = "z[" + I(i) + "]", pi = "ph[" + I(i) + "]";
+                        auto ucls = [&](unsigned off) {
+                            int c = 0;
+                            for (int cc = 0; cc < nsubj; ++cc)
+                                if (dyn ? (cc & rmq) == cs : cc == cs) c |= pool_cls(P, off + (unsigned)cc, 1, 0);
+                            return c;
+                        };
+                        const std::string Sg = "S" + I(m) + "_" + I(g), PHg = "PH" + I(m) + "_" + I(g);
                         for (int p = 0; p < oj.np; ++p) {
                             const unsigned eo = oj.mat_e + (unsigned)(p << oj.nc);
-                            const int c = ucls(eo, cs);
+                            const int c = ucls(eo);
                             const std::string acc = "acc_s" + I(oj.slot + p), e = elem(eo);
-                            if (c == 1) { emit("        " + acc + " = fma(" + zi + ".x, " + e + ".x, " + acc + ");\n"); fl += 2; }
-                            else if (c == 2) { emit("        " + acc + " = fma(-" + zi + ".y, " + e + ".y, " + acc + ");\n"); fl += 2; }
+                            if (c == 1) { emit("        " + acc + " = fma(" + Sg + ".x, " + e + ".x, " + acc + ");\n"); fl += 2; }
+                            else if (c == 2) { emit("        " + acc + " = fma(-" + Sg + ".y, " + e + ".y, " + acc + ");\n"); fl += 2; }
                             else if (c == 3) {
-                                emit("        " + acc + " = fma(" + zi + ".x, " + e + ".x, fma(-" + zi + ".y, " + e + ".y, " + acc + "));\n");
+                                emit("        " + acc + " = fma(" + Sg + ".x, " + e + ".x, fma(-" + Sg + ".y, " + e + ".y, " + acc + "));\n");
                                 fl += 4;
                             }
                         }
                         if (!dyn && ((oj.ident >> cs) & 1)) continue;
-                        const std::string m = elem(oj.mat);
-                        const int c = ucls(oj.mat, cs);
-                        if (!ph_set[i]) {
-                            emit("        " + pi + " = " + m + ";\n");
-                            ph_set[i] = true;
+                        const std::string mm = elem(oj.mat);
+                        const int c = ucls(oj.mat);
+                        bool &set = ph_set[{m, g}];
+                        if (!set) {
+                            emit("        " + PHg + " = " + mm + ";\n");
+                            set = true;
                         } else if (c == 1) {
-                            emit("        " + pi + ".x *= " + m + ".x; " + pi + ".y *= " + m + ".x;\n");
+                            emit("        " + PHg + ".x *= " + mm + ".x; " + PHg + ".y *= " + mm + ".x;\n");
                             fl += 2;
                         } else if (c == 2) {
-                            emit("        " + pi + " = make_double2(-" + m + ".y * " + pi + ".y, " + m + ".y * " + pi + ".x);\n");
+                            emit("        " + PHg + " = make_double2(-" + mm + ".y * " + PHg + ".y, " + mm + ".y * " + PHg + ".x);\n");
                             fl += 2;
                         } else {
-                            emit("        " + pi + " = cmul(" + m + ", " + pi + ");\n");
+                            emit("        " + PHg + " = cmul(" + mm + ", " + PHg + ");\n");
                             fl += 6;
                         }
                     }
@@ -1738,14 +1786,26 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
                     for (int p = 0; p < oj.np; ++p) open_slots.push_back(oj.slot + p);
                     flush_slots(acc_budget);
                 }
+                // every element: the product of its phase products
                 for (int i = 0; i < R; ++i) {
-                    if (!ph_set[i]) {
+                    std::string ph;
+                    for (int m : masks) {
+                        const int g = extract(i, m);
+                        if (!ph_set[{m, g}]) continue;
+                        const std::string t2 = "PH" + I(m) + "_" + I(g);
+                        if (ph.empty()) ph = t2;
+                        else {
+                            ph = "cmul(" + t2 + ", " + ph + ")";
+                            fl += 6;
+                        }
+                    }
+                    if (ph.empty()) {
                         emit("      vf[" + I(i) + "] = xbuf[" + I(i * T) + " + t]; vg[" + I(i) + "] = xbuf2[" + I(i * T) +
                              " + t];\n");
                         continue;
                     }
-                    emit("      vf[" + I(i) + "] = cmul(ph[" + I(i) + "], xbuf[" + I(i * T) + " + t]); vg[" + I(i) +
-                         "] = cmul(ph[" + I(i) + "], xbuf2[" + I(i * T) + " + t]);\n");
+                    emit("      { const double2 ph = " + ph + "; vf[" + I(i) + "] = cmul(ph, xbuf[" + I(i * T) +
+                         " + t]); vg[" + I(i) + "] = cmul(ph, xbuf2[" + I(i * T) + " + t]); }\n");
                     fl += 12;
                 }
                 // other threads' later relayout / wide-op writes reuse these slots
