@@ -1396,6 +1396,110 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
                 continue;
             }
             to_regs(sub);
+            {
+                // a run of diagonal operations (they commute): each one's
+                // element depends on register element i only through the
+                // register bits among its conditions (mask m, usually none or
+                // one bit), so it multiplies one of 2^|m| per-thread phase
+                // products PH_m[g]; every element gets its product once at
+                // the end of the run
+                int run_end = k;
+                while (run_end < sb.op_count && P.ops[sb.op_begin + run_end].nt == 0) ++run_end;
+                if (run_end - k >= 2 && env_int("VQB_JIT_DIAGRUN", 1)) {
+                    auto I = [](long long x) { return std::to_string(x); };
+                    auto rmask_of = [&](const ROp &o) {
+                        int m = 0;
+                        for (int q = 0; q < o.nc; ++q)
+                            if (o.ck[q] == 2) m |= 1 << o.cp[q];
+                        return m;
+                    };
+                    auto extract = [](int i, int m) {
+                        int g = 0, k2 = 0;
+                        for (int b = 0; b < RB; ++b)
+                            if ((m >> b) & 1) g |= ((i >> b) & 1) << k2++;
+                        return g;
+                    };
+                    std::vector<int> masks;
+                    for (int j = k; j < run_end; ++j) {
+                        const int m = rmask_of(P.ops[sb.op_begin + j]);
+                        if (std::find(masks.begin(), masks.end(), m) == masks.end()) masks.push_back(m);
+                    }
+                    emit("    {\n");
+                    for (int m : masks)
+                        for (int g = 0; g < (1 << __builtin_popcount(m)); ++g)
+                            emit("      double2 PH" + I(m) + "_" + I(g) + ";\n");
+                    std::map<std::pair<int, int>, bool> ph_set;
+                    for (int j = k; j < run_end; ++j) {
+                        const ROp &oj = P.ops[sb.op_begin + j];
+                        std::string dynx;
+                        int rmq = 0;
+                        for (int q = 0; q < oj.nc; ++q) {
+                            if (oj.ck[q] == 0)
+                                dynx += " | (int)(((base >> " + I(oj.cp[q]) + ") & 1) << " + I(q) + ")";
+                            else if (oj.ck[q] == 1)
+                                dynx += " | (((t >> " + I(oj.cp[q]) + ") & 1) << " + I(q) + ")";
+                            else
+                                rmq |= 1 << q;
+                        }
+                        const bool dynj = !dynx.empty();
+                        if (dynj) spool = true;
+                        const int m = rmask_of(oj);
+                        emit("      {\n");
+                        if (dynj) emit("        const int cd = 0" + dynx + ";\n");
+                        for (int g = 0; g < (1 << __builtin_popcount(m)); ++g) {
+                            int cs = 0, k2 = 0, full = 0;
+                            for (int b = 0; b < RB; ++b)
+                                if ((m >> b) & 1) full |= ((g >> k2++) & 1) << b;
+                            for (int q = 0; q < oj.nc; ++q)
+                                if (oj.ck[q] == 2 && ((full >> oj.cp[q]) & 1)) cs |= 1 << q;
+                            if (!dynj && ((oj.ident >> cs) & 1)) continue;
+                            const std::string mm = dynj ? "spool[" + I(oj.mat) + " + (cd | " + I(cs) + ")]"
+                                                        : MP + "[" + I(oj.mat + (unsigned)cs) + "]";
+                            int c = 0;
+                            for (int cc = 0; cc < (1 << oj.nc); ++cc)
+                                if (dynj ? (cc & rmq) == cs : cc == cs) c |= pool_cls(P, oj.mat + (unsigned)cc, 1, 0);
+                            const std::string PHg = "PH" + I(m) + "_" + I(g);
+                            bool &set = ph_set[{m, g}];
+                            if (!set) {
+                                emit("        " + PHg + " = " + mm + ";\n");
+                                set = true;
+                            } else if (c == 1) {
+                                emit("        " + PHg + ".x *= " + mm + ".x; " + PHg + ".y *= " + mm + ".x;\n");
+                                fl += 2;
+                            } else if (c == 2) {
+                                emit("        " + PHg + " = make_double2(-" + mm + ".y * " + PHg + ".y, " + mm + ".y * " +
+                                     PHg + ".x);\n");
+                                fl += 2;
+                            } else if (c == 0) {
+                                emit("        " + PHg + " = make_double2(0.0, 0.0);\n");
+                            } else {
+                                emit("        " + PHg + " = cmul(" + mm + ", " + PHg + ");\n");
+                                fl += 6;
+                            }
+                        }
+                        emit("      }\n");
+                    }
+                    for (int i = 0; i < R; ++i) {
+                        std::string ph;
+                        for (int m : masks) {
+                            const int g = extract(i, m);
+                            if (!ph_set[{m, g}]) continue;
+                            const std::string t2 = "PH" + I(m) + "_" + I(g);
+                            if (ph.empty()) ph = t2;
+                            else {
+                                ph = "cmul(" + t2 + ", " + ph + ")";
+                                fl += 6;
+                            }
+                        }
+                        if (ph.empty()) continue;
+                        emit("      v[" + I(i) + "] = cmul(" + ph + ", v[" + I(i) + "]);\n");
+                        fl += 6;
+                    }
+                    emit("    }\n");
+                    k = run_end - 1;
+                    continue;
+                }
+            }
             const int dd = 1 << (2 * op.nt);
             std::string dyn;
             for (int q = 0; q < op.nc; ++q) {
