@@ -198,6 +198,28 @@ inline void apply_circuit(const vqcs::Circuit<double> &c, vqcs::MixedState<doubl
     d.download(dm.entries());
 }
 
+// apply_circuit_copy (circuit.hpp:132-146) over a batch of host states: one
+// call, uploads / circuits / downloads of consecutive states overlapped
+// (vqb_apply_circuit_copy_batch). Host buffers of the reference's states are
+// pageable; register them (cudaHostRegister) for full copy overlap.
+inline std::vector<vqcs::PureState<double>> apply_circuit_copy(const vqcs::Circuit<double> &c,
+                                                              const std::vector<vqcs::PureState<double>> &in) {
+    std::vector<vqcs::PureState<double>> out(in.begin(), in.end());
+    if (in.empty()) return out;
+    const auto L = lower(c);
+    std::vector<const vqb_c128 *> src;
+    std::vector<vqb_c128 *> dst;
+    for (size_t j = 0; j < in.size(); ++j) {
+        if (in[j].num_qubits() != in[0].num_qubits())
+            throw vqcs::ShapeError("apply_circuit_copy: states of different sizes in one batch");
+        src.push_back(reinterpret_cast<const vqb_c128 *>(in[j].amplitudes().data()));
+        dst.push_back(reinterpret_cast<vqb_c128 *>(out[j].amplitudes().data()));
+    }
+    check(vqb_apply_circuit_copy_batch(in[0].num_qubits(), 0, L.ops.data(), static_cast<int64_t>(L.ops.size()),
+                                       src.data(), dst.data(), static_cast<int64_t>(in.size())));
+    return out;
+}
+
 inline std::complex<double> expectation(const vqcs::PauliOperator &op, const DeviceState &s) {
     const auto L = lower(op);
     vqb_c128 out{};

@@ -82,6 +82,20 @@ int main() {
     }
     for (std::uint64_t k = 0; k < m1.size(); ++k) mmax = std::max(mmax, std::abs(m1[k] - m2[k]));
 
+    // apply_circuit_copy over a batch of host states (one pipelined call)
+    std::vector<PureState<double>> ins;
+    for (int j = 0; j < 4; ++j) {
+        PureState<double> x(n);
+        vqcs::apply_circuit(bench::generate_rqc<double>(n, 1, 100 + j), x, cfg);
+        ins.push_back(x);
+    }
+    const auto outs = vqb::apply_circuit_copy(c, ins);
+    double bmax = outs.size() == ins.size() ? 0 : 1;
+    for (size_t j = 0; j < ins.size() && j < outs.size(); ++j) {
+        const PureState<double> r = vqcs::apply_circuit_copy(c, ins[j], cfg);
+        for (std::uint64_t k = 0; k < r.size(); ++k) bmax = std::max(bmax, std::abs(r[k] - outs[j][k]));
+    }
+
     // state dumps (io.hpp): a device dump loads back through the reference
     vqb::DeviceState ds(a);
     vqb::save_state(ds, "/tmp/vqb_facade_demo.vqcs");
@@ -91,10 +105,10 @@ int main() {
 
     std::printf("grad max|d|=%.3e (max|g|=%.3e) state max|d|=%.3e noisy max|d|=%.3e "
                 "non-invertible->vqcs::NonInvertibleChannelError:%d fuse max|d|=%.3e "
-                "measure outcomes equal:%d max|d|=%.3e dump max|d|=%.3e\n",
-                dmax, gmax, amax, nmax, threw, fmax, m_ok, mmax, iomax);
+                "measure outcomes equal:%d max|d|=%.3e dump max|d|=%.3e batch max|d|=%.3e\n",
+                dmax, gmax, amax, nmax, threw, fmax, m_ok, mmax, iomax, bmax);
     return (g_ok && amax <= 1e-12 && nmax <= 1e-10 * ngmax && threw && fmax <= 1e-15 && m_ok &&
-            mmax <= 1e-12 && iomax == 0)
+            mmax <= 1e-12 && iomax == 0 && bmax <= 1e-12)
                ? 0
                : 1;
 }
