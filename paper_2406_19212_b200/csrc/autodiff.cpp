@@ -8,11 +8,129 @@
 // the end (no per-gate synchronisation).
 #include "autodiff.hpp"
 
+#include <condition_variable>
+#include <deque>
+#include <functional>
+#include <future>
+#include <mutex>
+#include <thread>
+
 #include "engine.hpp"
 
 namespace vqb {
 
 namespace {
+
+// ---- host-parallel adjoint ----
+// One persistent worker thread (its thread-local executor buffers and kernel
+// lookups stay warm across calls) runs the reverse sweep's host work --
+// reverse program, folding, analysis, stage planning, block fusion, lowering,
+// kernel lookup -- while the calling thread plans and launches the forward
+// pass; the worker launches only after the caller opens the gate (stream
+// order: forward, costate, loss, then the sweep).
+struct LaunchGate {
+    std::mutex mu;
+    std::condition_variable cv;
+    bool open = false, abort = false;
+};
+thread_local LaunchGate *g_gate = nullptr;
+
+class Worker {
+  public:
+    Worker() : th_([this] { loop(); }) {}
+    ~Worker() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        th_.join();
+    }
+    std::future<void> submit(std::function<void()> fn) {
+        std::packaged_task<void()> task(std::move(fn));
+        auto fut = task.get_future();
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            q_.push_back(std::move(task));
+        }
+        cv_.notify_one();
+        return fut;
+    }
+
+  private:
+    void loop() {
+        for (;;) {
+            std::packaged_task<void()> task;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || !q_.empty(); });
+                if (stop_ && q_.empty()) return;
+                task = std::move(q_.front());
+                q_.pop_front();
+            }
+            task();
+        }
+    }
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<std::packaged_task<void()>> q_;
+    bool stop_ = false;
+    std::thread th_;
+};
+
+Worker &worker() {
+    static Worker w;
+    return w;
+}
+
+bool parallel_adjoint() {
+    static const bool on = [] {
+        const char *v = std::getenv("VQB_PARALLEL_ADJOINT");
+        return !(v && *v == '0');
+    }();
+    return on;
+}
+
+// Runs `sweep` on the worker behind a gate; open() lets it launch, finish()
+// waits for it (rethrowing its error). If the caller unwinds without opening,
+// the sweep is aborted before any launch.
+class GatedSweep {
+  public:
+    explicit GatedSweep(std::function<void()> sweep) {
+        fut_ = worker().submit([this, sweep = std::move(sweep)] {
+            g_gate = &gate_;
+            struct Reset {
+                ~Reset() { g_gate = nullptr; }
+            } reset;
+            sweep();
+        });
+    }
+    void open() {
+        {
+            std::lock_guard<std::mutex> lk(gate_.mu);
+            gate_.open = true;
+        }
+        gate_.cv.notify_all();
+    }
+    void finish() {
+        done_ = true;
+        fut_.get();
+    }
+    ~GatedSweep() {
+        if (done_) return;
+        {
+            std::lock_guard<std::mutex> lk(gate_.mu);
+            gate_.abort = true;
+        }
+        gate_.cv.notify_all();
+        fut_.wait();
+    }
+
+  private:
+    LaunchGate gate_;
+    std::future<void> fut_;
+    bool done_ = false;
+};
 
 // Device buffer for the gradient vector and the loss, reused across calls
 // on a thread (grow-only): a cudaMalloc/cudaFree pair per call would cost
@@ -130,6 +248,15 @@ double loss_mixed(const vqb_op *ops, int64_t count, const vqb_pauli_term *terms,
     return expectation(s, op).real();
 }
 
+void wait_issue_gate() {
+    LaunchGate *g = g_gate;
+    if (!g) return;
+    std::unique_lock<std::mutex> lk(g->mu);
+    g->cv.wait(lk, [&] { return g->open || g->abort; });
+    if (g->abort) raise(VQB_ERR_INTERNAL, "adjoint sweep aborted: the forward pass failed");
+    g_gate = nullptr; // open: later launches need not wait
+}
+
 GradientOut gradient_pure(const vqb_op *ops, int64_t count, const vqb_pauli_term *terms,
                           int64_t nterms, DeviceState *s0, bool want_residual, bool fused) {
     if (s0->mixed) raise(VQB_ERR_TYPE, "gradient_pure: pure initial state required");
@@ -150,28 +277,20 @@ GradientOut gradient_pure(const vqb_op *ops, int64_t count, const vqb_pauli_term
 
     DeviceState *phi = clone(s0);
     StateGuard gphi{phi};
-    {
-        HostTimer ht("gradient_pure forward");
-        run_program(phi, fwd, fused);
-    }
-
     GradientOut out;
     out.grads.assign(total, 0.0);
     if (total == 0) {
+        run_program(phi, fwd, fused);
         out.loss = expectation(phi, op).real();
         return out;
     }
     DeviceState *psi = scratch(n, 0); // fully overwritten by apply_operator
     StateGuard gpsi{psi};
-    VQB_CUDA(cudaStreamSynchronize(psi->stream));
-    apply_operator(phi, psi->amps, op, false);
     const size_t gbytes = sizeof(double2) * ((total + 1) / 2); // keep dloss 16-B aligned
     DevBuf dbuf(gbytes + sizeof(double2));
     double *dgrads = dbuf.as<double>();
     double2 *dloss = reinterpret_cast<double2 *>(dbuf.as<char>() + gbytes);
-    dot_async(phi, phi->amps, psi->amps, dloss); // loss = Re <phi|H phi>
-
-    {
+    auto sweep = [&] {
         HostTimer ht("gradient_pure reverse");
         std::vector<RevOp> rprog;
         {
@@ -179,6 +298,21 @@ GradientOut gradient_pure(const vqb_op *ops, int64_t count, const vqb_pauli_term
             rprog = pure_reverse_program(es, base);
         }
         run_reverse(phi, psi, rprog, dgrads, fused);
+    };
+    std::unique_ptr<GatedSweep> gs;
+    if (parallel_adjoint()) gs = std::make_unique<GatedSweep>(sweep);
+    {
+        HostTimer ht("gradient_pure forward");
+        run_program(phi, fwd, fused);
+    }
+    VQB_CUDA(cudaStreamSynchronize(psi->stream));
+    apply_operator(phi, psi->amps, op, false);
+    dot_async(phi, phi->amps, psi->amps, dloss); // loss = Re <phi|H phi>
+    if (gs) {
+        gs->open();
+        gs->finish();
+    } else {
+        sweep();
     }
 
     double2 hl;
@@ -236,22 +370,30 @@ GradientOut gradient_mixed(const vqb_op *ops, int64_t count, const vqb_pauli_ter
 
     DeviceState *phi = clone(dm0);
     StateGuard gphi{phi};
-    run_program(phi, mixed_forward_program(es, n), fused);
-
     DeviceState *psi = scratch(n, 1); // fully overwritten by identity_costate
     StateGuard gpsi{psi};
-    identity_costate(psi, op); // <<Psi| = <<I| H (autodiff.hpp:241-248)
-    VQB_CUDA(cudaStreamSynchronize(psi->stream));
-
     GradientOut out;
     out.grads.assign(total, 0.0);
     const size_t gbytes = sizeof(double2) * ((std::max<int64_t>(total, 1) + 1) / 2);
     DevBuf dbuf(gbytes + sizeof(double2));
     double *dgrads = dbuf.as<double>();
     double2 *dloss = reinterpret_cast<double2 *>(dbuf.as<char>() + gbytes);
+    auto sweep = [&] {
+        run_reverse(phi, psi, mixed_reverse_program(es, n, base, chan_inv, chan_adj), dgrads, fused);
+    };
+    std::unique_ptr<GatedSweep> gs;
+    if (total > 0 && parallel_adjoint()) gs = std::make_unique<GatedSweep>(sweep);
+    run_program(phi, mixed_forward_program(es, n), fused);
+    identity_costate(psi, op); // <<Psi| = <<I| H (autodiff.hpp:241-248)
+    VQB_CUDA(cudaStreamSynchronize(psi->stream));
     dot_async(phi, psi->amps, phi->amps, dloss); // loss = Re <<psi|phi>>
     if (total > 0) {
-        run_reverse(phi, psi, mixed_reverse_program(es, n, base, chan_inv, chan_adj), dgrads, fused);
+        if (gs) {
+            gs->open();
+            gs->finish();
+        } else {
+            sweep();
+        }
         VQB_CUDA(cudaMemcpyAsync(out.grads.data(), dgrads, sizeof(double) * total,
                                  cudaMemcpyDeviceToHost, phi->stream));
     }

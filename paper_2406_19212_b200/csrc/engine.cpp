@@ -277,6 +277,7 @@ void run_reverse(DeviceState *phi, DeviceState *psi, const std::vector<RevOp> &p
         }
         return;
     }
+    wait_issue_gate();
     for (const auto &r : prog) {
         if (r.dmats.empty()) {
             apply_gate_fast(phi->amps, phi->pn, r.phi_op, phi->stream);

@@ -40,6 +40,13 @@ std::vector<RevOp> mixed_reverse_program(const std::vector<Element> &es, int n,
                                          const std::vector<cvec> &chan_inv,
                                          const std::vector<cvec> &chan_adj);
 
+// Launch gate of the host-parallel adjoint: the reverse sweep is planned on
+// a worker thread while the calling thread launches the forward pass; the
+// worker's executors call wait_issue_gate() before their first device work,
+// which returns once the caller has enqueued everything that must precede
+// the sweep on the stream (no-op on threads without a gate).
+void wait_issue_gate();
+
 // Execute a forward program on s (asynchronous on s->stream).
 void run_program(DeviceState *s, const std::vector<Gate> &prog, bool fused);
 // Execute a reverse program on (phi, psi); gradients go to the device vector.

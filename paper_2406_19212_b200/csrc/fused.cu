@@ -835,6 +835,7 @@ void run_reverse_fused(DeviceState *phi, DeviceState *psi, const std::vector<Rev
     for (const auto &r : prog) fops.push_back(analyse_rev(r));
     const int k = tile_bits_for(phi->pn, true);
     const auto stages = plan_stages(fops, phi->pn, k);
+    wait_issue_gate();
     execute<true>(phi, psi, fops, stages, phi->pn, dgrads, [&](const FusedOp &f) {
         const RevOp &r = *f.rev;
         if (r.dmats.empty()) {

@@ -213,7 +213,8 @@ std::vector<const FusedOp *> fuse_blocks_ref(const std::vector<FusedOp> &ops, co
             continue;
         }
         // product of the candidates (disjoint supports, commuting), then op
-        std::sort(U, U + nu);
+        for (int i = 1; i < nu; ++i) // insertion sort (nu <= kMaxFuse)
+            for (int j = i; j > 0 && U[j - 1] > U[j]; --j) std::swap(U[j - 1], U[j]);
         const int du = 1 << nu;
         cplx acc_phi[kMaxFuseEnt], acc_psi[kMaxFuseEnt], tmp[kMaxFuseEnt];
         for (int i = 0; i < du * du; ++i) acc_phi[i] = cplx(0);

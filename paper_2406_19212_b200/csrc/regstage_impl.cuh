@@ -1706,7 +1706,7 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
     };
     static const int pair_p0[6] = {0, 0, 0, 1, 1, 2}, pair_p1[6] = {1, 2, 3, 2, 3, 3};
     const int jit_blocks = env_int("VQB_JIT_REV_BLOCKS", 4);
-    bool spool = false, wide2 = false;
+    bool spool = false;
     double fl = 0, wfl = 0; // FP64 flops per thread (register code) / per tile (wide ops)
     std::string body;
     auto emit = [&](const std::string &x) { body += x; };
@@ -1777,7 +1777,6 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
                 // phase multiplies one of 2^|rm| running products PH_rm[g];
                 // each element gets the product of its PH's at the end. Phi
                 // and Psi wait in thread-private shared-memory slots meanwhile.
-                wide2 = true;
                 auto rmask_of = [&](const ROp &o) {
                     int m = 0;
                     for (int q = 0; q < o.nc; ++q)
@@ -2026,7 +2025,6 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
         "        const __grid_constant__ JP P) {\n");
     // shared memory: xbuf (relayouts, Phi's wide ops) [| xbuf2 (Psi's wide
     // ops)] [| pool copy] | gradient reduction slots
-    (void)wide2;
     const int xt = 2; // xbuf (Phi) and xbuf2 (Psi)
     out("  extern __shared__ __align__(16) double2 sm[];\n  double2 *xbuf = sm;\n");
     out("  double2 *xbuf2 = sm + " + I(TS) + ";\n");
@@ -2215,6 +2213,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
     bool batching = false;
     std::vector<Action> pending;
     auto issue = [&](Action &act) {
+        if (REV) wait_issue_gate();
         if (act.fallback_op >= 0) {
             fallback(fops[act.fallback_op]);
             return;
@@ -2396,6 +2395,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
         }
     }
     if (REV && total_slots > 0) {
+        wait_issue_gate();
         if ((int)slots.scale.size() != total_slots) raise(VQB_ERR_INTERNAL, "gradient slot mismatch");
         m_slots.ensure((sizeof(double) + sizeof(long long)) * total_slots);
         VQB_CUDA(cudaMemcpyAsync(m_slots.p, slots.scale.data(), sizeof(double) * total_slots,
