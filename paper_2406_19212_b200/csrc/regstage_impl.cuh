@@ -1225,7 +1225,8 @@ struct WideState {
 // spread over the block's threads. Matrices come from the shared-memory pool
 // copy (*needs_spool).
 std::string jit_wide_op(const RParams &P, int sub, const ROp &op, const std::vector<WideState> &sts,
-                        const char *slot_base, double *wide_fl, bool *needs_spool, bool inplace = false) {
+                        const char *slot_base, double *wide_fl, bool *needs_spool, bool inplace = false,
+                        bool param_ok = false) {
     auto I = [](long long x) { return std::to_string(x); };
     const RLayout &L = P.subs[sub].L;
     const int NT = std::min(std::max(op.nt, 1), kMaxMix), D = 1 << NT;
@@ -1246,10 +1247,12 @@ std::string jit_wide_op(const RParams &P, int sub, const ROp &op, const std::vec
             if ((r >> q) & 1) o |= 1 << op.lb[q];
         sw_off[r] = swz(o);
     }
-    // matrices from the shared-memory pool copy: the parameter bank at literal
-    // offsets was measured slower here (the pool outgrows the constant cache)
-    const bool cond = true;
-    *needs_spool = true;
+    // conditioned matrices come from the shared-memory pool copy (run-time
+    // sub-matrix index); unconditioned ones may be parameter-bank operands at
+    // literal offsets (measured: faster in forward kernels, slower in adjoint
+    // kernels, whose larger pools outgrow the constant cache)
+    const bool cond = op.nc > 0 || !param_ok || !env_int("VQB_JIT_WIDE_PARAM", 1);
+    if (cond) *needs_spool = true;
     std::string e = "    {\n";
     if (!inplace) {
         for (const auto &st : sts)
@@ -1277,8 +1280,10 @@ std::string jit_wide_op(const RParams &P, int sub, const ROp &op, const std::vec
         }
         e += ";\n";
         if (st.ident) e += "        if ((" + std::to_string(st.ident) + "ull >> c) & 1) continue;\n";
-        e += cond ? "        const double2 *M = spool + " + I(st.mat) + " + c * " + I(op.nx * D) + ";\n"
-                  : "        const double2 *M = P.pool + " + I(st.mat) + ";\n";
+        if (cond) e += "        const double2 *M = spool + " + I(st.mat) + " + c * " + I(op.nx * D) + ";\n";
+        auto Mk = [&](int k) {
+            return cond ? "M[" + I(k) + "]" : "P.pool[" + I(st.mat + (unsigned)k) + "]";
+        };
         e += "        const int sb = swz(b);\n";
         // per-entry structure over every selectable sub-matrix (pool_cls)
         const int nsubm = 1 << op.nc;
@@ -1290,7 +1295,7 @@ std::string jit_wide_op(const RParams &P, int sub, const ROp &op, const std::vec
                 const int x = P.xpat[op.xoff + k];
                 const int c = pool_cls(P, st.mat + (unsigned)(k * D + r), nsubm, op.nx * D);
                 if (!c) continue;
-                e += cterm("M[" + I(k * D + r) + "]", std::string(st.buf) + "[sb ^ " + I(sw_off[r ^ x]) + "]",
+                e += cterm(Mk(k * D + r), std::string(st.buf) + "[sb ^ " + I(sw_off[r ^ x]) + "]",
                            "o" + I(r), c, first, fl);
                 first = false;
             }
@@ -1391,7 +1396,7 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
             if (op.nt >= 3) {
                 to_smem();
                 emit(jit_wide_op(P, sub, op, {{"v", "xbuf", op.mat, op.ident}}, ("st" + std::to_string(sub)).c_str(),
-                                 &wfl, &spool, true));
+                                 &wfl, &spool, true, true));
                 if (!lazy) to_regs(sub);
                 continue;
             }
@@ -2132,7 +2137,7 @@ std::string shape_key(const RParams &P, bool rev) {
             cls[(size_t)i >> 2] = (char)(cls[(size_t)i >> 2] | (pool_cls(P, (unsigned)i, 1, 0) << (2 * (i & 3))));
         key += cls;
     }
-    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY"}) {
+    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_JIT_WIDE_PARAM"}) {
         const char *v = std::getenv(e);
         key += '|';
         if (v) key += v;
