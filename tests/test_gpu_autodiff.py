@@ -259,3 +259,46 @@ def test_specialised_adjoint_matches_reference(dev, ref, monkeypatch, regs):
     loss, g = dev.gradient_mixed(w.observable, w.circuit, dev.mixed_state(7))
     rloss, rg = ref.gradient_mixed(w.observable, w.circuit, ref.mixed_state(7))
     assert abs(loss - rloss) <= RTOL * abs(rloss) and rel_err(g, rg) <= RTOL
+
+
+@pytest.mark.parametrize("variant", [{}, {"VQB_JIT_DIAGRUN": "0"}, {"VQB_JIT_ACC": "1000"},
+                                     {"VQB_JIT_LAZY": "0"}, {"VQB_PARALLEL_ADJOINT": "0"}])
+def test_structure_classes_and_generator_variants(dev, ref, monkeypatch, variant):
+    """Specialised kernels key on which matrix entries are exactly zero, real or
+    imaginary (structure-aware emission): angles that make entries vanish
+    (Rx(pi): zero real parts; Ry(pi): a zero diagonal; Rz(0): the identity)
+    must compile their own kernels and still match the reference, forward and
+    adjoint, in every generator variant (diagonal runs off, no accumulator
+    budget, eager relayouts, serial host planning)."""
+    monkeypatch.setenv("VQB_JIT", "1")
+    for k, v in variant.items():
+        monkeypatch.setenv(k, v)
+    n = 14
+    for angle in (0.7, math.pi, 0.0):
+        c = Circuit()
+        for q in range(1, n + 1):
+            c.push_back(standard_gate(GateKind.H, [q]))
+        for layer in range(2):
+            for q in range(1, n):
+                c.push_back(standard_gate(GateKind.Cnot, [q, q + 1]))
+                c.push_back(parametric_gate(GateKind.Rz, [q + 1], angle + 0.1 * layer, True))
+                c.push_back(standard_gate(GateKind.Cnot, [q, q + 1]))
+            for q in range(1, n + 1):
+                c.push_back(parametric_gate(GateKind.Rx, [q], angle, True))
+                c.push_back(parametric_gate(GateKind.Ry, [q], angle, True))
+        s = dev.pure_state(n)
+        dev.apply_circuit(c, s)
+        r = ref.pure_state(n)
+        ref.apply_circuit(c, r)
+        assert np.max(np.abs(dev.download(s) - ref.download(r))) <= 1e-12
+        op = sum_z(n)
+        loss, g = dev.gradient_pure(op, c, dev.pure_state(n))
+        rloss, rg = ref.gradient_pure(op, c, ref.pure_state(n))
+        # the loss and some gradients vanish at these angles: relative to
+        # max(|ref|, 1) (the observable's scale), i.e. 1e-10 absolute near zero
+        assert abs(loss - rloss) <= RTOL * max(abs(rloss), 1.0)
+        assert np.max(np.abs(g - rg)) <= RTOL * max(np.max(np.abs(rg)), 1.0)
+    w = circuits.config3(n=6, layers=1)
+    loss, g = dev.gradient_mixed(w.observable, w.circuit, dev.mixed_state(6))
+    rloss, rg = ref.gradient_mixed(w.observable, w.circuit, ref.mixed_state(6))
+    assert abs(loss - rloss) <= RTOL * abs(rloss) and rel_err(g, rg) <= RTOL
