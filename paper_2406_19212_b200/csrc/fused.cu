@@ -782,9 +782,14 @@ std::string debug_jit_source(int regs, const void *params, size_t nbytes, bool r
 namespace {
 // register-executor geometry: VQB_REGS / VQB_REV_REGS = 8 or 16 amplitudes per
 // thread (defaults: 16 for forward programs, 8 for adjoint sweeps)
-bool use_rs8(bool rev) {
+bool use_rs8(bool rev, const DeviceState *s = nullptr) {
     const char *v = std::getenv(rev ? "VQB_REV_REGS" : "VQB_REGS");
     if (v && *v) return std::atoi(v) == 8;
+    // density-matrix sweeps take 16 registers per state: their 4-bit channel
+    // superoperators then run on register bits (ROp::inreg), no shared-memory
+    // round trips; pure-state sweeps keep 8 (lighter, 4 blocks per SM)
+    if (rev && s && s->mixed && std::getenv("VQB_WIDE_REGS") == nullptr) return false;
+    if (rev && s && s->mixed) return std::atoi(std::getenv("VQB_WIDE_REGS")) == 0;
     return rev;
 }
 bool smem_forced() {
@@ -824,8 +829,9 @@ void run_program_fused(DeviceState *s, const std::vector<Gate> &prog) {
 void run_reverse_fused(DeviceState *phi, DeviceState *psi, const std::vector<RevOp> &prog,
                        double *dgrads) {
     if (!smem_forced()) {
-        if (use_rs8(true) ? rs8::regstage_available(phi->pn) : rs16::regstage_available(phi->pn)) {
-            if (use_rs8(true)) rs8::run_reverse_reg(phi, psi, prog, dgrads);
+        const bool r8 = use_rs8(true, phi);
+        if (r8 ? rs8::regstage_available(phi->pn) : rs16::regstage_available(phi->pn)) {
+            if (r8) rs8::run_reverse_reg(phi, psi, prog, dgrads);
             else rs16::run_reverse_reg(phi, psi, prog, dgrads);
             return;
         }

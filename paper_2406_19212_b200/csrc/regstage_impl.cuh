@@ -80,7 +80,7 @@ constexpr int B3 = RB > 3 ? 3 : 0;
 constexpr int kMaxSubs = 32;
 constexpr int kMaxOps = 56;
 constexpr int kMaxSlots = 64;
-constexpr int kMaxPool = 1088; // double2 entries
+constexpr int kMaxPool = 1072; // double2 entries
 constexpr int kMaxTab = 192;   // per-element diagonal tables, copied to shared memory
 
 struct RLayout {
@@ -107,6 +107,10 @@ struct ROp {
     // e_p[c] = D_p[c] * M[c] at pool offset mat_e
     int unit;
     unsigned mat_e;
+    // nt >= 3 operation whose mixing bits are all register bits (specialised
+    // kernels only): lb[q] is then the register bit of matrix bit q and the
+    // XOR-term pool is applied in registers, no shared-memory round trip
+    int inreg;
 };
 
 struct RSub {
@@ -813,7 +817,8 @@ struct SlotMap {
 // `remaining` (block indices, in a valid order) is consumed; what is left
 // must run in a following launch with the same tile bits.
 void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks,
-                     std::vector<int> &remaining, int pn, bool rev, RParams &P, SlotMap &slots) {
+                     std::vector<int> &remaining, int pn, bool rev, RParams &P, SlotMap &slots,
+                     bool regwide = false) {
     std::memset(&P, 0, sizeof P);
     for (int j = 0; j < K; ++j) P.bits[j] = sg.bits[j];
     P.ntiles = 1ull << (pn - K);
@@ -825,9 +830,10 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
     };
     // register bits an op needs: its mixing bits (wide ops run through the
     // shared-memory tile on any local bits and need none)
+    auto wide_in_regs = [&](const FusedOp &f) { return regwide && f.nt >= 3 && f.nt <= RB; };
     auto mixmask = [&](const FusedOp &f) {
         unsigned mix = 0;
-        if (f.nt >= 3) return mix;
+        if (f.nt >= 3 && !wide_in_regs(f)) return mix;
         for (int q = 0; q < f.nt; ++q) mix |= 1u << local_of(f.mix[q]);
         return mix;
     };
@@ -918,6 +924,9 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
                 if (f.nt == 2 && rp[1] < rp[0]) std::swap(order[0], order[1]);
                 if (f.nt == 1) o.code = rp[0];
                 if (f.nt == 2) o.code = pair_code(rp[order[0]], rp[order[1]]);
+            } else if (wide_in_regs(f)) {
+                o.inreg = 1;
+                for (int q = 0; q < f.nt; ++q) o.lb[q] = reg_of(local_of(f.mix[q]));
             } else {
                 for (int q = 0; q < f.nt; ++q) o.lb[q] = local_of(f.mix[q]);
             }
@@ -1316,6 +1325,64 @@ std::string jit_wide_op(const RParams &P, int sub, const ROp &op, const std::vec
     return e;
 }
 
+// A wide operation on register bits (ROp::inreg): out[r] = sum_k d_k[r]
+// v[r ^ x_k] per group of registers, XOR-term pool, register conditions
+// resolved per group, run-time ones (cd) select the sub-matrix. `mexpr(off)`
+// gives a pool entry expression at a literal offset (static sub-matrix) and
+// `dyn` is the run-time condition-index expression ("" if none).
+template <typename MExpr>
+std::string jit_wide_regs(const RParams &P, const ROp &op, const char *v, unsigned mat, unsigned long long ident,
+                          const std::string &dyn, MExpr mexpr, double &fl) {
+    auto I = [](long long x) { return std::to_string(x); };
+    const int NT = op.nt, D = 1 << NT, stride = op.nx * D;
+    int rmask = 0;
+    for (int q = 0; q < NT; ++q) rmask |= 1 << op.lb[q];
+    auto regidx = [&](int i0, int r) {
+        int x = i0;
+        for (int q = 0; q < NT; ++q)
+            if ((r >> q) & 1) x |= 1 << op.lb[q];
+        return x;
+    };
+    std::string e;
+    for (int i0 = 0; i0 < R; ++i0) {
+        if (i0 & rmask) continue;
+        int cs = 0, rq = 0;
+        for (int q = 0; q < op.nc; ++q) {
+            if (op.ck[q] == 2) {
+                rq |= 1 << q;
+                if ((i0 >> op.cp[q]) & 1) cs |= 1 << q;
+            }
+        }
+        if (dyn.empty() && ((ident >> cs) & 1)) continue;
+        e += "      {\n";
+        if (!dyn.empty())
+            e += "        const int cw = " + dyn + " | " + I(cs) + ";\n        if (!((" + std::to_string(ident) +
+                 "ull >> cw) & 1)) {\n";
+        for (int r = 0; r < D; ++r) e += "        const double2 x" + I(r) + " = " + v + "[" + I(regidx(i0, r)) + "];\n";
+        for (int r = 0; r < D; ++r) {
+            bool first = true;
+            e += "        double2 o" + I(r) + ";\n";
+            for (int k = 0; k < op.nx; ++k) {
+                const int x = P.xpat[op.xoff + k];
+                int c = 0;
+                for (int cc = 0; cc < (1 << op.nc); ++cc)
+                    if (dyn.empty() ? cc == cs : (cc & rq) == cs)
+                        c |= pool_cls(P, mat + (unsigned)(cc * stride + k * D + r), 1, 0);
+                if (!c) continue;
+                const std::string m = dyn.empty() ? mexpr(mat + (unsigned)(cs * stride + k * D + r))
+                                                  : "spool[" + I(mat + (unsigned)(k * D + r)) + " + cw * " + I(stride) + "]";
+                e += cterm(m, "x" + I(r ^ x), "o" + I(r), c, first, fl);
+                first = false;
+            }
+            if (first) e += "        o" + I(r) + " = make_double2(0.0, 0.0);\n";
+        }
+        for (int r = 0; r < D; ++r) e += "        " + std::string(v) + "[" + I(regidx(i0, r)) + "] = o" + I(r) + ";\n";
+        if (!dyn.empty()) e += "        }\n";
+        e += "      }\n";
+    }
+    return e;
+}
+
 std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *per_block, double *flops);
 // Source of a kernel equivalent to k_regstage<false, false> on one lowered
 // stage program, with every structural quantity a literal: tile bits, layouts
@@ -1393,6 +1460,23 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
         if (!lazy) to_regs(sub);
         for (int k = 0; k < sb.op_count; ++k) {
             const ROp &op = P.ops[sb.op_begin + k];
+            if (op.nt >= 3 && op.inreg) {
+                to_regs(sub);
+                std::string dyn;
+                for (int q = 0; q < op.nc; ++q) {
+                    if (op.ck[q] == 0)
+                        dyn += " | (int)(((base >> " + std::to_string(op.cp[q]) + ") & 1) << " + std::to_string(q) + ")";
+                    else if (op.ck[q] == 1)
+                        dyn += " | (((t >> " + std::to_string(op.cp[q]) + ") & 1) << " + std::to_string(q) + ")";
+                }
+                if (!dyn.empty()) {
+                    dyn = "(0" + dyn + ")";
+                    spool = true;
+                }
+                emit(jit_wide_regs(P, op, "v", op.mat, op.ident, dyn,
+                                   [&](unsigned off) { return MP + "[" + std::to_string(off) + "]"; }, fl));
+                continue;
+            }
             if (op.nt >= 3) {
                 to_smem();
                 emit(jit_wide_op(P, sub, op, {{"v", "xbuf", op.mat, op.ident}}, ("st" + std::to_string(sub)).c_str(),
@@ -1710,7 +1794,7 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
         return c;
     };
     static const int pair_p0[6] = {0, 0, 0, 1, 1, 2}, pair_p1[6] = {1, 2, 3, 2, 3, 3};
-    const int jit_blocks = env_int("VQB_JIT_REV_BLOCKS", 4);
+    const int jit_blocks = env_int("VQB_JIT_REV_BLOCKS", R >= 16 ? 2 : 4);
     bool spool = false;
     double fl = 0, wfl = 0; // FP64 flops per thread (register code) / per tile (wide ops)
     std::string body;
@@ -1763,7 +1847,7 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
         const RSub &sb = P.subs[sub];
         if (!lazy) to_regs(sub);
         for (int k = 0; k < sb.op_count; ++k) {
-            if (P.ops[sb.op_begin + k].nt < 3) to_regs(sub);
+            if (P.ops[sb.op_begin + k].nt < 3 || P.ops[sb.op_begin + k].inreg) to_regs(sub);
             const ROp &op = P.ops[sb.op_begin + k];
             // a run of unit-modulus diagonal steps: conj(psi) phi is invariant
             // along it, so every contribution is Re(z e_p) with z taken once,
@@ -1919,6 +2003,24 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
                 // other threads' later relayout / wide-op writes reuse these slots
                 emit("      __syncthreads();\n    }\n");
                 k = run_end - 1;
+                continue;
+            }
+            if (op.nt >= 3 && op.inreg) {
+                std::string dyn;
+                for (int q = 0; q < op.nc; ++q) {
+                    if (op.ck[q] == 0)
+                        dyn += " | (int)(((base >> " + I(op.cp[q]) + ") & 1) << " + I(q) + ")";
+                    else if (op.ck[q] == 1)
+                        dyn += " | (((to >> " + I(op.cp[q]) + ") & 1) << " + I(q) + ")";
+                }
+                if (!dyn.empty()) {
+                    dyn = "(0" + dyn + ")";
+                    spool = true;
+                }
+                auto pe = [&](unsigned off) { return "P.pool[" + I(off) + "]"; };
+                emit(jit_wide_regs(P, op, "vf", op.mat, op.ident, dyn, pe, fl));
+                emit(jit_wide_regs(P, op, "vg", op.pair ? op.mat_psi : op.mat, op.pair ? op.ident_psi : op.ident,
+                                   dyn, pe, fl));
                 continue;
             }
             if (op.nt >= 3) {
@@ -2137,7 +2239,7 @@ std::string shape_key(const RParams &P, bool rev) {
             cls[(size_t)i >> 2] = (char)(cls[(size_t)i >> 2] | (pool_cls(P, (unsigned)i, 1, 0) << (2 * (i & 3))));
         key += cls;
     }
-    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_JIT_WIDE_PARAM"}) {
+    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_JIT_WIDE_PARAM", "VQB_WIDE_REGS"}) {
         const char *v = std::getenv(e);
         key += '|';
         if (v) key += v;
@@ -2210,6 +2312,9 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
     static thread_local DevMem m_jpartial, m_slotsum;
     const size_t jpartial_bytes = sizeof(double) * (size_t)kMaxSlots * ntiles;
     const bool use_jit = jit::enabled(pn) && (!REV || jpartial_bytes <= (size_t(1) << 30));
+    // wide operations on register bits need the specialised kernels (the
+    // interpreter runs them through shared memory only)
+    const bool regwide = use_jit && RB >= 4 && env_int("VQB_WIDE_REGS", 1) != 0;
     if (REV && total_slots > 0) {
         m_slotsum.ensure(sizeof(double) * total_slots);
         VQB_CUDA(cudaMemsetAsync(m_slotsum.p, 0, sizeof(double) * total_slots, st));
@@ -2224,6 +2329,14 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             return;
         }
         RParams &P = *act.P;
+        if (!(act.jit && act.jit->k.e)) {
+            int nops = 0;
+            for (int i = 0; i < P.nsubs; ++i) nops = std::max(nops, P.subs[i].op_begin + P.subs[i].op_count);
+            for (int i = 0; i < nops; ++i)
+                if (P.ops[i].inreg)
+                    raise(VQB_ERR_INTERNAL, "stage program with register-resident wide operations has no "
+                                            "specialised kernel (set VQB_WIDE_REGS=0)");
+        }
         note_flops((act.jit && act.jit->k.e ? act.jit->flops_per_amp : act.dense_flops_per_amp) *
                    double(1ull << pn));
         const ProfMark pf_ = prof_begin(st);
@@ -2303,7 +2416,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             RParams &P = *act.P;
             {
                 HostAcc ha(&t_lower);
-                lower_stage_reg(sg, blocks, remaining, pn, REV, P, slots);
+                lower_stage_reg(sg, blocks, remaining, pn, REV, P, slots, regwide);
             }
             P.partial_ld = total_slots;
             if (stats) {
