@@ -714,7 +714,71 @@ __global__ void __launch_bounds__(kThreads) k_apply_operator(const double2 *__re
     }
 }
 
+// H|psi> for a diagonal operator with real coefficients (every term a Z
+// string: one group, x mask 0), e.g. the QAOA cost Hamiltonian: each thread
+// takes the 8 amplitudes b0 | i << 5 (i < 8; a warp's lanes cover bits 0-4, so
+// every load is coalesced), so a term's sign is the parity of (b0 & z) flipped
+// by the parity of (i & (z >> 5) & 7); terms that miss bits 5-7 add the same
+// signed coefficient to all 8 (one scalar), the others flip the sign bit of c
+// per element (integer ops, then one DADD). Same sums as group_weight up to
+// the summation order.
+__global__ void __launch_bounds__(kThreads) k_apply_zdiag(const double2 *__restrict__ a, double2 *__restrict__ out,
+                                                          uint64_t size, const PauliTermDev *__restrict__ terms_g,
+                                                          int nterms) {
+    extern __shared__ __align__(16) unsigned char zsm[];
+    auto *zm = reinterpret_cast<unsigned long long *>(zsm);
+    auto *cf = reinterpret_cast<double *>(zsm + sizeof(unsigned long long) * (size_t)nterms);
+    for (int i = threadIdx.x; i < nterms; i += blockDim.x) {
+        zm[i] = terms_g[i].zmask;
+        cf[i] = terms_g[i].coeff.x;
+    }
+    __syncthreads();
+    // byte lz of kPar: bit i = parity(i & lz)
+    constexpr unsigned long long kPar = 0x963C5AF066CCAA00ull;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < (size >> 3); j += stride) {
+        const uint64_t b0 = ((j >> 5) << 8) | (j & 31);
+        double w[8], wc = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) w[i] = 0.0;
+        for (int t = 0; t < nterms; ++t) {
+            const unsigned long long z = zm[t];
+            const double c = cf[t];
+            const int base = __popcll(b0 & z) & 1;
+            const int lz = (int)((z >> 5) & 7);
+            if (lz == 0) {
+                wc += base ? -c : c;
+                continue;
+            }
+            const unsigned pm = ((unsigned)(kPar >> (8 * lz)) & 0xFFu) ^ (base ? 0xFFu : 0u);
+            const int hi = __double2hiint(c), lo = __double2loint(c);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                w[i] += __hiloint2double(hi ^ (int)(((pm >> i) & 1u) << 31), lo);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const double2 v = a[b0 | ((uint64_t)i << 5)];
+            const double wi = w[i] + wc;
+            out[b0 | ((uint64_t)i << 5)] = make_double2(wi * v.x, wi * v.y);
+        }
+    }
+}
+
 void apply_operator(DeviceState *src, double2 *dst, const PauliPack &p, bool) {
+    bool zdiag = p.groups.size() == 1 && p.groups[0].xmask == 0 && src->size >= 256 &&
+                 p.terms.size() * 16 <= 40 * 1024;
+    for (const auto &t : p.terms) zdiag = zdiag && t.coeff.y == 0.0;
+    if (zdiag) {
+        upload_operator(src, p);
+        auto *terms = reinterpret_cast<const PauliTermDev *>(reinterpret_cast<const char *>(src->ws.terms) +
+                                                             sizeof(PauliGroupDev) * p.groups.size());
+        const ProfMark pf_ = prof_begin(src->stream);
+        k_apply_zdiag<<<grid_for(src->size >> 3), kThreads, 16 * p.terms.size(), src->stream>>>(
+            src->amps, dst, src->size, terms, (int)p.terms.size());
+        check_launch("k_apply_zdiag", pf_);
+        return;
+    }
     upload_operator(src, p);
     auto *groups = reinterpret_cast<const PauliGroupDev *>(src->ws.terms);
     auto *terms = reinterpret_cast<const PauliTermDev *>(

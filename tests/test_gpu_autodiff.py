@@ -76,6 +76,25 @@ def test_apply_operator(dev, ref):
         assert abs(np.vdot(amps, got) - dev.expectation(op, dev.from_amplitudes(amps))) <= 1e-10
 
 
+@pytest.mark.parametrize("n", [8, 14, 18])
+def test_apply_operator_z_diagonal(dev, ref, n):
+    """The Z-diagonal fast path of apply_operator (one Z-string group with real
+    coefficients: QAOA cost Hamiltonians, sums of Z): identity term, strings
+    on low, middle (bits 5-7) and high qubits, against the reference."""
+    rng = np.random.default_rng(n)
+    amps = random_state(n, rng)
+    terms = [PauliTerm([], 0.5)]
+    for _ in range(30):
+        k = int(rng.integers(1, 4))
+        qs = sorted(set(int(q) + 1 for q in rng.choice(n, size=k, replace=False)))
+        terms.append(PauliTerm([(q, "z") for q in qs], float(rng.standard_normal())))
+    ops = [PauliOperator(terms), circuits.config2(n=n, p=1).observable, sum_z(n)]
+    for op in ops:
+        got = dev.download(dev.apply_operator(op, dev.from_amplitudes(amps)))
+        want = ref.download(ref.apply_operator(op, ref.from_amplitudes(amps)))
+        assert np.max(np.abs(got - want)) <= 1e-12
+
+
 @pytest.mark.parametrize("theta", [0.0, 0.3, math.pi / 2, 1.9])
 def test_rotated_qubit_gradient(dev, theta):
     # tests/test_autodiff.cpp:49-85
