@@ -818,7 +818,7 @@ struct SlotMap {
 // must run in a following launch with the same tile bits.
 void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks,
                      std::vector<int> &remaining, int pn, bool rev, RParams &P, SlotMap &slots,
-                     bool regwide = false) {
+                     bool regwide = false, bool gdiff = false) {
     std::memset(&P, 0, sizeof P);
     for (int j = 0; j < K; ++j) P.bits[j] = sg.bits[j];
     P.ntiles = 1ull << (pn - K);
@@ -1019,7 +1019,40 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
             }
             if (o.np > 0) {
                 o.mat_d = (unsigned)npool;
-                for (int p = 0; p < f.np; ++p) push(f.sub_d, size_t(p) << f.nc, nullptr);
+                // Derivative generators: the contribution Re<psi|D_p inv phi>
+                // can be taken before the update with G_p = D_p inv; for
+                // rotations G_p is a scaled Pauli (dRx inv = -i X / 2), for
+                // superoperator steps a diagonal -- much sparser than D_p.
+                // Store whichever has fewer nonzero real/imaginary parts
+                // (ROp::unit bit 1 marks G; specialised kernels only).
+                bool use_g = false;
+                cvec G;
+                if (gdiff && f.nt >= 1 && f.nt <= 2 && !f.pair) {
+                    const int nsubm = 1 << f.nc;
+                    G.assign(f.sub_d.size(), cplx(0));
+                    auto weight = [](const cplx &x) { return (x.real() != 0.0) + (x.imag() != 0.0); };
+                    int wd = 0, wg = 0;
+                    for (int p = 0; p < f.np; ++p)
+                        for (int c = 0; c < nsubm; ++c) {
+                            const cplx *Dm = f.sub_d.data() + ((size_t(p) << f.nc) + c) * dd;
+                            const cplx *U = f.sub_phi.data() + size_t(c) * dd;
+                            cplx *Gm = G.data() + ((size_t(p) << f.nc) + c) * dd;
+                            for (int col = 0; col < D; ++col)
+                                for (int row = 0; row < D; ++row) {
+                                    cplx acc = 0;
+                                    for (int k2 = 0; k2 < D; ++k2) acc += Dm[row + k2 * D] * U[k2 + col * D];
+                                    // entries at rounding level of an exact zero are zero
+                                    if (std::abs(acc.real()) < 1e-15 * 4) acc.real(0.0);
+                                    if (std::abs(acc.imag()) < 1e-15 * 4) acc.imag(0.0);
+                                    Gm[row + col * D] = acc;
+                                    wg += weight(acc);
+                                    wd += weight(Dm[row + col * D]);
+                                }
+                        }
+                    use_g = wg < wd;
+                }
+                if (use_g) o.unit |= 2;
+                for (int p = 0; p < f.np; ++p) push(use_g ? G : f.sub_d, size_t(p) << f.nc, nullptr);
                 if (f.nt == 0) {
                     o.mat_e = (unsigned)npool;
                     for (int p = 0; p < f.np; ++p)
@@ -1854,7 +1887,7 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
             // and both states get the product of the phases at the end
             int run_end = k;
             while (run_end < sb.op_count && P.ops[sb.op_begin + run_end].nt == 0 &&
-                   P.ops[sb.op_begin + run_end].unit && !P.ops[sb.op_begin + run_end].pair)
+                   (P.ops[sb.op_begin + run_end].unit & 1) && !P.ops[sb.op_begin + run_end].pair)
                 ++run_end;
             if (run_end - k >= 2 && env_int("VQB_JIT_DIAGRUN", 1)) {
                 // Step-major, factored by register conditions. A step's
@@ -2107,11 +2140,13 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
                     const int cs = cstat(i);
                     int idx[4];
                     group_idx(op.nt, op.code, i, idx);
-                    emit(mv_code("vf", idx, D, mexpr(op.mat, cs), mcls(op.mat, cs), fl));
+                    const bool gpre = (op.unit & 2) != 0; // G_p = D_p inv on the old Phi
+                    if (!gpre) emit(mv_code("vf", idx, D, mexpr(op.mat, cs), mcls(op.mat, cs), fl));
                     for (int p = 0; p < op.np; ++p) {
                         const unsigned dof = op.mat_d + (unsigned)(p * nsub * dd);
                         emit(dot_code("acc_s" + I(op.slot + p), idx, D, mexpr(dof, cs), mcls(dof, cs), fl));
                     }
+                    if (gpre) emit(mv_code("vf", idx, D, mexpr(op.mat, cs), mcls(op.mat, cs), fl));
                     emit(mv_code("vg", idx, D, mexpr(op.mat, cs), mcls(op.mat, cs), fl));
                 }
                 for (int p = 0; p < op.np; ++p) open_slots.push_back(op.slot + p);
@@ -2239,7 +2274,7 @@ std::string shape_key(const RParams &P, bool rev) {
             cls[(size_t)i >> 2] = (char)(cls[(size_t)i >> 2] | (pool_cls(P, (unsigned)i, 1, 0) << (2 * (i & 3))));
         key += cls;
     }
-    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_JIT_WIDE_PARAM", "VQB_WIDE_REGS"}) {
+    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_JIT_WIDE_PARAM", "VQB_WIDE_REGS", "VQB_JIT_GDIFF"}) {
         const char *v = std::getenv(e);
         key += '|';
         if (v) key += v;
@@ -2333,7 +2368,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             int nops = 0;
             for (int i = 0; i < P.nsubs; ++i) nops = std::max(nops, P.subs[i].op_begin + P.subs[i].op_count);
             for (int i = 0; i < nops; ++i)
-                if (P.ops[i].inreg)
+                if (P.ops[i].inreg || (P.ops[i].nt > 0 && (P.ops[i].unit & 2)))
                     raise(VQB_ERR_INTERNAL, "stage program with register-resident wide operations has no "
                                             "specialised kernel (set VQB_WIDE_REGS=0)");
         }
@@ -2416,7 +2451,8 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             RParams &P = *act.P;
             {
                 HostAcc ha(&t_lower);
-                lower_stage_reg(sg, blocks, remaining, pn, REV, P, slots, regwide);
+                lower_stage_reg(sg, blocks, remaining, pn, REV, P, slots, regwide,
+                                use_jit && env_int("VQB_JIT_GDIFF", 1) != 0);
             }
             P.partial_ld = total_slots;
             if (stats) {
