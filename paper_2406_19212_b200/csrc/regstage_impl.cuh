@@ -1837,9 +1837,47 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
     // slots are pending, so the reduction overlaps the following steps and at
     // most acc_budget accumulators hold registers (dozens of slots per launch
     // would otherwise spill).
-    const int acc_budget = env_int("VQB_JIT_ACC", 6);
+    // Reductions go in batches of 8 slots through a warp transpose-reduce
+    // (9 double shuffles for 8 slots instead of 40; lane l ends with slot
+    // (l >> 2) & 7); VQB_JIT_ACCBATCH=0 reduces slot by slot.
+    const bool acc_batch = env_int("VQB_JIT_ACCBATCH", 0) != 0; // measured: no gain (QAOA), spills (rs16)
+    const int acc_budget = env_int("VQB_JIT_ACC", acc_batch ? 8 : 6);
     std::vector<int> open_slots;
+    auto flush_batch = [&](const std::vector<int> &sl) {
+        std::string e = "    {\n      double a0";
+        for (int k = 1; k < 8; ++k) e += ", a" + I(k);
+        e += ";\n";
+        for (int k = 0; k < 8; ++k)
+            e += "      a" + I(k) + " = " + (k < (int)sl.size() ? "acc_s" + I(sl[k]) : std::string("0.0")) + ";\n";
+        e += "      const bool h4 = lane & 16, h3 = lane & 8, h2 = lane & 4;\n";
+        for (int k = 0; k < 4; ++k)
+            e += "      const double b" + I(k) + " = (h4 ? a" + I(k + 4) + " : a" + I(k) +
+                 ") + __shfl_xor_sync(0xffffffffu, h4 ? a" + I(k) + " : a" + I(k + 4) + ", 16);\n";
+        for (int k = 0; k < 2; ++k)
+            e += "      const double c" + I(k) + " = (h3 ? b" + I(k + 2) + " : b" + I(k) +
+                 ") + __shfl_xor_sync(0xffffffffu, h3 ? b" + I(k) + " : b" + I(k + 2) + ", 8);\n";
+        e += "      double d = (h2 ? c1 : c0) + __shfl_xor_sync(0xffffffffu, h2 ? c0 : c1, 4);\n";
+        e += "      d += __shfl_xor_sync(0xffffffffu, d, 2);\n      d += __shfl_xor_sync(0xffffffffu, d, 1);\n";
+        // slot index per lane group
+        e += "      const int q = (lane >> 2) & 7;\n      if ((lane & 3) == 0) {\n";
+        for (int k = 0; k < (int)sl.size(); ++k)
+            e += "        if (q == " + I(k) + ") red[" + I(sl[k] * NW) + " + warp] = d;\n";
+        e += "      }\n    }\n";
+        emit(e);
+    };
     auto flush_slots = [&](int keep) {
+        if (acc_batch) {
+            while ((int)open_slots.size() >= 8 && (int)open_slots.size() > keep) {
+                std::vector<int> b(open_slots.begin(), open_slots.begin() + 8);
+                open_slots.erase(open_slots.begin(), open_slots.begin() + 8);
+                flush_batch(b);
+            }
+            if (keep == 0 && !open_slots.empty()) {
+                flush_batch(open_slots);
+                open_slots.clear();
+            }
+            return;
+        }
         while ((int)open_slots.size() > keep) {
             const int sl = open_slots.front();
             open_slots.erase(open_slots.begin());
@@ -1916,10 +1954,15 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
                     const int m = rmask_of(P.ops[sb.op_begin + j]);
                     if (std::find(masks.begin(), masks.end(), m) == masks.end()) masks.push_back(m);
                 }
+                // Phi and Psi stay in registers through the run (VQB_JIT_STASH=1
+                // parks them in shared memory: measured slower since the class
+                // sums replaced per-element z and phase registers)
+                const bool stash = env_int("VQB_JIT_STASH", 0) != 0;
                 emit("    {\n");
-                for (int i = 0; i < R; ++i)
-                    emit("      xbuf[" + I(i * T) + " + t] = vf[" + I(i) + "]; xbuf2[" + I(i * T) + " + t] = vg[" + I(i) +
-                         "];\n");
+                if (stash)
+                    for (int i = 0; i < R; ++i)
+                        emit("      xbuf[" + I(i * T) + " + t] = vf[" + I(i) + "]; xbuf2[" + I(i * T) + " + t] = vg[" +
+                             I(i) + "];\n");
                 emit("      double2 z[" + I(R) + "];\n");
                 for (int i = 0; i < R; ++i)
                     emit("      z[" + I(i) + "] = make_double2(fma(vg[" + I(i) + "].x, vf[" + I(i) + "].x, vg[" + I(i) +
@@ -2024,17 +2067,18 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
                             fl += 6;
                         }
                     }
+                    const std::string sf = stash ? "xbuf[" + I(i * T) + " + t]" : "vf[" + I(i) + "]";
+                    const std::string sg = stash ? "xbuf2[" + I(i * T) + " + t]" : "vg[" + I(i) + "]";
                     if (ph.empty()) {
-                        emit("      vf[" + I(i) + "] = xbuf[" + I(i * T) + " + t]; vg[" + I(i) + "] = xbuf2[" + I(i * T) +
-                             " + t];\n");
+                        if (stash) emit("      vf[" + I(i) + "] = " + sf + "; vg[" + I(i) + "] = " + sg + ";\n");
                         continue;
                     }
-                    emit("      { const double2 ph = " + ph + "; vf[" + I(i) + "] = cmul(ph, xbuf[" + I(i * T) +
-                         " + t]); vg[" + I(i) + "] = cmul(ph, xbuf2[" + I(i * T) + " + t]); }\n");
+                    emit("      { const double2 ph = " + ph + "; vf[" + I(i) + "] = cmul(ph, " + sf + "); vg[" + I(i) +
+                         "] = cmul(ph, " + sg + "); }\n");
                     fl += 12;
                 }
                 // other threads' later relayout / wide-op writes reuse these slots
-                emit("      __syncthreads();\n    }\n");
+                emit(stash ? "      __syncthreads();\n    }\n" : "    }\n");
                 k = run_end - 1;
                 continue;
             }
@@ -2274,7 +2318,7 @@ std::string shape_key(const RParams &P, bool rev) {
             cls[(size_t)i >> 2] = (char)(cls[(size_t)i >> 2] | (pool_cls(P, (unsigned)i, 1, 0) << (2 * (i & 3))));
         key += cls;
     }
-    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_JIT_WIDE_PARAM", "VQB_WIDE_REGS", "VQB_JIT_GDIFF"}) {
+    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_JIT_WIDE_PARAM", "VQB_WIDE_REGS", "VQB_JIT_GDIFF", "VQB_JIT_ACCBATCH", "VQB_JIT_STASH"}) {
         const char *v = std::getenv(e);
         key += '|';
         if (v) key += v;
