@@ -491,7 +491,8 @@ def main():
     f0 = eng.flop_count()
     eng.profile_begin()
     step()
-    prof = eng.profile_end()
+    launch_recs = []
+    prof = eng.profile_end(launch_recs)
     step_flops = eng.flop_count() - f0
     peak, peak_kind = hbm_peak()
     roof = None
@@ -538,6 +539,25 @@ def main():
                 pass
             # which ceiling the stage kernels sit closer to
             roof["limiter"] = "fp64" if roof["fp64"]["frac"] > roof["frac"] else "hbm"
+        if launch_recs:
+            # per launch, the binding roofline is the larger of its HBM time
+            # (algorithmic bytes / measured copy peak) and its FP64 time
+            # (executed flops / measured DFMA peak); the stage kernels' time
+            # against the sum of those floors
+            try:
+                with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+                    dfma = float(json.load(f)["dfma_tflops"])
+            except Exception:
+                dfma = 148 * 64 * 2 * 1.965e9 / 1e12
+            t_meas = sum(r[1] for r in launch_recs) / 1e3
+            t_floor = sum(max(r[3] / (peak * 1e9), r[2] / (dfma * 1e12)) for r in launch_recs)
+            n_hbm = sum(1 for r in launch_recs if r[3] / (peak * 1e9) >= r[2] / (dfma * 1e12))
+            roof["per_launch_bound"] = {
+                "frac": t_floor / t_meas if t_meas else None, "floor_ms": 1e3 * t_floor,
+                "measured_ms": 1e3 * t_meas, "launches": len(launch_recs), "hbm_bound_launches": n_hbm,
+                "fp64_peak_tflops": dfma,
+                "what": "sum over stage launches of max(bytes / HBM peak, executed flops / measured DFMA peak) "
+                        "divided by their measured time"}
     algo_gbs = wl.algorithmic_bytes(world) / (ms_per_step / 1e3) / 1e9
 
     # end to end through the C-ABI with host buffers

@@ -78,4 +78,5 @@ struct ProfMark {
 };
 ProfMark prof_begin(cudaStream_t st);
 void check_launch(const char *what, const ProfMark &m);
+void prof_annotate(const ProfMark &m, double flops, double bytes);
 } // namespace vqb

@@ -25,6 +25,7 @@ std::mutex g_mu;
 struct Rec {
     const char *name = nullptr;
     cudaEvent_t a = nullptr, b = nullptr;
+    double flops = 0, bytes = 0; // algorithmic FP64 flops / HBM bytes, if annotated
 };
 std::vector<Rec> g_recs;
 std::vector<cudaEvent_t> g_pool;
@@ -80,6 +81,14 @@ void check_launch(const char *what, const ProfMark &m) {
     }
 }
 
+// Attach the launch's FP64 flops and HBM bytes (per-launch roofline).
+void prof_annotate(const ProfMark &m, double flops, double bytes) {
+    if (m.slot < 0) return;
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_recs[m.slot].flops = flops;
+    g_recs[m.slot].bytes = bytes;
+}
+
 // Starts a profiling window (clears earlier records).
 void prof_start() {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -109,6 +118,14 @@ std::string prof_stop() {
     char buf[256];
     for (auto &[k, v] : agg) {
         std::snprintf(buf, sizeof buf, "%s %ld %.6f\n", k.c_str(), v.first, v.second);
+        out += buf;
+    }
+    // annotated launches, one line each: "#L name ms flops bytes"
+    for (auto &r : g_recs) {
+        if (!r.name || (r.flops == 0 && r.bytes == 0)) continue;
+        float ms = 0;
+        VQB_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+        std::snprintf(buf, sizeof buf, "#L %s %.6f %.6g %.6g\n", r.name, ms, r.flops, r.bytes);
         out += buf;
     }
     return out;

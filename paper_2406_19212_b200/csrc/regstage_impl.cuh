@@ -2416,9 +2416,11 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
                     raise(VQB_ERR_INTERNAL, "stage program with register-resident wide operations has no "
                                             "specialised kernel (set VQB_WIDE_REGS=0)");
         }
-        note_flops((act.jit && act.jit->k.e ? act.jit->flops_per_amp : act.dense_flops_per_amp) *
-                   double(1ull << pn));
+        const double launch_flops =
+            (act.jit && act.jit->k.e ? act.jit->flops_per_amp : act.dense_flops_per_amp) * double(1ull << pn);
+        note_flops(launch_flops);
         const ProfMark pf_ = prof_begin(st);
+        prof_annotate(pf_, launch_flops, 32.0 * (REV ? 2 : 1) * double(1ull << pn));
         if (act.jit && act.jit->k.e && REV) {
             const JitShape &sh = *act.jit;
             const size_t sm = (size_t)(sh.xtiles * TS + (sh.spool ? P.npool : 0)) * sizeof(double2) +

@@ -79,12 +79,19 @@ class Engine:
     def profile_begin(self) -> None:
         self.check(self._fn("profile_begin")())
 
-    def profile_end(self) -> dict:
-        """-> {kernel name: (launches, total_ms)} for the window."""
-        buf = ct.create_string_buffer(1 << 16)
+    def profile_end(self, launches: Optional[list] = None) -> dict:
+        """-> {kernel name: (launches, total_ms)} for the window; annotated
+        launches (stage kernels: name, ms, FP64 flops, HBM bytes) are appended
+        to `launches` when given."""
+        buf = ct.create_string_buffer(1 << 20)
         self.check(self._fn("profile_end")(buf, len(buf)))
         out = {}
         for line in buf.value.decode().splitlines():
+            if line.startswith("#L "):
+                if launches is not None:
+                    _, name, ms, fl, by = line.split()
+                    launches.append((name, float(ms), float(fl), float(by)))
+                continue
             name, cnt, ms = line.split()
             out[name] = (int(cnt), float(ms))
         return out
