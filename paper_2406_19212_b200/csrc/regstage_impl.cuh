@@ -813,6 +813,8 @@ struct SlotMap {
     std::vector<long long> dst;
 };
 
+int env_int(const char *name, int dflt);
+
 // Lower as much of a stage's block list as fits one parameter block.
 // `remaining` (block indices, in a valid order) is consumed; what is left
 // must run in a following launch with the same tile bits.
@@ -889,15 +891,54 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
             const unsigned mix = mixmask(*blocks[i]);
             if (__builtin_popcount(rset | mix) <= RB) rset |= mix;
         }
+        // Stable layouts (opt-in, VQB_STABLE_LAYOUT=1): after the first
+        // sub-stage, bits stay where they are unless they must enter the
+        // registers; an entering bit swaps places with a leaving one, so the
+        // specialised kernels can relayout by warp shuffles when the entering
+        // bits are lane bits. Measured slower than fresh layouts with
+        // conflict-free lanes (QAOA adjoint 577 -> 615 ms), hence off.
+        const bool stable = P.nsubs > 0 && env_int("VQB_STABLE_LAYOUT", 0) != 0;
+        if (stable) {
+            const RLayout &A = P.subs[P.nsubs - 1].L;
+            for (int b = 0; b < RB && __builtin_popcount(rset) < RB; ++b) rset |= 1u << A.reg[b];
+        }
         for (int j = K - 1; j >= 0 && __builtin_popcount(rset) < RB; --j) rset |= 1u << j;
         RSub &sb = P.subs[P.nsubs++];
-        int nr = 0;
-        std::vector<int> free_bits;
-        for (int j = 0; j < K; ++j) {
-            if (rset >> j & 1) sb.L.reg[nr++] = j;
-            else free_bits.push_back(j);
+        if (stable) {
+            const RLayout A = P.subs[P.nsubs - 2].L;
+            RLayout B = A;
+            std::vector<int> leaving, entering;
+            for (int b = 0; b < RB; ++b)
+                if (!((rset >> A.reg[b]) & 1)) leaving.push_back(b);
+            for (int j = 0; j < K; ++j) {
+                if (!((rset >> j) & 1)) continue;
+                bool in = false;
+                for (int b = 0; b < RB; ++b) in |= A.reg[b] == j;
+                if (!in) entering.push_back(j);
+            }
+            // lane bits first (shuffle-able), then warp bits
+            auto thr_pos = [&](int j) {
+                for (int b = 0; b < TB; ++b)
+                    if (A.thr[b] == j) return b;
+                return -1;
+            };
+            std::stable_sort(entering.begin(), entering.end(),
+                             [&](int x, int y) { return (thr_pos(x) >= 5) < (thr_pos(y) >= 5); });
+            for (size_t k2 = 0; k2 < entering.size() && k2 < leaving.size(); ++k2) {
+                const int p = leaving[k2], e = entering[k2], q = thr_pos(e);
+                B.thr[q] = A.reg[p];
+                B.reg[p] = e;
+            }
+            sb.L = B;
+        } else {
+            int nr = 0;
+            std::vector<int> free_bits;
+            for (int j = 0; j < K; ++j) {
+                if (rset >> j & 1) sb.L.reg[nr++] = j;
+                else free_bits.push_back(j);
+            }
+            choose_threads(sb.L, free_bits);
         }
-        choose_threads(sb.L, free_bits);
         auto reg_of = [&](int j) {
             for (int b = 0; b < RB; ++b)
                 if (sb.L.reg[b] == j) return b;
@@ -1358,6 +1399,45 @@ std::string jit_wide_op(const RParams &P, int sub, const ROp &op, const std::vec
     return e;
 }
 
+// Relayout of register arrays from layout A to B by warp shuffles, when B is
+// A with some register bits exchanged for lane bits (stable layouts): per
+// exchanged pair (register bit p, lane bit q) and register pair (i, i | 1<<p),
+// lane value l keeps one element and receives the other from lane ^ (1<<q).
+// Returns "" when B is not reachable that way (warp bits or other moves).
+std::string shuffle_relayout(const RLayout &A, const RLayout &B, const std::vector<std::string> &vs) {
+    std::vector<std::pair<int, int>> swaps; // (register position p, lane bit q)
+    RLayout C = A;
+    for (int p = 0; p < RB; ++p) {
+        if (A.reg[p] == B.reg[p]) continue;
+        int q = -1;
+        for (int b = 0; b < TB; ++b)
+            if (A.thr[b] == B.reg[p]) q = b;
+        if (q < 0 || q >= 5 || B.thr[q] != A.reg[p]) return "";
+        swaps.push_back({p, q});
+        C.reg[p] = B.reg[p];
+        C.thr[q] = A.reg[p];
+    }
+    for (int b = 0; b < TB; ++b)
+        if (C.thr[b] != B.thr[b]) return "";
+    if (swaps.empty()) return " ";
+    std::string e = "    {\n";
+    for (auto [p, q] : swaps) {
+        e += "      {\n        const bool l = (threadIdx.x >> " + std::to_string(q) + ") & 1;\n";
+        for (const auto &v : vs)
+            for (int i = 0; i < R; ++i) {
+                if ((i >> p) & 1) continue;
+                const int j = i | (1 << p);
+                const std::string vi = v + "[" + std::to_string(i) + "]", vj = v + "[" + std::to_string(j) + "]";
+                e += "        { const double2 s = l ? " + vi + " : " + vj +
+                     "; const double2 r = make_double2(__shfl_xor_sync(0xffffffffu, s.x, " + std::to_string(1 << q) +
+                     "), __shfl_xor_sync(0xffffffffu, s.y, " + std::to_string(1 << q) + ")); if (l) " + vi +
+                     " = r; else " + vj + " = r; }\n";
+            }
+        e += "      }\n";
+    }
+    return e + "    }\n";
+}
+
 // A wide operation on register bits (ROp::inreg): out[r] = sum_k d_k[r]
 // v[r ^ x_k] per group of registers, XOR-term pool, register conditions
 // resolved per group, run-time ones (cd) select the sub-matrix. `mexpr(off)`
@@ -1477,8 +1557,17 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
         emit("    __syncthreads();\n");
         in_smem = true;
     };
+    const bool shuffles = env_int("VQB_JIT_SHUFFLE", 1) != 0;
     auto to_regs = [&](int sub) {
         if (!in_smem && cur_sub == sub) return;
+        if (!in_smem && shuffles) {
+            const std::string sh = shuffle_relayout(P.subs[cur_sub].L, P.subs[sub].L, {"v"});
+            if (!sh.empty()) {
+                emit(sh);
+                cur_sub = sub;
+                return;
+            }
+        }
         to_smem();
         for (int i = 0; i < R; ++i)
             emit("    v[" + std::to_string(i) + "] = xbuf[st" + std::to_string(sub) + " ^ " +
@@ -1902,8 +1991,17 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
         emit("    __syncthreads();\n");
         in_smem = true;
     };
+    const bool shuffles = env_int("VQB_JIT_SHUFFLE", 1) != 0;
     auto to_regs = [&](int sub) {
         if (!in_smem && cur_sub == sub) return;
+        if (!in_smem && shuffles) {
+            const std::string sh = shuffle_relayout(P.subs[cur_sub].L, P.subs[sub].L, {"vf", "vg"});
+            if (!sh.empty()) {
+                emit(sh);
+                cur_sub = sub;
+                return;
+            }
+        }
         to_smem();
         for (int i = 0; i < R; ++i) {
             const std::string sl = "st" + I(sub) + " ^ " + I(slot_const(P.subs[sub].L, i));
@@ -2318,7 +2416,7 @@ std::string shape_key(const RParams &P, bool rev) {
             cls[(size_t)i >> 2] = (char)(cls[(size_t)i >> 2] | (pool_cls(P, (unsigned)i, 1, 0) << (2 * (i & 3))));
         key += cls;
     }
-    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_JIT_WIDE_PARAM", "VQB_WIDE_REGS", "VQB_JIT_GDIFF", "VQB_JIT_ACCBATCH", "VQB_JIT_STASH"}) {
+    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_JIT_WIDE_PARAM", "VQB_WIDE_REGS", "VQB_JIT_GDIFF", "VQB_JIT_ACCBATCH", "VQB_JIT_STASH", "VQB_JIT_SHUFFLE", "VQB_STABLE_LAYOUT"}) {
         const char *v = std::getenv(e);
         key += '|';
         if (v) key += v;
