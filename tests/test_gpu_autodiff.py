@@ -281,14 +281,18 @@ def test_specialised_adjoint_matches_reference(dev, ref, monkeypatch, regs):
 
 
 @pytest.mark.parametrize("variant", [{}, {"VQB_JIT_DIAGRUN": "0"}, {"VQB_JIT_ACC": "1000"},
-                                     {"VQB_JIT_LAZY": "0"}, {"VQB_PARALLEL_ADJOINT": "0"}])
+                                     {"VQB_JIT_LAZY": "0"}, {"VQB_PARALLEL_ADJOINT": "0"},
+                                     {"VQB_STABLE_LAYOUT": "1"}, {"VQB_JIT_ACCBATCH": "1"},
+                                     {"VQB_JIT_GDIFF": "0", "VQB_JIT_STASH": "1"}])
 def test_structure_classes_and_generator_variants(dev, ref, monkeypatch, variant):
     """Specialised kernels key on which matrix entries are exactly zero, real or
     imaginary (structure-aware emission): angles that make entries vanish
     (Rx(pi): zero real parts; Ry(pi): a zero diagonal; Rz(0): the identity)
     must compile their own kernels and still match the reference, forward and
     adjoint, in every generator variant (diagonal runs off, no accumulator
-    budget, eager relayouts, serial host planning)."""
+    budget, eager relayouts, serial host planning, stable layouts with shuffle
+    relayouts, batched slot reductions, no derivative generators with parked
+    states)."""
     monkeypatch.setenv("VQB_JIT", "1")
     for k, v in variant.items():
         monkeypatch.setenv(k, v)
