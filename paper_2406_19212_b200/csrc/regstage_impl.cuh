@@ -1505,7 +1505,7 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
 // tile bits come from a shared-memory copy. Returns "" for programs the
 // generator does not cover (wide operations).
 std::string jit_forward_source(const RParams &P, bool *uses_spool, bool *per_block, double *flops) {
-    if constexpr (RB != 4 || TB != 7) return "";
+    if constexpr (RB != 4) return "";
     else return jit_forward_source_rs16(P, uses_spool, per_block, flops);
 }
 
@@ -1536,7 +1536,7 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
     const char *pool_env = std::getenv("VQB_JIT_POOL");
     const bool pool_smem = pool_env && std::strcmp(pool_env, "smem") == 0;
     const std::string MP = pool_smem ? "spool" : "P.pool";
-    const int jit_blocks = env_int("VQB_JIT_BLOCKS", 4);
+    const int jit_blocks = env_int("VQB_JIT_BLOCKS", TB >= 8 ? 2 : 4);
     const char *mode_env = std::getenv("VQB_JIT_MODE");
     const bool per_block_mode = !(mode_env && std::strcmp(mode_env, "persistent") == 0);
     std::string body;
@@ -1729,10 +1729,11 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
             std::string tmpl;
             int mask = 0;
             if (op.nt == 1) {
-                tmpl = "1, " + std::to_string(op.code) + ", 0, 16";
+                tmpl = "1, " + std::to_string(op.code) + ", 0, " + std::to_string(R);
                 mask = 1 << op.code;
             } else if (op.nt == 2) {
-                tmpl = "2, " + std::to_string(pair_p0[op.code]) + ", " + std::to_string(pair_p1[op.code]) + ", 16";
+                tmpl = "2, " + std::to_string(pair_p0[op.code]) + ", " + std::to_string(pair_p1[op.code]) + ", " +
+                       std::to_string(R);
                 mask = (1 << pair_p0[op.code]) | (1 << pair_p1[op.code]);
             }
             const std::string ident = num(op.ident);
@@ -1784,19 +1785,19 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
     const RLayout &Lf = P.subs[P.nsubs - 1].L;
     out("#include \"jit_rt.cuh\"\nusing namespace vqbjit;\n");
     out("struct JP { double2 pool[" + std::to_string(std::max(P.npool, 1)) + "]; };\n");
-    out("extern \"C\" __global__ void __launch_bounds__(128, " + std::to_string(jit_blocks) + ")\n"
+    out("extern \"C\" __global__ void __launch_bounds__(" + std::to_string(T) + ", " + std::to_string(jit_blocks) + ")\n"
         "vqb_stage(double2 *__restrict__ a, const __grid_constant__ JP P) {\n");
     out(per_block_mode ? "  extern __shared__ __align__(16) double2 sm[];\n  double2 *xbuf = sm;\n"
                        : "  extern __shared__ __align__(16) double2 sm[];\n"
-                         "  double2 *stage = sm, *xbuf = sm + 2048;\n");
+                         "  double2 *stage = sm, *xbuf = sm + " + std::to_string(TS) + ";\n");
     // matrices are read from a shared-memory copy at constant offsets: loads
     // the compiler cannot hoist out of the tile loop (parameter-bank reads
     // would be hoisted into registers and spill)
     spool = spool || pool_smem;
     if (spool)
-        out(std::string("  double2 *spool = sm + ") + (per_block_mode ? "2048" : "4096") +
+        out(std::string("  double2 *spool = sm + ") + std::to_string(per_block_mode ? TS : 2 * TS) +
             ";\n  for (int i = threadIdx.x; i < " + std::to_string(P.npool) +
-            "; i += 128) spool[i] = P.pool[i];\n  __syncthreads();\n");
+            "; i += " + std::to_string(T) + ") spool[i] = P.pool[i];\n  __syncthreads();\n");
     out("  const int t = threadIdx.x;\n");
     int nat_local[TB];
     for (int b = 0; b < TB; ++b) nat_local[b] = b;
@@ -1836,7 +1837,7 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
     if (per_block_mode) {
         // one tile per block: coalesced loads straight into registers, one
         // relayout to the first layout; other resident blocks cover latency
-        out("  {\n    const u64 tile = blockIdx.x;\n    const u64 base = base_of(tile);\n    double2 v[16];\n");
+        out("  {\n    const u64 tile = blockIdx.x;\n    const u64 base = base_of(tile);\n    double2 v[" + std::to_string(R) + "];\n");
         for (int s2 = 0; s2 < R; ++s2) {
             unsigned long long g;
             int sl;
@@ -1863,7 +1864,7 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
         out("    cp_async_commit();\n  };\n");
         out("  u64 tile = blockIdx.x;\n  if (tile < NT) prefetch(tile);\n"
             "  for (; tile < NT; tile += gridDim.x) {\n    const u64 base = base_of(tile);\n"
-            "    cp_async_wait_all();\n    __syncthreads();\n    double2 v[16];\n");
+            "    cp_async_wait_all();\n    __syncthreads();\n    double2 v[" + std::to_string(R) + "];\n");
         out(slot_bases);
         for (int i = 0; i < R; ++i)
             out("    v[" + std::to_string(i) + "] = stage[st0 ^ " + std::to_string(slot_const(P.subs[0].L, i)) + "];\n");
