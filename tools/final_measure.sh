@@ -4,7 +4,8 @@
 # kernel. Outputs under gpurun_out/final/.
 mkdir -p gpurun_out/final
 for c in rqc28 hea20 qaoa30 noisy15 rqc33; do
-  timeout 900 python bench.py --config $c > gpurun_out/final/bench_$c.json 2> gpurun_out/final/bench_$c.err
+  K=5; [ "$c" = hea20 ] && K=50   # 2 ms steps: a longer timed region
+  timeout 900 python bench.py --config $c --steps $K > gpurun_out/final/bench_$c.json 2> gpurun_out/final/bench_$c.err
   timeout 600 python bench.py --impl reference --config $c --steps 2 > gpurun_out/final/ref_$c.json 2> gpurun_out/final/ref_$c.err
 done
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/final/launches_rqc28.csv \
