@@ -1192,6 +1192,16 @@ template <bool REV, bool WIDE> int grid_size(unsigned long long ntiles, size_t s
 
 
 
+// Lanes per warp that keep a partial sum of a gradient slot (the rest of the
+// warp reduction happens in the block's final sum): VQB_JIT_REDLANES (1, 2,
+// 4, 8); measured best 4 for 8-register adjoints (QAOA 578 -> 556 ms), 2 for
+// 16-register ones (noisy 915 -> 898 ms); 1 for batched reductions.
+int red_lanes_of(bool batch) {
+    if (batch) return 1;
+    int v = env_int("VQB_JIT_REDLANES", R >= 16 ? 2 : 4);
+    return v >= 8 ? 8 : v >= 4 ? 4 : v >= 2 ? 2 : 1;
+}
+
 // ---------------------------------------------------------------- structure-aware emission
 // The specialised kernels read matrix values at run time, but which entries
 // are exactly zero, purely real or purely imaginary is structure: channel
@@ -1931,6 +1941,7 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
     // (9 double shuffles for 8 slots instead of 40; lane l ends with slot
     // (l >> 2) & 7); VQB_JIT_ACCBATCH=0 reduces slot by slot.
     const bool acc_batch = env_int("VQB_JIT_ACCBATCH", 0) != 0; // measured: no gain (QAOA), spills (rs16)
+    const int red_lanes = red_lanes_of(acc_batch);
     const int acc_budget = env_int("VQB_JIT_ACC", acc_batch ? 8 : 6);
     std::vector<int> open_slots;
     auto flush_batch = [&](const std::vector<int> &sl) {
@@ -1951,7 +1962,8 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
         // slot index per lane group
         e += "      const int q = (lane >> 2) & 7;\n      if ((lane & 3) == 0) {\n";
         for (int k = 0; k < (int)sl.size(); ++k)
-            e += "        if (q == " + I(k) + ") red[" + I(sl[k] * NW) + " + warp] = d;\n";
+            e += "        if (q == " + I(k) + ") red[" + I(sl[k] * NW * red_lanes) + " + warp * " + I(red_lanes) +
+                 "] = d;\n";
         e += "      }\n    }\n";
         emit(e);
     };
@@ -1971,8 +1983,14 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
         while ((int)open_slots.size() > keep) {
             const int sl = open_slots.front();
             open_slots.erase(open_slots.begin());
-            emit("    { const double x = warp_sum(acc_s" + I(sl) + "); if (lane == 0) red[" + I(sl * NW) +
-                 " + warp] = x; }\n");
+            // reduce over the lane bits above log2(PL) only; PL lanes per warp
+            // store partial sums (fewer dependent shuffles per slot)
+            std::string e = "    { double x = acc_s" + I(sl) + ";";
+            for (int sh = 16; sh >= red_lanes; sh >>= 1)
+                e += " x += __shfl_xor_sync(0xffffffffu, x, " + I(sh) + ");";
+            e += " if (lane < " + I(red_lanes) + ") red[" + I(sl * NW * red_lanes) + " + warp * " + I(red_lanes) +
+                 " + lane] = x; }\n";
+            emit(e);
         }
     };
     // Where Phi and Psi live: in registers in the layout of sub-stage cur_sub,
@@ -2362,7 +2380,7 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
         // every slot was reduced into red[] by flush_slots
         out("  __syncthreads();\n");
         out("  for (int s = t; s < " + I(P.nslots) + "; s += " + I(T) + ") {\n    double x = 0;\n");
-        for (int w = 0; w < NW; ++w) out("    x += red[s * " + I(NW) + " + " + I(w) + "];\n");
+        for (int w = 0; w < NW * red_lanes; ++w) out("    x += red[s * " + I(NW * red_lanes) + " + " + I(w) + "];\n");
         out("    partial[(size_t)s * " + num(P.ntiles) + " + tile] = x;\n  }\n");
     }
     out("}\n");
@@ -2417,7 +2435,7 @@ std::string shape_key(const RParams &P, bool rev) {
             cls[(size_t)i >> 2] = (char)(cls[(size_t)i >> 2] | (pool_cls(P, (unsigned)i, 1, 0) << (2 * (i & 3))));
         key += cls;
     }
-    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_JIT_WIDE_PARAM", "VQB_WIDE_REGS", "VQB_JIT_GDIFF", "VQB_JIT_ACCBATCH", "VQB_JIT_STASH", "VQB_JIT_SHUFFLE", "VQB_STABLE_LAYOUT"}) {
+    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_JIT_WIDE_PARAM", "VQB_WIDE_REGS", "VQB_JIT_GDIFF", "VQB_JIT_ACCBATCH", "VQB_JIT_STASH", "VQB_JIT_SHUFFLE", "VQB_STABLE_LAYOUT", "VQB_JIT_REDLANES"}) {
         const char *v = std::getenv(e);
         key += '|';
         if (v) key += v;
@@ -2523,7 +2541,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
         if (act.jit && act.jit->k.e && REV) {
             const JitShape &sh = *act.jit;
             const size_t sm = (size_t)(sh.xtiles * TS + (sh.spool ? P.npool : 0)) * sizeof(double2) +
-                              sizeof(double) * (size_t)P.nslots * NW;
+                              sizeof(double) * (size_t)P.nslots * NW * red_lanes_of(env_int("VQB_JIT_ACCBATCH", 0) != 0);
             void *a0 = sphi->amps, *a1 = spsi->amps, *pp = m_jpartial.p;
             void *args[4] = {&a0, &a1, &pp, P.pool};
             jit::launch(sh.k, (unsigned)ntiles, T, sm, st, args);
