@@ -152,17 +152,33 @@ class ShardedState:
             send_half = v[:, 1 - mine, :]
             hi, lo = v.shape[0], v.shape[2]
             rows_per_chunk = max(1, self.chunk // lo)
+            # two chunks in flight: chunk k+1's transfer overlaps chunk k's
+            # copy into place (a chunk is overwritten only after its own send
+            # completed; the send reads the shard directly when the half is
+            # contiguous, lpos = top local bit)
+            pending = []
+
+            def finish(item):
+                reqs, rbuf, a, b = item
+                for req in reqs:
+                    req.wait()
+                send_half[a:b] = torch.view_as_complex(rbuf)
+
             for r0 in range(0, hi, rows_per_chunk):
                 r1 = min(hi, r0 + rows_per_chunk)
                 sbuf = torch.view_as_real(send_half[r0:r1].contiguous())
                 rbuf = torch.empty_like(sbuf)
+                reqs = []
                 if self.world > 1:
                     ops = [self.dist.P2POp(self.dist.isend, sbuf, partner),
                            self.dist.P2POp(self.dist.irecv, rbuf, partner)]
-                    for req in self.dist.batch_isend_irecv(ops):
-                        req.wait()
-                send_half[r0:r1] = torch.view_as_complex(rbuf)
+                    reqs = self.dist.batch_isend_irecv(ops)
+                pending.append((reqs, rbuf, r0, r1))
                 self.bytes_exchanged += sbuf.numel() * 8
+                if len(pending) == 2:
+                    finish(pending.pop(0))
+            for item in pending:
+                finish(item)
         # logical qubits on the two physical bits trade places
         a = self.log2phys.index(gpos)
         b = self.log2phys.index(lpos)
