@@ -406,11 +406,15 @@ def main():
     ap.add_argument("--unfused", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run rqc33/qaoa30 through the sharded runner even at N = 1 (plumbing check)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
     world, rank, local, dist = dist_setup(args)
     wl = Workload(args.config, args, world)
+    if args.sharded and args.config in ("rqc33", "qaoa30"):
+        wl.sharded = True
     if args.impl == "reference":
         return run_reference_arm(args, wl, world, rank)
 
@@ -575,7 +579,8 @@ def main():
             if wl.sharded:
                 runner.reset()
                 runner.step()
-                return state.norm()
+                # apply: the norm; gradient: loss + gradients (all-reduced) on the host
+                return state.norm() if wl.kind == "apply" else runner.loss
             reset()
             eng.apply_circuit(wl.w.circuit, state)
             return eng.norm(state)
@@ -591,11 +596,15 @@ def main():
         e1.record(stream)
         e1.synchronize()
         ems = max_over_ranks(dist, e0.elapsed_time(e1))
+        grad = wl.kind != "apply"
         e2e = {"value": world * wl.units_per_step * args.steps / (ems / 1e3), "unit": wl.unit,
-               "h2d_bytes_per_step": ct.sizeof(vqb_op) * wl.gates, "d2h_bytes_per_step": 8,
+               "h2d_bytes_per_step": ct.sizeof(vqb_op) * wl.gates,
+               "d2h_bytes_per_step": 8 * (1 + wl.w.circuit.num_active_params()) if grad else 8,
                "ms_per_step": ems / args.steps,
-               "path": "vqb_state_set_zero -> vqb_apply_circuit (ops packed from host objects) -> vqb_norm "
-                       "(the 128 GiB state does not round-trip through host memory)"}
+               "path": ("sharded |0...0> -> ShardedState.gradient_pure (loss + all-reduced gradients to the host)"
+                        if grad else
+                        "vqb_state_set_zero -> vqb_apply_circuit (ops packed from host objects) -> vqb_norm "
+                        "(the 128 GiB state does not round-trip through host memory)")}
     elif not args.no_e2e and wl.kind == "apply":
         # the user call: vqb_apply_circuit_copy_batch over host states (one job
         # per step: upload the input state from pinned memory, run the circuit,
