@@ -744,20 +744,35 @@ __global__ void k_grads(const double *__restrict__ partial, int nblocks, int ld,
 // Specialised adjoint launches write one partial per (slot, tile); this sums a
 // slot's row in fixed order (strided per thread, then a fixed tree):
 // deterministic. One block per slot of the launch.
+// Split over kSlotSplit blocks per slot (blockIdx.y), each summing a
+// contiguous share of the row into split[slot][y]; k_slot_final adds the
+// shares in fixed order. (One block per slot left most SMs idle: 0.45 ms per
+// launch at 2^20 tiles.)
+constexpr int kSlotSplit = 16;
 __global__ void __launch_bounds__(256) k_slot_sums(const double *__restrict__ partial,
                                                    unsigned long long ntiles,
-                                                   double *__restrict__ out) {
+                                                   double *__restrict__ split) {
     __shared__ double sh[256];
     const double *row = partial + (size_t)blockIdx.x * ntiles;
+    const unsigned long long per = (ntiles + gridDim.y - 1) / gridDim.y;
+    const unsigned long long lo = per * blockIdx.y, hi = lo + per < ntiles ? lo + per : ntiles;
     double v = 0;
-    for (unsigned long long i = threadIdx.x; i < ntiles; i += 256) v += row[i];
+    for (unsigned long long i = lo + threadIdx.x; i < hi; i += 256) v += row[i];
     sh[threadIdx.x] = v;
     __syncthreads();
     for (int w = 128; w > 0; w >>= 1) {
         if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
         __syncthreads();
     }
-    if (threadIdx.x == 0) out[blockIdx.x] = sh[0];
+    if (threadIdx.x == 0) split[blockIdx.x * gridDim.y + blockIdx.y] = sh[0];
+}
+__global__ void k_slot_final(const double *__restrict__ split, int nslots, int nsplit,
+                             double *__restrict__ out) {
+    for (int s = threadIdx.x; s < nslots; s += blockDim.x) {
+        double x = 0;
+        for (int y = 0; y < nsplit; ++y) x += split[s * nsplit + y];
+        out[s] = x;
+    }
 }
 
 // ---------------------------------------------------------------- host planning
@@ -2505,7 +2520,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
         double dense_flops_per_amp = 0; // interpreter: dense matrices
     };
     // adjoint specialisation: per-(slot, tile) partials, summed per launch
-    static thread_local DevMem m_jpartial, m_slotsum;
+    static thread_local DevMem m_jpartial, m_slotsum, m_slotsplit;
     const size_t jpartial_bytes = sizeof(double) * (size_t)kMaxSlots * ntiles;
     const bool use_jit = jit::enabled(pn) && (!REV || jpartial_bytes <= (size_t(1) << 30));
     // wide operations on register bits need the specialised kernels (the
@@ -2548,8 +2563,19 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             check_launch("k_regstage_rev_jit", pf_);
             if (P.nslots > 0) {
                 const ProfMark pf2 = prof_begin(st);
-                k_slot_sums<<<P.nslots, 256, 0, st>>>(static_cast<const double *>(m_jpartial.p), ntiles,
-                                                       static_cast<double *>(m_slotsum.p) + P.slot_begin);
+                // small sweeps (few tiles): one block per slot, straight to the sums
+                double *slot_out = static_cast<double *>(m_slotsum.p) + P.slot_begin;
+                if (ntiles >= (1ull << 16)) {
+                    m_slotsplit.ensure(sizeof(double) * kMaxSlots * kSlotSplit);
+                    k_slot_sums<<<dim3(P.nslots, kSlotSplit), 256, 0, st>>>(
+                        static_cast<const double *>(m_jpartial.p), ntiles, static_cast<double *>(m_slotsplit.p));
+                    k_slot_final<<<1, 64, 0, st>>>(static_cast<const double *>(m_slotsplit.p), P.nslots,
+                                                   kSlotSplit, slot_out);
+                    note_launch(1); // k_slot_final (check_launch below counts k_slot_sums)
+                } else {
+                    k_slot_sums<<<dim3(P.nslots, 1), 256, 0, st>>>(static_cast<const double *>(m_jpartial.p),
+                                                                  ntiles, slot_out);
+                }
                 check_launch("k_slot_sums", pf2);
             }
             return;
