@@ -1572,8 +1572,12 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
     // in the layout of cur_sub, or in xbuf in tile-index space; wide ops work
     // on xbuf in place, so they share the round trip of a neighbouring
     // relayout. The one-tile-per-block prologue leaves the tile in xbuf.
-    bool in_smem = per_block_mode;
-    int cur_sub = per_block_mode ? -1 : 0;
+    // VQB_JIT_DIRECT: the one-tile-per-block prologue loads straight into the
+    // first sub-stage's layout (lanes 0-2 on the tile's low bits keep the
+    // loads in full sectors) instead of through the shared-memory tile
+    const bool direct = per_block_mode && env_int("VQB_JIT_DIRECT", 1) != 0;
+    bool in_smem = per_block_mode && !direct;
+    int cur_sub = per_block_mode && !direct ? -1 : 0;
     auto to_smem = [&]() {
         if (in_smem) return;
         for (int i = 0; i < R; ++i)
@@ -1863,20 +1867,31 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
         // one tile per block: coalesced loads straight into registers, one
         // relayout to the first layout; other resident blocks cover latency
         out("  {\n    const u64 tile = blockIdx.x;\n    const u64 base = base_of(tile);\n    double2 v[" + std::to_string(R) + "];\n");
-        for (int s2 = 0; s2 < R; ++s2) {
+        if (direct) {
+            const RLayout &L0 = P.subs[0].L;
+            out("    const u64 g0 = " + thread_expr(L0.thr, true) + ";\n");
+            for (int i = 0; i < R; ++i) {
+                unsigned long long g = 0;
+                for (int b = 0; b < RB; ++b)
+                    if ((i >> b) & 1) g |= 1ull << P.bits[L0.reg[b]];
+                out("    v[" + std::to_string(i) + "] = a[base | g0 | " + num(g) + "];\n");
+            }
+            out(slot_bases);
+        }
+        for (int s2 = 0; s2 < R && !direct; ++s2) {
             unsigned long long g;
             int sl;
             natural(s2, &g, &sl);
             out("    v[" + std::to_string(s2) + "] = a[base | glo | " + num(g) + "];\n");
         }
-        out(slot_bases + "    const int nat_st = swz(to);\n");
-        for (int s2 = 0; s2 < R; ++s2) {
+        if (!direct) out(slot_bases + "    const int nat_st = swz(to);\n");
+        for (int s2 = 0; s2 < R && !direct; ++s2) {
             unsigned long long g;
             int sl;
             natural(s2, &g, &sl);
             out("    xbuf[nat_st ^ " + std::to_string(sl) + "] = v[" + std::to_string(s2) + "];\n");
         }
-        out("    __syncthreads();\n"); // the body starts with the tile in xbuf (lazy residency)
+        if (!direct) out("    __syncthreads();\n"); // the body starts with the tile in xbuf (lazy residency)
     } else {
         out("  auto prefetch = [&](u64 tile) {\n    const u64 b = base_of(tile) | glo;\n    " + opaque_t("tn") +
             "    const int nat_st = swz(tn);\n");
@@ -2014,8 +2029,11 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
     // registers of their layout, wide ops push them to the tiles, so a
     // relayout next to a wide operation shares its shared-memory round trip
     // and sub-stages without register work cost no relayout.
-    bool in_smem = true; // the prologue leaves both states in the tiles
-    int cur_sub = -1;
+    // the prologue leaves both states in the tiles, or (VQB_JIT_DIRECT) loads
+    // them straight into the first sub-stage's layout
+    const bool direct = env_int("VQB_JIT_DIRECT", 1) != 0;
+    bool in_smem = !direct;
+    int cur_sub = direct ? 0 : -1;
     auto to_smem = [&]() {
         if (in_smem) return;
         for (int i = 0; i < R; ++i) {
@@ -2365,7 +2383,18 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
     out("    return c;\n  };\n");
     out("  const u64 tile = blockIdx.x;\n  const u64 base = base_of(tile);\n");
     out("  double2 vf[" + I(R) + "], vg[" + I(R) + "];\n");
-    for (int s2 = 0; s2 < R; ++s2) {
+    if (direct) {
+        const RLayout &L0 = P.subs[0].L;
+        out("  const u64 g0 = " + thread_expr(L0.thr, true, "t") + ";\n");
+        for (int i = 0; i < R; ++i) {
+            unsigned long long g = 0;
+            for (int b = 0; b < RB; ++b)
+                if ((i >> b) & 1) g |= 1ull << P.bits[L0.reg[b]];
+            out("  vf[" + I(i) + "] = a[base | g0 | " + num(g) + "];\n  vg[" + I(i) + "] = b2[base | g0 | " + num(g) +
+                "];\n");
+        }
+    }
+    for (int s2 = 0; s2 < R && !direct; ++s2) {
         unsigned long long g = 0;
         for (int b = 0; b < RB; ++b)
             if ((s2 >> b) & 1) g |= 1ull << P.bits[TB + b];
@@ -2375,14 +2404,18 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
     out("  int to; asm volatile(\"mov.b32 %0, %1;\" : \"=r\"(to) : \"r\"(t));\n");
     for (int sub = 0; sub < P.nsubs; ++sub)
         out("  const int st" + I(sub) + " = swz" + thread_expr(P.subs[sub].L.thr, false, "to") + ";\n");
-    out("  const int nat_st = swz(to);\n");
-    for (int s2 = 0; s2 < R; ++s2) {
-        int sl = 0;
-        for (int b = 0; b < RB; ++b)
-            if ((s2 >> b) & 1) sl ^= swz(T << b);
-        out("  xbuf[nat_st ^ " + I(sl) + "] = vf[" + I(s2) + "]; xbuf2[nat_st ^ " + I(sl) + "] = vg[" + I(s2) + "];\n");
+    if (!direct) {
+        out("  const int nat_st = swz(to);\n");
+        for (int s2 = 0; s2 < R; ++s2) {
+            int sl = 0;
+            for (int b = 0; b < RB; ++b)
+                if ((s2 >> b) & 1) sl ^= swz(T << b);
+            out("  xbuf[nat_st ^ " + I(sl) + "] = vf[" + I(s2) + "]; xbuf2[nat_st ^ " + I(sl) + "] = vg[" + I(s2) + "];\n");
+        }
+        out("  __syncthreads();\n");
+    } else if (spool) {
+        out("  __syncthreads(); // the pool copy above is read by every thread\n");
     }
-    out("  __syncthreads();\n");
     out(body);
     for (int i = 0; i < R; ++i) {
         unsigned long long g = 0;
@@ -2450,7 +2483,7 @@ std::string shape_key(const RParams &P, bool rev) {
             cls[(size_t)i >> 2] = (char)(cls[(size_t)i >> 2] | (pool_cls(P, (unsigned)i, 1, 0) << (2 * (i & 3))));
         key += cls;
     }
-    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_JIT_WIDE_PARAM", "VQB_WIDE_REGS", "VQB_JIT_GDIFF", "VQB_JIT_ACCBATCH", "VQB_JIT_STASH", "VQB_JIT_SHUFFLE", "VQB_STABLE_LAYOUT", "VQB_JIT_REDLANES"}) {
+    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_JIT_WIDE_PARAM", "VQB_WIDE_REGS", "VQB_JIT_GDIFF", "VQB_JIT_ACCBATCH", "VQB_JIT_STASH", "VQB_JIT_SHUFFLE", "VQB_STABLE_LAYOUT", "VQB_JIT_REDLANES", "VQB_JIT_DIRECT"}) {
         const char *v = std::getenv(e);
         key += '|';
         if (v) key += v;

@@ -284,7 +284,8 @@ def test_specialised_adjoint_matches_reference(dev, ref, monkeypatch, regs):
                                      {"VQB_JIT_LAZY": "0"}, {"VQB_PARALLEL_ADJOINT": "0"},
                                      {"VQB_STABLE_LAYOUT": "1"}, {"VQB_JIT_ACCBATCH": "1"},
                                      {"VQB_JIT_GDIFF": "0", "VQB_JIT_STASH": "1"},
-                                     {"VQB_JIT_REDLANES": "1"}, {"VQB_JIT_REDLANES": "8"}])
+                                     {"VQB_JIT_REDLANES": "1"}, {"VQB_JIT_REDLANES": "8"},
+                                     {"VQB_JIT_DIRECT": "0"}])
 def test_structure_classes_and_generator_variants(dev, ref, monkeypatch, variant):
     """Specialised kernels key on which matrix entries are exactly zero, real or
     imaginary (structure-aware emission): angles that make entries vanish
