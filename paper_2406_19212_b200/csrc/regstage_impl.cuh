@@ -1972,7 +1972,8 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
     // (l >> 2) & 7); VQB_JIT_ACCBATCH=0 reduces slot by slot.
     const bool acc_batch = env_int("VQB_JIT_ACCBATCH", 0) != 0; // measured: no gain (QAOA), spills (rs16)
     const int red_lanes = red_lanes_of(acc_batch);
-    const int acc_budget = env_int("VQB_JIT_ACC", acc_batch ? 8 : 6);
+    // measured: 6 for 8-register sweeps, 3 for the register-heavy 16-register ones
+    const int acc_budget = env_int("VQB_JIT_ACC", acc_batch ? 8 : (R >= 16 ? 3 : 6));
     std::vector<int> open_slots;
     auto flush_batch = [&](const std::vector<int> &sl) {
         std::string e = "    {\n      double a0";
