@@ -150,6 +150,22 @@ VQB_API int vqb_debug_jit_source(int32_t regs, const void *params, size_t nbytes
 VQB_API int vqb_profile_begin(void);
 VQB_API int vqb_profile_end(char *buf, int64_t cap);
 
+/* ---- allocation bookkeeping: state.hpp:56-83,154-161 ---- */
+/* state_alloc_stats(): live and peak counts of full amplitude buffers (every
+ * state created by this library, including working states a loss/gradient
+ * keeps cached for the next call), plus live/peak device bytes of everything
+ * the library allocated (scratch included). Null outputs are skipped. */
+VQB_API int vqb_alloc_stats(int64_t *live_states, int64_t *peak_states, uint64_t *live_bytes,
+                            uint64_t *peak_bytes);
+/* reset_state_alloc_peak(): peak counters <- live counters. */
+VQB_API int vqb_reset_alloc_peak(void);
+/* Frees every cache the library keeps across calls (working states of
+ * losses/gradients, the batch API's rotating states, executor scratch) on
+ * every device. No reference analogue (the reference frees its working
+ * copies at the end of each call, autodiff.hpp:111-124). Must not run
+ * concurrently with any other call. */
+VQB_API int vqb_release_caches(void);
+
 /* ---- device state: replaces PureState / MixedState storage ---- */
 /* PureState(n) (state.hpp:182-185) when mixed == 0, MixedState(n)
  * (state.hpp:264-268) when mixed != 0; initialised to |0...0> (<0...0|). */
@@ -174,6 +190,12 @@ VQB_API int vqb_state_set_zero(vqb_state *st); /* back to |0...0> */
 VQB_API int vqb_state_upload(vqb_state *st, const vqb_c128 *host, uint64_t count);
 VQB_API int vqb_state_download(const vqb_state *st, vqb_c128 *host, uint64_t count);
 VQB_API int vqb_state_copy(vqb_state *dst, const vqb_state *src);
+/* Amplitudes [offset, offset + count) in canonical order (the host-side view
+ * of a slice of state.hpp's amplitude vector, state.hpp:222-226) — for states
+ * too large to download whole (config 4: 128 GiB). INDEX if the range does not
+ * fit the state. */
+VQB_API int vqb_state_download_range(const vqb_state *st, uint64_t offset, uint64_t count,
+                                     vqb_c128 *host);
 
 /* ---- gate / channel application: kernels.hpp, circuit.hpp ---- */
 /* apply_gate_fast (kernels.hpp:365-430) on a pure state; apply_gate_mixed

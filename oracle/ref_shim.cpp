@@ -199,6 +199,22 @@ REF_API const char *vqcsref_last_error(void) { return g_last_error.c_str(); }
 REF_API void vqcsref_set_num_threads(int t) { g_threads = t; }
 REF_API int vqcsref_get_num_threads(void) { return cfg().num_threads; }
 
+// ---- allocation bookkeeping: state_alloc_stats (state.hpp:154-161) ----
+REF_API int vqcsref_alloc_stats(int64_t *live, int64_t *peak, uint64_t *live_bytes,
+                                uint64_t *peak_bytes) {
+    const auto a = vqcs::state_alloc_stats();
+    if (live) *live = a.live;
+    if (peak) *peak = a.peak;
+    if (live_bytes) *live_bytes = 0; // the reference counts buffers, not bytes
+    if (peak_bytes) *peak_bytes = 0;
+    return VQB_OK;
+}
+REF_API int vqcsref_reset_alloc_peak(void) {
+    vqcs::reset_state_alloc_peak();
+    return VQB_OK;
+}
+REF_API int vqcsref_release_caches(void) { return VQB_OK; } // the reference caches nothing
+
 // ---- state ----
 REF_API int vqcsref_state_create(int32_t n, int32_t mixed, RefState **out) {
     return guard([&] {
@@ -209,6 +225,16 @@ REF_API int vqcsref_state_create(int32_t n, int32_t mixed, RefState **out) {
             s->pure.emplace(n); // PureState(n) state.hpp:182-185
         }
         *out = s.release();
+    });
+}
+
+// The reference harness's per-repetition reset (src/bench.cpp:138-141):
+// std::fill with zero, then amplitude 0 = 1 (pure) / entry (0,0) = 1 (mixed).
+REF_API int vqcsref_state_set_zero(RefState *s) {
+    return guard([&] {
+        auto a = s->amps();
+        std::fill(a.begin(), a.end(), C(0));
+        a[0] = 1;
     });
 }
 
@@ -242,6 +268,17 @@ REF_API int vqcsref_state_download(const RefState *s, vqb_c128 *host, uint64_t c
             throw ShapeError("state_download: count mismatch");
         }
         std::memcpy(host, a.data(), count * sizeof(C));
+    });
+}
+
+REF_API int vqcsref_state_download_range(const RefState *s, uint64_t offset, uint64_t count,
+                                         vqb_c128 *host) {
+    return guard([&] {
+        auto a = s->amps();
+        if (offset > a.size() || count > a.size() - offset) {
+            throw IndexError("state_download_range: range exceeds the state");
+        }
+        std::memcpy(host, a.data() + offset, count * sizeof(C));
     });
 }
 

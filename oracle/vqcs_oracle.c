@@ -540,6 +540,21 @@ typedef struct {
     cd *a;
 } ostate;
 
+/* AllocStats state.hpp:56-83,154-161: live/peak full-state buffers */
+static int64_t g_live, g_peak;
+ORC_API int vqcsorc_alloc_stats(int64_t *live, int64_t *peak, uint64_t *live_bytes, uint64_t *peak_bytes) {
+    if (live) *live = g_live;
+    if (peak) *peak = g_peak;
+    if (live_bytes) *live_bytes = 0;
+    if (peak_bytes) *peak_bytes = 0;
+    return VQB_OK;
+}
+ORC_API int vqcsorc_reset_alloc_peak(void) {
+    g_peak = g_live;
+    return VQB_OK;
+}
+ORC_API int vqcsorc_release_caches(void) { return VQB_OK; }
+
 ORC_API int vqcsorc_state_create(int32_t n, int32_t mixed, ostate **out) {
     const int maxq = mixed ? 20 : 40; /* state.hpp:179,261 */
     if (n < 1) return fail(VQB_ERR_SIZE, "qubit count must be >= 1");
@@ -555,12 +570,14 @@ ORC_API int vqcsorc_state_create(int32_t n, int32_t mixed, ostate **out) {
         return fail(VQB_ERR_SIZE, "cannot allocate state");
     }
     s->a[0] = C(1, 0);
+    if (++g_live > g_peak) g_peak = g_live;
     *out = s;
     return VQB_OK;
 }
 
 ORC_API int vqcsorc_state_destroy(ostate *s) {
     if (s) {
+        --g_live;
         free(s->a);
         free(s);
     }
@@ -583,6 +600,19 @@ ORC_API int vqcsorc_state_upload(ostate *s, const cd *h, uint64_t count) {
 ORC_API int vqcsorc_state_download(const ostate *s, cd *h, uint64_t count) {
     if (count != s->size) return fail(VQB_ERR_SHAPE, "state_download: count mismatch");
     memcpy(h, s->a, sizeof(cd) * count);
+    return VQB_OK;
+}
+
+ORC_API int vqcsorc_state_download_range(const ostate *s, uint64_t offset, uint64_t count, cd *h) {
+    if (offset > s->size || count > s->size - offset)
+        return fail(VQB_ERR_INDEX, "state_download_range: range exceeds the state");
+    memcpy(h, s->a + offset, sizeof(cd) * count);
+    return VQB_OK;
+}
+
+ORC_API int vqcsorc_state_set_zero(ostate *s) {
+    memset(s->a, 0, sizeof(cd) * s->size);
+    s->a[0].re = 1.0;
     return VQB_OK;
 }
 

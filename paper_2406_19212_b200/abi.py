@@ -367,6 +367,7 @@ def bind_abi(lib: ct.CDLL, prefix: str) -> None:
         "state_upload": (ct.c_int, [vp, c128_p, u64]),
         "state_download": (ct.c_int, [vp, c128_p, u64]),
         "state_copy": (ct.c_int, [vp, vp]),
+        "state_download_range": (ct.c_int, [vp, u64, u64, c128_p]),
         "apply_gate": (ct.c_int, [vp, op_p]),
         "apply_channel": (ct.c_int, [vp, op_p]),
         "apply_matrix": (ct.c_int, [vp, ct.POINTER(i32), i32, c128_p]),
@@ -397,6 +398,9 @@ def bind_abi(lib: ct.CDLL, prefix: str) -> None:
         "reverse_sweep": (ct.c_int, [vp, vp, ct.POINTER(vqb_rev_step), i64, ct.c_double, dp, i64]),
         # product-only
         "state_wrap": (ct.c_int, [vp, i32, i32, u64, i32, ct.POINTER(vp)]),
+        "alloc_stats": (ct.c_int, [ct.POINTER(i64), ct.POINTER(i64), ct.POINTER(u64), ct.POINTER(u64)]),
+        "reset_alloc_peak": (ct.c_int, []),
+        "release_caches": (ct.c_int, []),
         "state_device_ptr": (ct.c_int, [vp, ct.POINTER(vp)]),
         "state_set_zero": (ct.c_int, [vp]),
         "apply_circuit_unfused": (ct.c_int, [vp, op_p, i64]),
@@ -428,9 +432,9 @@ def bind_abi(lib: ct.CDLL, prefix: str) -> None:
 
 ABI_FUNCTIONS = [
     "last_error", "build_info", "kernel_launch_count", "flop_count", "debug_jit_source", "profile_begin", "profile_end",
-    "state_stream", "state_create", "state_wrap",
+    "state_stream", "alloc_stats", "reset_alloc_peak", "release_caches", "state_create", "state_wrap",
     "state_destroy", "state_info", "state_device_ptr", "state_set_zero", "state_upload",
-    "state_download", "state_copy", "apply_gate", "apply_channel", "apply_matrix",
+    "state_download", "state_download_range", "state_copy", "apply_gate", "apply_channel", "apply_matrix",
     "apply_circuit", "apply_circuit_unfused", "apply_circuit_copy_batch", "norm", "trace", "expectation",
     "apply_operator", "bilinear_form", "reverse_step", "loss_pure", "gradient_pure",
     "loss_mixed", "gradient_mixed", "gate_matrix", "gate_derivative", "gate_inverse",

@@ -97,7 +97,11 @@ bool parallel_adjoint() {
 class GatedSweep {
   public:
     explicit GatedSweep(std::function<void()> sweep) {
-        fut_ = worker().submit([this, sweep = std::move(sweep)] {
+        // the worker drives the caller's device (its buffers and the states'
+        // streams live there)
+        const int dev = current_device();
+        fut_ = worker().submit([this, dev, sweep = std::move(sweep)] {
+            VQB_CUDA(cudaSetDevice(dev));
             g_gate = &gate_;
             struct Reset {
                 ~Reset() { g_gate = nullptr; }
@@ -133,86 +137,99 @@ class GatedSweep {
 };
 
 // Device buffer for the gradient vector and the loss, reused across calls
-// on a thread (grow-only): a cudaMalloc/cudaFree pair per call would cost
-// more than a small gradient (and cudaFree synchronises the device).
+// on a thread (grow-only, per device): a cudaMalloc/cudaFree pair per call
+// would cost more than a small gradient (and cudaFree synchronises the device).
 struct DevBuf {
     void *p = nullptr;
     explicit DevBuf(size_t bytes) {
-        static thread_local void *cached = nullptr;
-        static thread_local size_t cap = 0;
-        if (bytes > cap) {
-            if (cached) cudaFree(cached);
-            cached = nullptr;
-            VQB_CUDA(cudaMalloc(&cached, bytes));
-            cap = bytes;
-        }
-        p = cached;
+        static thread_local DevMem cached;
+        cached.ensure(bytes);
+        p = cached.p;
     }
     template <typename T> T *as() { return static_cast<T *>(p); }
 };
 
-// Working states of the losses / gradients. States up to 2^26 amplitudes
-// (1 GiB) are cached per thread and reused across calls (allocation, stream
-// and workspace setup otherwise dominate small problems such as config 0);
-// larger ones are allocated per call so no large buffer outlives the call.
+// Working states of the losses / gradients, kept for the next call instead
+// of being freed (allocation, stream and workspace setup otherwise dominate
+// small problems such as config 0, and allocating and freeing 2 x 16 GiB per
+// 30-qubit gradient cost 100-500 ms of cudaMalloc/cudaFree against a ~0.8 s
+// gradient). One process-wide pool keyed by (device, shape): any number of
+// states up to 2^26 amplitudes (1 GiB) up to 8 in total, and at most two of
+// one larger shape (<= 2^31 amplitudes: a 30-qubit gradient's Phi and Psi;
+// caching a new large shape drops the old one). Cached states stay counted in
+// vqb_alloc_stats; vqb_release_caches() frees them.
 constexpr uint64_t kCacheLimit = 1ull << 26;
-
-struct ScratchCache {
-    std::vector<DeviceState *> free_list;
-    ~ScratchCache() {
-        for (auto *s : free_list) state_destroy(s);
-    }
-};
-thread_local ScratchCache g_cache;
-
-// Large working states (up to 2^31 amplitudes, two at a time: a 30-qubit
-// gradient's Phi and Psi) are kept too: allocating and freeing 2 x 16 GiB per
-// call cost 100-500 ms of cudaMalloc/cudaFree (page mapping, and cudaFree
-// synchronises the device) against a ~0.8 s gradient.
 constexpr uint64_t kLargeCacheLimit = 1ull << 31;
 constexpr int kLargeCacheCount = 2;
-int large_cached() {
-    int k = 0;
-    for (auto *s : g_cache.free_list) k += s->size > kCacheLimit;
-    return k;
+constexpr size_t kSmallCacheCount = 8;
+
+struct ScratchPool {
+    std::mutex mu;
+    std::vector<DeviceState *> free_list;
+};
+ScratchPool &pool() {
+    static ScratchPool *p = [] {
+        register_cache_release([] {
+            ScratchPool &sp = pool();
+            std::vector<DeviceState *> v;
+            {
+                std::lock_guard<std::mutex> lk(sp.mu);
+                v.swap(sp.free_list);
+            }
+            for (DeviceState *s : v) state_destroy(s);
+        });
+        return new ScratchPool; // never destroyed: states may outlive static teardown
+    }();
+    return *p;
 }
 
 DeviceState *scratch(int n, int mixed) {
     const uint64_t size = 1ull << (mixed ? 2 * n : n);
-    if (size <= kLargeCacheLimit)
-        for (size_t i = 0; i < g_cache.free_list.size(); ++i) {
-            DeviceState *s = g_cache.free_list[i];
-            if (s->n == n && s->mixed == mixed) {
-                g_cache.free_list.erase(g_cache.free_list.begin() + i);
+    const int dev = current_device();
+    if (size <= kLargeCacheLimit) {
+        ScratchPool &sp = pool();
+        std::lock_guard<std::mutex> lk(sp.mu);
+        for (size_t i = 0; i < sp.free_list.size(); ++i) {
+            DeviceState *s = sp.free_list[i];
+            if (s->n == n && s->mixed == mixed && s->device == dev) {
+                sp.free_list.erase(sp.free_list.begin() + i);
                 return s;
             }
         }
+    }
     return state_create(n, mixed);
 }
 
 struct StateGuard {
     DeviceState *s;
     ~StateGuard() {
-        const bool small = s->size <= kCacheLimit && g_cache.free_list.size() < 8;
-        const bool large = s->size > kCacheLimit && s->size <= kLargeCacheLimit;
-        if (large) {
-            // keep the newest shape: drop cached large states of other shapes
-            for (size_t i = 0; i < g_cache.free_list.size();) {
-                DeviceState *c = g_cache.free_list[i];
-                if (c->size > kCacheLimit && (c->n != s->n || c->mixed != s->mixed)) {
-                    state_destroy(c);
-                    g_cache.free_list.erase(g_cache.free_list.begin() + i);
-                } else {
-                    ++i;
+        cudaStreamSynchronize(s->stream);
+        std::vector<DeviceState *> drop;
+        {
+            ScratchPool &sp = pool();
+            std::lock_guard<std::mutex> lk(sp.mu);
+            int small_n = 0, large_n = 0;
+            for (DeviceState *c : sp.free_list) ++(c->size > kCacheLimit ? large_n : small_n);
+            const bool small = s->size <= kCacheLimit && small_n < (int)kSmallCacheCount;
+            const bool large = s->size > kCacheLimit && s->size <= kLargeCacheLimit;
+            if (large) {
+                // keep the newest shape: drop cached large states of other shapes
+                for (size_t i = 0; i < sp.free_list.size();) {
+                    DeviceState *c = sp.free_list[i];
+                    if (c->size > kCacheLimit &&
+                        (c->n != s->n || c->mixed != s->mixed || c->device != s->device)) {
+                        drop.push_back(c);
+                        sp.free_list.erase(sp.free_list.begin() + i);
+                        --large_n;
+                    } else {
+                        ++i;
+                    }
                 }
             }
+            if (small || (large && large_n < kLargeCacheCount)) sp.free_list.push_back(s);
+            else drop.push_back(s);
         }
-        if (small || (large && large_cached() < kLargeCacheCount)) {
-            cudaStreamSynchronize(s->stream);
-            g_cache.free_list.push_back(s);
-        } else {
-            state_destroy(s);
-        }
+        for (DeviceState *d : drop) state_destroy(d);
     }
 };
 

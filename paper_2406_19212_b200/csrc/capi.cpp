@@ -46,6 +46,12 @@ DeviceState *ds(vqb_state *s) {
 }
 DeviceState *ds(const vqb_state *s) { return ds(const_cast<vqb_state *>(s)); }
 
+void same_device(const DeviceState *a, const DeviceState *b) {
+    if (a->device != b->device)
+        raise(VQB_ERR_USAGE, "states on different devices (" + std::to_string(a->device) + " and " +
+                                 std::to_string(b->device) + ")");
+}
+
 void need(const void *p, const char *what) {
     if (!p) raise(VQB_ERR_USAGE, std::string("null argument: ") + what);
 }
@@ -65,6 +71,25 @@ void write_grads(const GradientOut &r, double *loss, double *grads, int64_t cap,
     if (!r.grads.empty()) std::memcpy(grads, r.grads.data(), sizeof(double) * r.grads.size());
     *ng = (int64_t)r.grads.size();
     if (res) *res = r.residual;
+}
+
+// Device states of vqb_apply_circuit_copy_batch, kept for the next call of
+// the same shape; freed by vqb_release_caches().
+struct BatchSlots {
+    std::mutex mu;
+    std::vector<DeviceState *> states;
+};
+BatchSlots &batch_slots() {
+    static BatchSlots *b = [] {
+        register_cache_release([] {
+            BatchSlots &bs = batch_slots();
+            std::lock_guard<std::mutex> lk(bs.mu);
+            for (DeviceState *d : bs.states) state_destroy(d);
+            bs.states.clear();
+        });
+        return new BatchSlots;
+    }();
+    return *b;
 }
 
 } // namespace
@@ -109,6 +134,25 @@ VQB_API int vqb_profile_end(char *buf, int64_t cap) {
     });
 }
 
+VQB_API int vqb_alloc_stats(int64_t *live_states, int64_t *peak_states, uint64_t *live_bytes,
+                            uint64_t *peak_bytes) {
+    return guard([&] {
+        const AllocStats a = alloc_stats();
+        if (live_states) *live_states = a.live_states;
+        if (peak_states) *peak_states = a.peak_states;
+        if (live_bytes) *live_bytes = a.live_bytes;
+        if (peak_bytes) *peak_bytes = a.peak_bytes;
+    });
+}
+
+VQB_API int vqb_reset_alloc_peak(void) {
+    return guard([&] { reset_alloc_peak(); });
+}
+
+VQB_API int vqb_release_caches(void) {
+    return guard([&] { release_caches(); });
+}
+
 VQB_API int vqb_state_stream(const vqb_state *s, void **stream) {
     return guard([&] {
         need(stream, "stream");
@@ -139,6 +183,7 @@ VQB_API int vqb_state_destroy(vqb_state *s) {
 VQB_API int vqb_state_info(const vqb_state *s, int32_t *n, int32_t *mixed, uint64_t *count) {
     return guard([&] {
         const DeviceState *d = ds(s);
+        DevScope on_(d->device);
         if (n) *n = d->n;
         if (mixed) *mixed = d->mixed;
         if (count) *count = d->size;
@@ -149,11 +194,17 @@ VQB_API int vqb_state_device_ptr(const vqb_state *s, void **ptr) {
     return guard([&] { *ptr = ds(s)->amps; });
 }
 
-VQB_API int vqb_state_set_zero(vqb_state *s) { return guard([&] { state_set_zero(ds(s)); }); }
+VQB_API int vqb_state_set_zero(vqb_state *s) {
+    return guard([&] {
+        DevScope on_(ds(s)->device);
+        state_set_zero(ds(s));
+    });
+}
 
 VQB_API int vqb_state_upload(vqb_state *s, const vqb_c128 *host, uint64_t count) {
     return guard([&] {
         DeviceState *d = ds(s);
+        DevScope on_(d->device);
         need(host, "host");
         check_count(d, count, "state_upload");
         VQB_CUDA(cudaMemcpyAsync(d->amps, host, sizeof(double2) * count, cudaMemcpyHostToDevice,
@@ -165,6 +216,7 @@ VQB_API int vqb_state_upload(vqb_state *s, const vqb_c128 *host, uint64_t count)
 VQB_API int vqb_state_download(const vqb_state *s, vqb_c128 *host, uint64_t count) {
     return guard([&] {
         DeviceState *d = ds(s);
+        DevScope on_(d->device);
         need(host, "host");
         check_count(d, count, "state_download");
         VQB_CUDA(cudaMemcpyAsync(host, d->amps, sizeof(double2) * count, cudaMemcpyDeviceToHost,
@@ -173,9 +225,28 @@ VQB_API int vqb_state_download(const vqb_state *s, vqb_c128 *host, uint64_t coun
     });
 }
 
+VQB_API int vqb_state_download_range(const vqb_state *s, uint64_t offset, uint64_t count,
+                                     vqb_c128 *host) {
+    return guard([&] {
+        DeviceState *d = ds(s);
+        DevScope on_(d->device);
+        if (count > 0) need(host, "host");
+        if (offset > d->size || count > d->size - offset)
+            raise(VQB_ERR_INDEX, "state_download_range: range [" + std::to_string(offset) + ", " +
+                                     std::to_string(offset + count) + ") exceeds the state's " +
+                                     std::to_string(d->size) + " amplitudes");
+        if (count == 0) return;
+        VQB_CUDA(cudaMemcpyAsync(host, d->amps + offset, sizeof(double2) * count,
+                                 cudaMemcpyDeviceToHost, d->stream));
+        sync(d);
+    });
+}
+
 VQB_API int vqb_state_copy(vqb_state *dst, const vqb_state *src) {
     return guard([&] {
         DeviceState *a = ds(dst), *b = ds(src);
+        same_device(a, b);
+        DevScope on_(a->device);
         if (a->size != b->size) raise(VQB_ERR_SHAPE, "state_copy: shape mismatch");
         sync(b);
         VQB_CUDA(cudaMemcpyAsync(a->amps, b->amps, sizeof(double2) * b->size,
@@ -187,6 +258,7 @@ VQB_API int vqb_state_copy(vqb_state *dst, const vqb_state *src) {
 VQB_API int vqb_apply_gate(vqb_state *s, const vqb_op *op) {
     return guard([&] {
         DeviceState *d = ds(s);
+        DevScope on_(d->device);
         need(op, "gate");
         const Gate g = gate_from_op(*op);
         check_fit(g.pos, g.m, d->n);
@@ -199,6 +271,7 @@ VQB_API int vqb_apply_gate(vqb_state *s, const vqb_op *op) {
 VQB_API int vqb_apply_channel(vqb_state *s, const vqb_op *op) {
     return guard([&] {
         DeviceState *d = ds(s);
+        DevScope on_(d->device);
         need(op, "channel");
         if (!d->mixed)
             raise(VQB_ERR_TYPE, "apply_channel: a quantum channel cannot act on a pure state");
@@ -212,6 +285,7 @@ VQB_API int vqb_apply_channel(vqb_state *s, const vqb_op *op) {
 VQB_API int vqb_apply_matrix(vqb_state *s, const int32_t *pos, int32_t m, const vqb_c128 *mat) {
     return guard([&] {
         DeviceState *d = ds(s);
+        DevScope on_(d->device);
         need(pos, "positions");
         need(mat, "matrix");
         if (m < 1 || m > VQB_MAX_POSITIONS) raise(VQB_ERR_UNSUPPORTED, "apply_matrix: 1..6 positions");
@@ -228,6 +302,7 @@ VQB_API int vqb_apply_matrix(vqb_state *s, const int32_t *pos, int32_t m, const 
 
 static void apply_circuit_impl(vqb_state *s, const vqb_op *ops, int64_t count, bool fused) {
     DeviceState *d = ds(s);
+        DevScope on_(d->device);
     HostTimer ht_call("apply_circuit (to launch end)");
     if (count > 0) need(ops, "ops");
     std::vector<Element> es;
@@ -282,10 +357,11 @@ VQB_API int vqb_apply_circuit_copy_batch(int32_t num_qubits, int32_t mixed, cons
         // shape (allocating and freeing 3 x 2^n amplitudes per call costs
         // more than a job); a call of another shape releases them first
         constexpr int kSlots = 3;
-        static std::mutex mu;
-        static std::vector<DeviceState *> cache;
-        std::lock_guard<std::mutex> lk(mu);
-        if (!cache.empty() && (cache[0]->n != num_qubits || cache[0]->mixed != (mixed ? 1 : 0))) {
+        BatchSlots &bs = batch_slots();
+        std::lock_guard<std::mutex> lk(bs.mu);
+        std::vector<DeviceState *> &cache = bs.states;
+        if (!cache.empty() && (cache[0]->n != num_qubits || cache[0]->mixed != (mixed ? 1 : 0) ||
+                               cache[0]->device != current_device())) {
             for (DeviceState *d : cache) state_destroy(d);
             cache.clear();
         }
@@ -327,6 +403,7 @@ VQB_API int vqb_apply_circuit_unfused(vqb_state *s, const vqb_op *ops, int64_t c
 VQB_API int vqb_norm(const vqb_state *s, double *out) {
     return guard([&] {
         DeviceState *d = ds(s);
+        DevScope on_(d->device);
         need(out, "out");
         if (d->mixed) raise(VQB_ERR_TYPE, "norm: pure states only (use trace)");
         *out = std::sqrt(norm_sq(d));
@@ -336,6 +413,7 @@ VQB_API int vqb_norm(const vqb_state *s, double *out) {
 VQB_API int vqb_trace(const vqb_state *s, vqb_c128 *out) {
     return guard([&] {
         DeviceState *d = ds(s);
+        DevScope on_(d->device);
         need(out, "out");
         if (!d->mixed) raise(VQB_ERR_TYPE, "trace: mixed states only");
         const cplx t = trace(d);
@@ -348,6 +426,7 @@ VQB_API int vqb_expectation(const vqb_state *s, const vqb_pauli_term *terms, int
                             vqb_c128 *out) {
     return guard([&] {
         DeviceState *d = ds(s);
+        DevScope on_(d->device);
         need(out, "out");
         const PauliPack p = pack_operator(terms, nt, false);
         if (p.max_qubit > d->n)
@@ -363,6 +442,8 @@ VQB_API int vqb_apply_operator(const vqb_state *src, vqb_state *dst, const vqb_p
                                int64_t nt) {
     return guard([&] {
         DeviceState *a = ds(src), *b = ds(dst);
+        same_device(a, b);
+        DevScope on_(a->device);
         if (a->mixed || b->mixed) raise(VQB_ERR_TYPE, "apply_operator: pure states only");
         if (a->size != b->size) raise(VQB_ERR_SHAPE, "apply_operator: shape mismatch");
         if (a == b) raise(VQB_ERR_USAGE, "apply_operator: src and dst must differ");
@@ -385,6 +466,8 @@ VQB_API int vqb_bilinear_form(const vqb_state *bra, const vqb_state *ket, const 
                               int32_t m, const vqb_c128 *local, vqb_c128 *out) {
     return guard([&] {
         DeviceState *a = ds(bra), *b = ds(ket);
+        same_device(a, b);
+        DevScope on_(a->device);
         need(pos, "positions");
         need(local, "local");
         need(out, "out");
@@ -403,6 +486,8 @@ VQB_API int vqb_reverse_step(vqb_state *phi, vqb_state *psi, const int32_t *pos,
                              const vqb_c128 *inv, const vqb_c128 *dmats, int32_t np, vqb_c128 *out) {
     return guard([&] {
         DeviceState *a = ds(phi), *b = ds(psi);
+        same_device(a, b);
+        DevScope on_(a->device);
         need(pos, "positions");
         need(inv, "inv");
         if (np > 0) {
@@ -443,6 +528,7 @@ VQB_API int vqb_loss_pure(const vqb_op *ops, int64_t count, const vqb_pauli_term
                           const vqb_state *s0, double *loss) {
     return guard([&] {
         need(loss, "loss");
+        DevScope on_(ds(s0)->device);
         *loss = loss_pure(ops, count, terms, nt, ds(s0), true);
     });
 }
@@ -451,6 +537,7 @@ VQB_API int vqb_loss_mixed(const vqb_op *ops, int64_t count, const vqb_pauli_ter
                            int64_t nt, const vqb_state *dm0, double *loss) {
     return guard([&] {
         need(loss, "loss");
+        DevScope on_(ds(dm0)->device);
         *loss = loss_mixed(ops, count, terms, nt, ds(dm0), true);
     });
 }
@@ -461,6 +548,7 @@ VQB_API int vqb_gradient_pure(const vqb_op *ops, int64_t count, const vqb_pauli_
     return guard([&] {
         need(loss, "loss");
         need(ng, "num_grads");
+        DevScope on_(ds(s0)->device);
         const auto r = gradient_pure(ops, count, terms, nt, ds(s0), res != nullptr, true);
         if (!r.grads.empty()) need(grads, "grads");
         write_grads(r, loss, grads, cap, ng, res);
@@ -473,6 +561,7 @@ VQB_API int vqb_gradient_mixed(const vqb_op *ops, int64_t count, const vqb_pauli
     return guard([&] {
         need(loss, "loss");
         need(ng, "num_grads");
+        DevScope on_(ds(dm0)->device);
         const auto r = gradient_mixed(ops, count, terms, nt, ds(dm0), res != nullptr, true);
         if (!r.grads.empty()) need(grads, "grads");
         write_grads(r, loss, grads, cap, ng, res);
@@ -484,12 +573,19 @@ VQB_API int vqb_reverse_sweep(vqb_state *phi, vqb_state *psi, const vqb_rev_step
                               int64_t count, double scale, double *grads, int64_t grads_len) {
     return guard([&] {
         DeviceState *a = ds(phi), *b = ds(psi);
+        same_device(a, b);
+        DevScope on_(a->device);
         if (a == b) raise(VQB_ERR_USAGE, "reverse_sweep: phi and psi must be distinct states");
         if (a->size != b->size) raise(VQB_ERR_SHAPE, "reverse_sweep: shape mismatch");
         if (count > 0) need(steps, "steps");
         std::vector<RevOp> prog;
         prog.reserve((size_t)count);
         bool any_param = false;
+        // every step gets private device slots (the executor writes, not
+        // adds, a step's contributions); the host adds them into grads at
+        // grad_index, so steps sharing an index (tied parameters) accumulate
+        int64_t nslots = 0;
+        std::vector<int64_t> dst;
         for (int64_t i = 0; i < count; ++i) {
             const vqb_rev_step &st = steps[i];
             const int m = st.num_positions;
@@ -517,32 +613,28 @@ VQB_API int vqb_reverse_sweep(vqb_state *phi, vqb_state *psi, const vqb_rev_step
                         d[e] = cplx(st.dmats[p * dd + e].re, st.dmats[p * dd + e].im);
                     r.dmats.push_back(std::move(d));
                 }
-                r.grad_base = st.grad_index;
+                r.grad_base = nslots;
+                for (int p = 0; p < st.num_dmats; ++p) dst.push_back(st.grad_index + p);
+                nslots += st.num_dmats;
                 r.scale = scale;
                 any_param = true;
             }
             prog.push_back(std::move(r));
         }
         double *dg = nullptr;
+        static thread_local DevMem slots;
         if (any_param) {
-            VQB_CUDA(cudaMalloc(&dg, sizeof(double) * (size_t)grads_len + 16));
-            VQB_CUDA(cudaMemsetAsync(dg, 0, sizeof(double) * (size_t)grads_len, a->stream));
+            slots.ensure(sizeof(double) * (size_t)nslots + 16);
+            dg = static_cast<double *>(slots.p);
+            VQB_CUDA(cudaMemsetAsync(dg, 0, sizeof(double) * (size_t)nslots, a->stream));
         }
-        struct Free {
-            double *p;
-            ~Free() {
-                if (p) cudaFree(p);
-            }
-        } free_dg{dg};
         sync(b);
         run_reverse(a, b, prog, dg, true);
         sync(a);
         if (any_param) {
-            std::vector<double> h((size_t)grads_len);
-            VQB_CUDA(cudaMemcpy(h.data(), dg, sizeof(double) * (size_t)grads_len,
-                                cudaMemcpyDeviceToHost));
-            for (const RevOp &r : prog)
-                for (size_t p = 0; p < r.dmats.size(); ++p) grads[r.grad_base + p] += h[r.grad_base + p];
+            std::vector<double> h((size_t)nslots);
+            VQB_CUDA(cudaMemcpy(h.data(), dg, sizeof(double) * (size_t)nslots, cudaMemcpyDeviceToHost));
+            for (int64_t k = 0; k < nslots; ++k) grads[dst[(size_t)k]] += h[(size_t)k];
         }
     });
 }
@@ -561,6 +653,7 @@ VQB_API int vqb_measure(vqb_state *s, int32_t qubit, double uniform, int32_t *ou
                         double *probability) {
     return guard([&] {
         DeviceState *d = ds(s);
+        DevScope on_(d->device);
         need(outcome, "outcome");
         need(probability, "probability");
         check_qubit(d, qubit);
@@ -580,6 +673,7 @@ VQB_API int vqb_measure(vqb_state *s, int32_t qubit, double uniform, int32_t *ou
 VQB_API int vqb_measure_probability(const vqb_state *s, int32_t qubit, double *p1) {
     return guard([&] {
         DeviceState *d = ds(s);
+        DevScope on_(d->device);
         need(p1, "p1");
         check_qubit(d, qubit);
         *p1 = prob_one(d, qubit);
@@ -589,6 +683,7 @@ VQB_API int vqb_measure_probability(const vqb_state *s, int32_t qubit, double *p
 VQB_API int vqb_collapse(vqb_state *s, int32_t qubit, int32_t outcome, double probability) {
     return guard([&] {
         DeviceState *d = ds(s);
+        DevScope on_(d->device);
         check_qubit(d, qubit);
         if (outcome != 0 && outcome != 1) raise(VQB_ERR_DOMAIN, "collapse: outcome must be 0 or 1");
         if (!(probability > 0)) raise(VQB_ERR_DEGENERATE, "collapse: outcome probability must be > 0");
@@ -600,6 +695,7 @@ VQB_API int vqb_collapse(vqb_state *s, int32_t qubit, int32_t outcome, double pr
 VQB_API int vqb_state_save(const vqb_state *s, const char *path) {
     return guard([&] {
         need(path, "path");
+        DevScope on_(ds(s)->device);
         state_save(ds(s), path);
     });
 }

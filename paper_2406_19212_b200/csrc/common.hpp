@@ -80,3 +80,50 @@ ProfMark prof_begin(cudaStream_t st);
 void check_launch(const char *what, const ProfMark &m);
 void prof_annotate(const ProfMark &m, double flops, double bytes);
 } // namespace vqb
+
+namespace vqb {
+// ---- devices and device memory (memory.cpp) ----
+constexpr int kMaxDevices = 16;
+int current_device();
+// Makes `dev` the calling thread's current device for the scope (no-op when
+// it already is); every entry point that touches a state opens one on the
+// state's device, so states on several devices can be driven from one thread.
+struct DevScope {
+    int prev = -1;
+    explicit DevScope(int dev);
+    ~DevScope();
+    DevScope(const DevScope &) = delete;
+    DevScope &operator=(const DevScope &) = delete;
+};
+
+// Tracked device allocations: `state` buffers are full amplitude vectors
+// (the reference's AmpBuffer bookkeeping, state.hpp:56-83), the rest scratch.
+void *dev_alloc(size_t bytes, bool state, bool raise_on_fail = true);
+void dev_free(void *p, size_t bytes, bool state);
+struct AllocStats {
+    int64_t live_states, peak_states;
+    uint64_t live_bytes, peak_bytes;
+};
+AllocStats alloc_stats();
+void reset_alloc_peak();
+
+// Grow-only device scratch, one buffer per device (a thread may drive states
+// on several devices). ensure() makes `p` the current device's buffer.
+// Instances register themselves so release_caches() can free every one.
+struct DevMem {
+    void *p = nullptr;
+    void *ptr[kMaxDevices] = {};
+    size_t cap[kMaxDevices] = {};
+    DevMem();
+    ~DevMem();
+    DevMem(const DevMem &) = delete;
+    DevMem &operator=(const DevMem &) = delete;
+    void ensure(size_t bytes);
+    void release();
+};
+// Callbacks run by release_caches() (cached working states, batch slots).
+void register_cache_release(void (*fn)());
+// Frees every cached device buffer of this process (scratch, cached working
+// states); must not run concurrently with other calls.
+void release_caches();
+} // namespace vqb

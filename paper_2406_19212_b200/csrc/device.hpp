@@ -25,6 +25,7 @@ struct DeviceState {
     int mixed = 0;
     int pn = 0;         // pseudo qubits (n, or 2n for a density matrix)
     uint64_t size = 0;  // 2^pn
+    int device = 0;     // CUDA device holding amps (every call runs there)
     bool owned = true;
     uint64_t global_offset = 0;
     int global_qubits = 0;

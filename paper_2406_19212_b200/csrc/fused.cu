@@ -526,19 +526,6 @@ int tile_bits_for(int pn, bool rev) {
     return std::min(kmax, std::max(10, pn - 9));
 }
 
-struct DevMem {
-    void *p = nullptr;
-    size_t cap = 0;
-    void ensure(size_t bytes) {
-        if (bytes <= cap) return;
-        if (p) VQB_CUDA(cudaFree(p));
-        VQB_CUDA(cudaMalloc(&p, bytes));
-        cap = bytes;
-    }
-    ~DevMem() {
-        if (p) cudaFree(p);
-    }
-};
 
 size_t smem_bytes(bool rev, int k, int nops, int nslots) {
     const int tsize = 1 << k;

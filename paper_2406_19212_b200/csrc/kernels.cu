@@ -566,8 +566,10 @@ void upload_operator(DeviceState *s, const PauliPack &p) {
     const size_t tb = sizeof(PauliTermDev) * p.terms.size();
     const size_t need = gb + tb + 16;
     if (need > s->ws.terms_bytes) {
-        if (s->ws.terms) VQB_CUDA(cudaFree(s->ws.terms));
-        VQB_CUDA(cudaMalloc(&s->ws.terms, need));
+        if (s->ws.terms) dev_free(s->ws.terms, s->ws.terms_bytes, false);
+        s->ws.terms = nullptr;
+        s->ws.terms_bytes = 0;
+        s->ws.terms = dev_alloc(need, false);
         s->ws.terms_bytes = need;
     }
     std::vector<char> buf(gb + tb);
@@ -982,11 +984,13 @@ struct PinnedResults {
 };
 static thread_local PinnedResults g_pinned;
 
+constexpr size_t kWorkspaceBytes =
+    sizeof(double2) * kMaxReduceBlocks * kMaxReduceSlots + sizeof(double2) * 64 + 64;
+
 static void alloc_workspace(DeviceState *s) {
     // one device allocation: partials | result | counter
     const size_t pb = sizeof(double2) * kMaxReduceBlocks * kMaxReduceSlots;
-    char *base = nullptr;
-    VQB_CUDA(cudaMalloc(&base, pb + sizeof(double2) * 64 + 64));
+    char *base = static_cast<char *>(dev_alloc(kWorkspaceBytes, false));
     s->ws.partials = reinterpret_cast<double2 *>(base);
     s->ws.result = reinterpret_cast<double2 *>(base + pb);
     s->ws.counter = reinterpret_cast<unsigned *>(base + pb + sizeof(double2) * 64);
@@ -1006,10 +1010,10 @@ DeviceState *state_create(int n, int mixed) {
     s->mixed = mixed ? 1 : 0;
     s->pn = mixed ? 2 * n : n;
     s->size = 1ull << s->pn;
+    s->device = current_device();
     VQB_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
-    const cudaError_t e = cudaMalloc(&s->amps, sizeof(double2) * s->size);
-    if (e != cudaSuccess) {
-        cudaGetLastError();
+    s->amps = static_cast<double2 *>(dev_alloc(sizeof(double2) * s->size, true, false));
+    if (!s->amps) {
         cudaStreamDestroy(s->stream);
         delete s;
         raise(VQB_ERR_SIZE, "state: cannot allocate 2^" + std::to_string(mixed ? 2 * n : n) +
@@ -1021,6 +1025,11 @@ DeviceState *state_create(int n, int mixed) {
 }
 
 DeviceState *state_wrap(void *ptr, int n, int mixed, uint64_t global_offset, int global_qubits) {
+    cudaPointerAttributes attr{};
+    VQB_CUDA(cudaPointerGetAttributes(&attr, ptr));
+    if (attr.type != cudaMemoryTypeDevice && attr.type != cudaMemoryTypeManaged)
+        raise(VQB_ERR_USAGE, "state_wrap: pointer is not device memory");
+    DevScope on(attr.device);
     auto *s = new DeviceState();
     s->n = n;
     s->mixed = mixed ? 1 : 0;
@@ -1028,6 +1037,7 @@ DeviceState *state_wrap(void *ptr, int n, int mixed, uint64_t global_offset, int
     s->size = 1ull << s->pn;
     s->amps = static_cast<double2 *>(ptr);
     s->owned = false;
+    s->device = attr.device;
     s->global_offset = global_offset;
     s->global_qubits = global_qubits;
     VQB_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
@@ -1046,11 +1056,15 @@ void state_set_zero(DeviceState *s) {
 
 void state_destroy(DeviceState *s) {
     if (!s) return;
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != s->device) cudaSetDevice(s->device);
     cudaStreamSynchronize(s->stream);
-    if (s->owned && s->amps) cudaFree(s->amps);
-    cudaFree(s->ws.partials); // partials | result | counter are one allocation
-    if (s->ws.terms) cudaFree(s->ws.terms);
+    if (s->owned && s->amps) dev_free(s->amps, sizeof(double2) * s->size, true);
+    dev_free(s->ws.partials, kWorkspaceBytes, false); // partials | result | counter: one allocation
+    if (s->ws.terms) dev_free(s->ws.terms, s->ws.terms_bytes, false);
     cudaStreamDestroy(s->stream);
+    if (cur >= 0 && cur != s->device) cudaSetDevice(cur);
     delete s;
 }
 

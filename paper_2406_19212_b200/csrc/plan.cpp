@@ -73,6 +73,79 @@ FusedOp analyse(const int *pos1, int m, const std::vector<const cvec *> &mats) {
 
 } // namespace
 
+int entry_class(const cplx &v) {
+    const double re = v.real(), im = v.imag();
+    if (im == 0.0) {
+        if (re == 0.0) return 0;
+        if (re == 1.0) return 4;
+        if (re == -1.0) return 5;
+        return 1;
+    }
+    if (re == 0.0) {
+        if (im == 1.0) return 6;
+        if (im == -1.0) return 7;
+        return 2;
+    }
+    return 3;
+}
+
+double subs_cost(const cplx *sub, int nt, int nc) {
+    const int D = 1 << nt, dd = D * D;
+    double total = 0;
+    for (int c = 0; c < (1 << nc); ++c) {
+        const cplx *M = sub + size_t(c) * dd;
+        bool ident = true;
+        for (int r = 0; r < D && ident; ++r)
+            for (int col = 0; col < D; ++col)
+                if (M[r + col * D] != (r == col ? cplx(1) : cplx(0))) {
+                    ident = false;
+                    break;
+                }
+        if (ident) continue;
+        for (int r = 0; r < D; ++r) {
+            bool first = true;
+            for (int col = 0; col < D; ++col) {
+                const int k = entry_class(M[r + col * D]);
+                if (k == 0) continue;
+                if (first) total += (k >= 4 ? 0 : (k == 3 ? 4 : 2));
+                else total += (k == 3 ? 4 : 2);
+                first = false;
+            }
+        }
+    }
+    return total / double(D << nc);
+}
+
+void divide_by(cplx *sub, size_t count, const cplx &s) {
+    const double n2 = s.real() * s.real() + s.imag() * s.imag();
+    for (size_t i = 0; i < count; ++i) {
+        const double a = sub[i].real(), b = sub[i].imag();
+        sub[i] = cplx((a * s.real() + b * s.imag()) / n2, (b * s.real() - a * s.imag()) / n2);
+    }
+}
+
+cplx best_scale(const cplx *sub, int nt, int nc, double *cost) {
+    const size_t count = size_t(1) << (2 * nt) << nc;
+    double best = subs_cost(sub, nt, nc);
+    cplx bs = 1.0;
+    std::vector<cplx> tried, tmp(count);
+    for (size_t i = 0; i < count; ++i) {
+        const cplx s = sub[i];
+        if (s == cplx(0) || s == cplx(1)) continue;
+        if (std::find(tried.begin(), tried.end(), s) != tried.end()) continue;
+        tried.push_back(s);
+        std::copy(sub, sub + count, tmp.begin());
+        divide_by(tmp.data(), count, s);
+        const double c = subs_cost(tmp.data(), nt, nc);
+        if (c < best) {
+            best = c;
+            bs = s;
+        }
+    }
+    if (cost) *cost = best;
+    return bs;
+}
+
 FusedOp analyse_gate(const Gate &g) {
     FusedOp f = analyse(g.pos, g.m, {&g.mat});
     f.gate = g;
@@ -151,7 +224,7 @@ struct Block {
 } // namespace
 
 std::vector<const FusedOp *> fuse_blocks_ref(const std::vector<FusedOp> &ops, const std::vector<int> &order,
-                                             int max_support, std::deque<FusedOp> &store) {
+                                             int max_support, std::deque<FusedOp> &store, bool cost_model) {
     max_support = std::min(max_support, kMaxFuse);
     std::vector<Block> blocks;
     blocks.reserve(order.size());
@@ -242,6 +315,34 @@ std::vector<const FusedOp *> fuse_blocks_ref(const std::vector<FusedOp> &ops, co
         if (any_pair) {
             embed_mul(pair ? f.rev->psi_op.mat.data() : g.mat.data(), P, np, U, nu, acc_psi, tmp);
             std::copy(tmp, tmp + du * du, acc_psi);
+        }
+        if (cost_model && !any_pair) {
+            // merge only if the specialised kernel's cost does not grow
+            auto block_cost = [&](const cplx *M, const int *Ub, int nub) {
+                int pos1[kMaxFuse];
+                for (int i = 0; i < nub; ++i) pos1[i] = Ub[i] + 1;
+                const int dub = 1 << nub;
+                cvec mm(M, M + dub * dub);
+                const FusedOp a = analyse(pos1, nub, {&mm});
+                if (!a.fusable) return 1e30;
+                double c = 0;
+                best_scale(a.sub_phi.data(), a.nt, a.nc, &c);
+                return c;
+            };
+            double parts = 0;
+            for (int k = 0; k < nc; ++k) {
+                const Block &b = blocks[cands[k]];
+                parts += block_cost(src_mat(b, false), b.U, b.nu);
+            }
+            {
+                double c = 0;
+                best_scale(f.sub_phi.data(), f.nt, f.nc, &c);
+                parts += c;
+            }
+            if (block_cost(acc_phi, U, nu) > parts + 1e-9) {
+                fresh(false);
+                continue;
+            }
         }
         const int keep = *std::max_element(cands, cands + nc);
         for (int k = 0; k < nc; ++k)

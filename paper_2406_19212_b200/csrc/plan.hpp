@@ -58,8 +58,30 @@ std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k);
 std::vector<FusedOp> fuse_blocks(const std::vector<FusedOp> &ops, const std::vector<int> &order,
                                  int max_support);
 // The same without copying: unmerged operations are returned as pointers into
-// `ops`, merged blocks are stored in `store` (stable addresses).
+// `ops`, merged blocks are stored in `store` (stable addresses). With
+// `cost_model`, a merge happens only if the merged block's emitted cost
+// (op_cost, after scalar factoring) does not exceed the parts' total: the
+// structure-aware specialised kernels run a sparse fSim or a factored sqrt(X)
+// far cheaper than the dense product of both (the interpreter runs every
+// block dense, so it merges whenever it can).
 std::vector<const FusedOp *> fuse_blocks_ref(const std::vector<FusedOp> &ops, const std::vector<int> &order,
-                                             int max_support, std::deque<FusedOp> &store);
+                                             int max_support, std::deque<FusedOp> &store,
+                                             bool cost_model = false);
+
+// ---- emitted-cost model of the structure-aware specialised kernels ----
+// Entry class: 0 zero, 1 real, 2 imaginary, 3 complex, 4 exactly +1,
+// 5 exactly -1, 6 exactly +i, 7 exactly -i.
+int entry_class(const cplx &v);
+// FP64 instructions per amplitude of an op's register code: per output row
+// the first nonzero term costs 0 (unit), 2 (real/imaginary) or 4 (complex)
+// instructions, every further term 2 (unit, real, imaginary) or 4; identity
+// sub-matrices cost nothing. Averaged over rows and condition values.
+double subs_cost(const cplx *sub, int nt, int nc);
+// The scalar s (a nonzero entry, or 1) minimising subs_cost(sub / s); its
+// cost in *cost. Dividing every sub-matrix by s is exact for the entries
+// equal to s (they become exactly 1).
+cplx best_scale(const cplx *sub, int nt, int nc, double *cost);
+// sub / s entry by entry (textbook complex division, so x / x == 1 exactly)
+void divide_by(cplx *sub, size_t count, const cplx &s);
 
 } // namespace vqb

@@ -835,7 +835,18 @@ int env_int(const char *name, int dflt);
 // must run in a following launch with the same tile bits.
 void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks,
                      std::vector<int> &remaining, int pn, bool rev, RParams &P, SlotMap &slots,
-                     bool regwide = false, bool gdiff = false) {
+                     bool regwide = false, bool gdiff = false, bool factor = false) {
+    // Scalar factoring (forward, specialised kernels): every register op's
+    // matrices are divided by the scalar that makes the most entries exact
+    // units (sqrt(X) = e^{i pi/4}/sqrt2 [[1, -i], [-i, 1]]: adds only; a
+    // rotation diag(e^{-it/2}, e^{it/2}) = e^{-it/2} diag(1, e^{it}): half the
+    // elements untouched); the scalars' product is applied once at the end
+    // of the launch by one extra op (a 1x1 "diagonal" without conditions).
+    // Results equal the unfactored product up to rounding.
+    factor = factor && !rev;
+    cplx scale = 1.0;
+    const int ops_cap = factor ? kMaxOps - 1 : kMaxOps;
+    const int pool_cap = factor ? kMaxPool - 1 : kMaxPool;
     std::memset(&P, 0, sizeof P);
     for (int j = 0; j < K; ++j) P.bits[j] = sg.bits[j];
     P.ntiles = 1ull << (pn - K);
@@ -885,8 +896,8 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
             const FusedOp &f = *blocks[i];
             const unsigned mix = mixmask(f);
             const int nx = count_x(f);
-            const bool fits_res = nops + ops_used < kMaxOps &&
-                                  npool + pool_used + pool_need(f) <= kMaxPool &&
+            const bool fits_res = nops + ops_used < ops_cap &&
+                                  npool + pool_used + pool_need(f) <= pool_cap &&
                                   nslots + slots_used + (rev ? f.np : 0) <= kMaxSlots &&
                                   P.nxpat + xp_used + nx <= 256;
             if ((f.support & blocked) || __builtin_popcount(rset | mix) > RB || !fits_res) {
@@ -1064,6 +1075,15 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
                 };
                 o.mat = pushx(f.sub_phi, &o.ident);
                 if (f.pair) o.mat_psi = pushx(f.sub_psi, &o.ident_psi);
+            } else if (factor && !f.pair) {
+                cvec sub = f.sub_phi;
+                double c = 0;
+                const cplx sc = best_scale(sub.data(), f.nt, f.nc, &c);
+                if (sc != cplx(1)) {
+                    divide_by(sub.data(), sub.size(), sc);
+                    scale *= sc;
+                }
+                o.mat = push(sub, 0, &o.ident);
             } else {
                 o.mat = push(f.sub_phi, 0, &o.ident);
                 if (f.pair) o.mat_psi = push(f.sub_psi, 0, &o.ident_psi);
@@ -1155,20 +1175,19 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
         sb.op_count = nops - sb.op_begin;
         remaining.swap(deferred);
     }
+    if (factor && scale != cplx(1) && P.nsubs > 0) {
+        // the factored scalars, once per amplitude, in the last sub-stage
+        ROp &o = P.ops[nops++];
+        o.tab = o.tab_psi = -1;
+        o.mat = (unsigned)npool;
+        P.pool[npool++] = make_double2(scale.real(), scale.imag());
+        P.fast[nops - 1] = 0;
+        ++P.subs[P.nsubs - 1].op_count;
+    }
     P.nslots = nslots;
     P.npool = npool;
 }
 
-struct DevMem {
-    void *p = nullptr;
-    size_t cap = 0;
-    void ensure(size_t bytes) {
-        if (bytes <= cap) return;
-        if (p) VQB_CUDA(cudaFree(p));
-        VQB_CUDA(cudaMalloc(&p, bytes));
-        cap = bytes;
-    }
-};
 
 int env_int(const char *name, int dflt) {
     const char *v = std::getenv(name);
@@ -1238,6 +1257,26 @@ int pool_cls(const RParams &P, unsigned off, int count, int stride) {
     return c;
 }
 
+// pool_cls extended by the unit classes of entry_class (4: +1, 5: -1, 6: +i,
+// 7: -i) when every selected entry is the same unit: those terms are adds
+// (or plain copies as a row's first term), no multiplications
+int pool_ucls(const RParams &P, unsigned off, int count, int stride) {
+    int u = -1;
+    for (int k = 0; k < count; ++k) {
+        const double2 v = P.pool[off + (unsigned)(k * stride)];
+        const int c = entry_class(cplx(v.x, v.y));
+        if (c < 4 || (u >= 0 && u != c)) return pool_cls(P, off, count, stride);
+        u = c;
+    }
+    return u < 0 ? 0 : u;
+}
+// class of a term that may take either of two entries (a run-time choice)
+int merge_cls(int a, int b) {
+    if (a == b) return a;
+    auto bits = [](int c) { return c < 4 ? c : (c <= 5 ? 1 : 2); };
+    return bits(a) | bits(b);
+}
+
 // acc (=|+=) m * x for an entry of class cls; adds the FP64 flops per thread
 std::string cterm(const std::string &m, const std::string &x, const std::string &acc, int cls, bool first,
                   double &fl) {
@@ -1254,6 +1293,22 @@ std::string cterm(const std::string &m, const std::string &x, const std::string 
         return first ? "        " + acc + " = make_double2(-" + m + ".y * " + x + ".y, " + m + ".y * " + x + ".x);\n"
                      : "        " + acc + ".x = fma(-" + m + ".y, " + x + ".y, " + acc + ".x); " + acc + ".y = fma(" +
                            m + ".y, " + x + ".x, " + acc + ".y);\n";
+    case 4: // +1
+        if (first) return "        " + acc + " = " + x + ";\n";
+        fl += 2;
+        return "        " + acc + ".x += " + x + ".x; " + acc + ".y += " + x + ".y;\n";
+    case 5: // -1
+        if (first) return "        " + acc + " = make_double2(-" + x + ".x, -" + x + ".y);\n";
+        fl += 2;
+        return "        " + acc + ".x -= " + x + ".x; " + acc + ".y -= " + x + ".y;\n";
+    case 6: // +i
+        if (first) return "        " + acc + " = make_double2(-" + x + ".y, " + x + ".x);\n";
+        fl += 2;
+        return "        " + acc + ".x -= " + x + ".y; " + acc + ".y += " + x + ".x;\n";
+    case 7: // -i
+        if (first) return "        " + acc + " = make_double2(" + x + ".y, -" + x + ".x);\n";
+        fl += 2;
+        return "        " + acc + ".x += " + x + ".y; " + acc + ".y -= " + x + ".x;\n";
     default:
         fl += 8;
         return first ? "        " + acc + " = cmul(" + m + ", " + x + ");\n"
@@ -1772,10 +1827,13 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
             for (int q = 0; q < op.nc; ++q)
                 if (op.ck[q] == 2) rmask |= 1 << q;
             auto ecls = [&](unsigned off, int cs, int k) {
-                int c = 0;
+                int c = -1;
                 for (int cc = 0; cc < (1 << op.nc); ++cc)
-                    if ((cc & rmask) == cs) c |= pool_cls(P, off + (unsigned)(cc * dd + k), 1, 0);
-                return c;
+                    if ((cc & rmask) == cs) {
+                        const int e = pool_ucls(P, off + (unsigned)(cc * dd + k), 1, 0);
+                        c = c < 0 ? e : merge_cls(c, e);
+                    }
+                return c < 0 ? 0 : c;
             };
             const int D = 1 << op.nt;
             if (dyn.empty()) {
@@ -1788,7 +1846,7 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
                     const unsigned base_off = op.mat + (unsigned)(c * dd);
                     emit(mv_code(
                         "v", idx, D, [&](int k) { return MP + "[" + std::to_string(base_off + (unsigned)k) + "]"; },
-                        [&](int k) { return pool_cls(P, base_off + (unsigned)k, 1, 0); }, fl));
+                        [&](int k) { return pool_ucls(P, base_off + (unsigned)k, 1, 0); }, fl));
                 }
                 continue;
             }
@@ -2479,12 +2537,12 @@ std::string shape_key(const RParams &P, bool rev) {
     // per-entry structure of the matrices (zero / real / imaginary / complex,
     // pool_cls): the generated code depends on it, the values themselves not
     {
-        std::string cls((size_t)(P.npool + 3) / 4, '\0');
+        std::string cls((size_t)(P.npool + 1) / 2, '\0');
         for (int i = 0; i < P.npool; ++i)
-            cls[(size_t)i >> 2] = (char)(cls[(size_t)i >> 2] | (pool_cls(P, (unsigned)i, 1, 0) << (2 * (i & 3))));
+            cls[(size_t)i >> 1] = (char)(cls[(size_t)i >> 1] | (pool_ucls(P, (unsigned)i, 1, 0) << (4 * (i & 1))));
         key += cls;
     }
-    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_JIT_WIDE_PARAM", "VQB_WIDE_REGS", "VQB_JIT_GDIFF", "VQB_JIT_ACCBATCH", "VQB_JIT_STASH", "VQB_JIT_SHUFFLE", "VQB_STABLE_LAYOUT", "VQB_JIT_REDLANES", "VQB_JIT_DIRECT"}) {
+    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_JIT_WIDE_PARAM", "VQB_WIDE_REGS", "VQB_JIT_GDIFF", "VQB_JIT_ACCBATCH", "VQB_JIT_STASH", "VQB_JIT_SHUFFLE", "VQB_STABLE_LAYOUT", "VQB_JIT_REDLANES", "VQB_JIT_DIRECT", "VQB_JIT_FACTOR"}) {
         const char *v = std::getenv(e);
         key += '|';
         if (v) key += v;
@@ -2565,6 +2623,10 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
         VQB_CUDA(cudaMemsetAsync(m_slotsum.p, 0, sizeof(double) * total_slots, st));
         if (use_jit) m_jpartial.ensure(jpartial_bytes);
     }
+    // structure-aware kernels: merge blocks only where the emitted cost does
+    // not grow, factor scalars out of the forward matrices (VQB_JIT_FACTOR=0:
+    // merge whenever possible, no factoring)
+    const bool cost_fusion = use_jit && !REV && env_int("VQB_JIT_FACTOR", 1) != 0;
     bool batching = false;
     std::vector<Action> pending;
     auto issue = [&](Action &act) {
@@ -2663,7 +2725,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
         }
         std::vector<const FusedOp *> blocks;
         HostAcc ha_f(&t_fuse);
-        if (max_support > 0) blocks = fuse_blocks_ref(fops, sg.ops, max_support, fused_store);
+        if (max_support > 0) blocks = fuse_blocks_ref(fops, sg.ops, max_support, fused_store, cost_fusion);
         else
             for (int idx : sg.ops) blocks.push_back(&fops[idx]);
         std::vector<int> remaining(blocks.size());
@@ -2675,7 +2737,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             {
                 HostAcc ha(&t_lower);
                 lower_stage_reg(sg, blocks, remaining, pn, REV, P, slots, regwide,
-                                use_jit && env_int("VQB_JIT_GDIFF", 1) != 0);
+                                use_jit && env_int("VQB_JIT_GDIFF", 1) != 0, cost_fusion);
             }
             P.partial_ld = total_slots;
             if (stats) {

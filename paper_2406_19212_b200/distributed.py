@@ -107,8 +107,11 @@ class ShardedState:
         self.log2phys = list(range(n))  # logical qubit (0-based) -> physical bit
         self.chunk = chunk_amps
         self.followers: list = []  # extra shards (the adjoint costate) sharing the qubit map
-        self.swaps = 0
-        self.bytes_exchanged = 0
+        self.swaps = 0              # exchange rounds
+        self.swapped_bits = 0       # global<->local bit exchanges over all rounds
+        self.bytes_exchanged = 0    # sent by this rank
+        self.max_buffer_amps = 0    # largest single transfer buffer
+        self.inflight_amps = 0      # most receive-buffer amplitudes in flight at once
         self._gate_matrix = engine.gate_matrix
 
     # ---------------------------------------------------------------- init / io
@@ -139,51 +142,137 @@ class ShardedState:
         return phys[pidx]
 
     # ---------------------------------------------------------------- swaps
-    def _swap(self, gpos: int, lpos: int) -> None:
-        """Exchange physical global bit gpos (>= n_loc) with local bit lpos."""
+    def _chunks(self, view, limit: int):
+        """Index tuples that cut a (strided) view into pieces of at most
+        `limit` elements: split the outermost dimension whose inner block
+        fits, iterate over every index of the dimensions before it."""
+        import itertools
+        dims = list(view.shape)
+        inner = 1
+        d = len(dims)
+        while d > 0 and inner * dims[d - 1] <= limit:
+            inner *= dims[d - 1]
+            d -= 1
+        if d == 0:
+            yield ()
+            return
+        step = max(1, limit // inner)
+        for head in itertools.product(*[range(x) for x in dims[:d - 1]]):
+            for a in range(0, dims[d - 1], step):
+                yield head + (slice(a, min(dims[d - 1], a + step)),)
+
+    def _swap_many(self, pairs) -> None:
+        """Exchange k physical global bits with k local bits in one all-to-all
+        round (pairs = [(global bit, local bit), ...], k <= g).
+
+        Rank r with value a on the global bits G exchanges, for every b != a,
+        its amplitudes whose local bits L equal b with the rank r' (G bits = b)
+        amplitudes whose L bits equal a; those land in the slots with L bits
+        = b. All 2^k - 1 partners are served by one grouped send/recv per
+        chunk. Every transfer buffer is bounded: the receive buffers of one
+        round in flight (two chunk generations x partners) hold at most
+        `chunk_amps` amplitudes together, the send staging as much."""
         import torch
-        j = gpos - self.n_loc
-        partner = self.rank ^ (1 << j)
-        mine = (self.rank >> j) & 1
-        # local amplitudes with bit lpos == 1 - mine go to the partner, which
-        # sends back its amplitudes with bit lpos == mine
+        pairs = sorted(pairs, key=lambda p: p[1])
+        k = len(pairs)
+        G = [gp - self.n_loc for gp, _ in pairs]
+        L = [lp for _, lp in pairs]
+        a = sum(((self.rank >> G[i]) & 1) << i for i in range(k))
+        partners = []
+        for b in range(1 << k):
+            if b == a:
+                continue
+            r2 = self.rank
+            for i in range(k):
+                r2 = (r2 & ~(1 << G[i])) | (((b >> i) & 1) << G[i])
+            partners.append((b, r2))
+        per = max(1, self.chunk // (2 * len(partners)))  # two generations in flight
+        # shard viewed with one dimension of size 2 per local bit in L
+        # (ascending), rest dims in between: [hi, 2, mid_{k-1}, ..., 2, lo]
+        shape = []
+        prev = self.n_loc
+        for l in reversed(L):
+            shape += [1 << (prev - l - 1), 2]
+            prev = l
+        shape.append(1 << prev)
+
+        def select(v, b):
+            # index the "2" dims (positions 1, 3, ...) with b's bits (high L first)
+            idx = []
+            for j, l in enumerate(reversed(L)):
+                bit = (b >> (k - 1 - j)) & 1
+                idx += [slice(None), bit]
+            return v[tuple(idx)]
+
         for shard in [self.local] + self.followers:
-            v = shard.view(-1, 2, 1 << lpos)  # [hi, bit lpos, lo]
-            send_half = v[:, 1 - mine, :]
-            hi, lo = v.shape[0], v.shape[2]
-            rows_per_chunk = max(1, self.chunk // lo)
-            # two chunks in flight: chunk k+1's transfer overlaps chunk k's
-            # copy into place (a chunk is overwritten only after its own send
-            # completed; the send reads the shard directly when the half is
-            # contiguous, lpos = top local bit)
+            v = shard.view(*shape)
+            views = [(select(v, b), r2) for b, r2 in partners]
+            slices = list(self._chunks(views[0][0], per))
             pending = []
 
             def finish(item):
-                reqs, rbuf, a, b = item
+                reqs, bufs = item
                 for req in reqs:
                     req.wait()
-                send_half[a:b] = torch.view_as_complex(rbuf)
+                for (dst, sl), rbuf in bufs:
+                    dst[sl] = torch.view_as_complex(rbuf).view(dst[sl].shape)
 
-            for r0 in range(0, hi, rows_per_chunk):
-                r1 = min(hi, r0 + rows_per_chunk)
-                sbuf = torch.view_as_real(send_half[r0:r1].contiguous())
-                rbuf = torch.empty_like(sbuf)
-                reqs = []
-                if self.world > 1:
-                    ops = [self.dist.P2POp(self.dist.isend, sbuf, partner),
-                           self.dist.P2POp(self.dist.irecv, rbuf, partner)]
-                    reqs = self.dist.batch_isend_irecv(ops)
-                pending.append((reqs, rbuf, r0, r1))
-                self.bytes_exchanged += sbuf.numel() * 8
+            for sl in slices:
+                ops, bufs = [], []
+                for dst, r2 in views:
+                    sbuf = torch.view_as_real(dst[sl].contiguous()).reshape(-1)
+                    rbuf = torch.empty_like(sbuf)
+                    self.max_buffer_amps = max(self.max_buffer_amps, rbuf.numel() // 2)
+                    if self.world > 1:
+                        ops += [self.dist.P2POp(self.dist.isend, sbuf, r2),
+                                self.dist.P2POp(self.dist.irecv, rbuf, r2)]
+                    else:
+                        rbuf.copy_(sbuf)
+                    bufs.append(((dst, sl), rbuf.view(-1, 2)))
+                    self.bytes_exchanged += sbuf.numel() * 8
+                reqs = self.dist.batch_isend_irecv(ops) if ops else []
+                pending.append((reqs, bufs))
+                self.inflight_amps = max(self.inflight_amps,
+                                         sum(rb.numel() // 2 for _, b in pending for _, rb in b))
                 if len(pending) == 2:
                     finish(pending.pop(0))
             for item in pending:
                 finish(item)
-        # logical qubits on the two physical bits trade places
-        a = self.log2phys.index(gpos)
-        b = self.log2phys.index(lpos)
-        self.log2phys[a], self.log2phys[b] = lpos, gpos
+        # logical qubits on the exchanged physical bits trade places
+        for gp, lp in pairs:
+            x = self.log2phys.index(gp)
+            y = self.log2phys.index(lp)
+            self.log2phys[x], self.log2phys[y] = lp, gp
         self.swaps += 1
+        self.swapped_bits += k
+
+    def _swap(self, gpos: int, lpos: int) -> None:
+        """Exchange physical global bit gpos (>= n_loc) with local bit lpos."""
+        self._swap_many([(gpos, lpos)])
+
+    def _bring_local(self, need_global, upcoming, avoid) -> None:
+        """Swap the global physical bits `need_global` local in one round,
+        together with every other global bit a mixing operation in
+        `upcoming` (phys-bit sets, program order) needs, as long as free local
+        bits remain. Local partners: bits not in `avoid` and unused by the
+        upcoming operations, highest first (long contiguous runs)."""
+        soon = set()
+        for bits in upcoming:
+            soon.update(bits)
+        want = list(dict.fromkeys(need_global))
+        for bits in upcoming:
+            for b in bits:
+                if b >= self.n_loc and b not in want:
+                    want.append(b)
+        free = [l for l in range(self.n_loc - 1, -1, -1) if l not in avoid and l not in soon]
+        rest = [l for l in range(self.n_loc - 1, -1, -1) if l not in avoid and l in soon]
+        pairs = []
+        for gb in want:
+            if free:
+                pairs.append((gb, free.pop(0)))
+            elif gb in need_global and rest:
+                pairs.append((gb, rest.pop(0)))
+        self._swap_many(pairs)
 
     # ---------------------------------------------------------------- circuits
     def _flush(self, batch: List[LocalOp]) -> None:
@@ -203,18 +292,17 @@ class ShardedState:
             m = len(e.positions)
             phys = [self.log2phys[p - 1] for p in e.positions]
             mix = _mixing_bits(mat, m)
-            for b in mix:
-                if phys[b] >= self.n_loc:
-                    # bring it local: pick a local bit this gate does not use,
-                    # preferring one not needed by the next gates
-                    self._flush(batch)
-                    soon = set()
-                    for f in elems[idx + 1: idx + 1 + lookahead]:
-                        soon.update(self.log2phys[p - 1] for p in f.positions)
-                    cands = [l for l in range(self.n_loc - 1, -1, -1) if l not in phys]
-                    pick = next((l for l in cands if l not in soon), cands[0])
-                    self._swap(phys[b], pick)
-                    phys = [self.log2phys[p - 1] for p in e.positions]
+            need = [phys[b] for b in mix if phys[b] >= self.n_loc]
+            if need:
+                # one all-to-all round brings this gate's global mixing bits
+                # local, plus those of the next gates while free local bits last
+                self._flush(batch)
+                upcoming = []
+                for f in elems[idx + 1: idx + 1 + lookahead]:
+                    fm = _mixing_bits(self._gate_matrix(f), len(f.positions))
+                    upcoming.append([self.log2phys[f.positions[b] - 1] for b in fm])
+                self._bring_local(need, upcoming, set(phys))
+                phys = [self.log2phys[p - 1] for p in e.positions]
             fixed = {b: (self.rank >> (phys[b] - self.n_loc)) & 1
                      for b in range(m) if phys[b] >= self.n_loc}
             sub = _restrict(mat, m, fixed) if fixed else mat.reshape(1 << m, 1 << m, order="F")
@@ -250,13 +338,12 @@ class ShardedState:
         # every qubit carrying an X or Y factor in any term must be local; swap
         # global ones with local bits whose qubits carry no X/Y factor at all
         xy = {q - 1 for t in op.terms for q, l in t.factors if str(l).lower() in "xy"}
-        for q in sorted(xy):
-            if self.log2phys[q] >= self.n_loc:
-                cands = [b for b in range(self.n_loc - 1, -1, -1)
-                         if self.log2phys.index(b) not in xy]
-                if not cands:
-                    raise UnsupportedError("expectation: too many X/Y qubits for the local shard")
-                self._swap(self.log2phys[q], cands[0])
+        need = [self.log2phys[q] for q in sorted(xy) if self.log2phys[q] >= self.n_loc]
+        if need:
+            cands = [b for b in range(self.n_loc - 1, -1, -1) if self.log2phys.index(b) not in xy]
+            if len(cands) < len(need):
+                raise UnsupportedError("expectation: too many X/Y qubits for the local shard")
+            self._swap_many(list(zip(need, cands)))
         local_terms = []
         for t in op.terms:
             sign = 1
@@ -334,17 +421,19 @@ class ShardedState:
                 for d in dmats:
                     mix.update(_mixing_bits(d, m))
                 phys = [self.log2phys[p - 1] for p in e.positions]
-                for b in sorted(mix):
-                    if phys[b] >= self.n_loc:
-                        self.engine.reverse_sweep(self, psi, steps, grads)
-                        steps = []
-                        soon = set()
-                        for f in elems[max(0, i - lookahead): i]:
-                            soon.update(self.log2phys[p - 1] for p in f.positions)
-                        cands = [l for l in range(self.n_loc - 1, -1, -1) if l not in phys]
-                        pick = next((l for l in cands if l not in soon), cands[0])
-                        self._swap(phys[b], pick)
-                        phys = [self.log2phys[p - 1] for p in e.positions]
+                need = [phys[b] for b in sorted(mix) if phys[b] >= self.n_loc]
+                if need:
+                    self.engine.reverse_sweep(self, psi, steps, grads)
+                    steps = []
+                    upcoming = []
+                    for f in reversed(elems[max(0, i - lookahead): i]):
+                        fm = set(_mixing_bits(self.engine.gate_inverse(f), len(f.positions)))
+                        for p_ in range(len(f.is_param)):
+                            if f.is_param[p_]:
+                                fm.update(_mixing_bits(self.engine.gate_derivative(f, p_), len(f.positions)))
+                        upcoming.append([self.log2phys[f.positions[b] - 1] for b in sorted(fm)])
+                    self._bring_local(need, upcoming, set(phys))
+                    phys = [self.log2phys[p - 1] for p in e.positions]
                 st = self._local_step(inv, dmats, list(e.positions))
                 if st is not None:
                     steps.append((st[0], st[1], st[2], base[i]))
@@ -384,12 +473,16 @@ class DeviceEngine:
         s.free()
 
     def local_norm_sq(self, st: ShardedState) -> float:
+        import torch
+        torch.cuda.current_stream().synchronize()  # swaps write the shard on torch's stream
         s = self._wrap(st)
         v = self.eng.norm(s) ** 2
         s.free()
         return v
 
     def local_expectation(self, st: ShardedState, op: PauliOperator) -> complex:
+        import torch
+        torch.cuda.current_stream().synchronize()
         s = self._wrap(st)
         v = self.eng.expectation(op, s)
         s.free()

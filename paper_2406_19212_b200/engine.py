@@ -96,6 +96,19 @@ class Engine:
             out[name] = (int(cnt), float(ms))
         return out
 
+    def alloc_stats(self) -> dict:
+        """state_alloc_stats (state.hpp:154-161) plus device bytes."""
+        a, b = ct.c_int64(), ct.c_int64()
+        c, d = ct.c_uint64(), ct.c_uint64()
+        self.check(self._fn("alloc_stats")(ct.byref(a), ct.byref(b), ct.byref(c), ct.byref(d)))
+        return {"live": a.value, "peak": b.value, "live_bytes": c.value, "peak_bytes": d.value}
+
+    def reset_alloc_peak(self) -> None:
+        self.check(self._fn("reset_alloc_peak")())
+
+    def release_caches(self) -> None:
+        self.check(self._fn("release_caches")())
+
     def stream_of(self, s: "State") -> int:
         v = ct.c_void_p()
         self.check(self._fn("state_stream")(s.handle, ct.byref(v)))
@@ -131,6 +144,20 @@ class Engine:
             out = np.empty(s.size, dtype=np.complex128)
         self.check(self._fn("state_download")(s.handle, out.ctypes.data_as(c128_p),
                                               ct.c_uint64(out.size)))
+        return out
+
+    def set_zero(self, s: State) -> None:
+        """Back to |0...0> (the reference harness's std::fill reset,
+        src/bench.cpp:138-141)."""
+        self.check(self._fn("state_set_zero")(s.handle))
+
+    def download_range(self, s: State, offset: int, count: int,
+                       out: Optional[np.ndarray] = None) -> np.ndarray:
+        """Amplitudes [offset, offset + count) (canonical order)."""
+        if out is None:
+            out = np.empty(count, dtype=np.complex128)
+        self.check(self._fn("state_download_range")(s.handle, ct.c_uint64(offset), ct.c_uint64(count),
+                                                    out.ctypes.data_as(c128_p)))
         return out
 
     def copy(self, s: State) -> State:

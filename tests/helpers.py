@@ -92,3 +92,67 @@ def rel_err(a, b) -> float:
     b = np.asarray(b)
     den = max(float(np.max(np.abs(b))) if b.size else 0.0, 1e-300)
     return float(np.max(np.abs(a - b))) / den if b.size else 0.0
+
+
+# ---------------------------------------------------------------- size-independent state checksums
+# A state too large to compare whole (config 4: 2^33 amplitudes) is compared
+# through a fixed sample of amplitudes and a few random projections
+# P_j = sum_k w_j(k) a_k with weights hashed from the flat index k (SplitMix64
+# finaliser, rng.hpp:31-36). A qubit relabelling, a transposed matrix or a
+# misplaced superoperator changes every P_j by O(|a|·sqrt(2^n)) ~ O(1), while
+# rounding moves them by ~1e-15 — so the projections pin the whole state.
+NUM_PROJECTIONS = 4
+_M64 = (1 << 64) - 1
+
+
+def _mix64_np(k: np.ndarray) -> np.ndarray:
+    z = k.astype(np.uint64) + np.uint64(0x9E3779B97F4A7C15)
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def projection_weights(k0: int, count: int) -> np.ndarray:
+    """[NUM_PROJECTIONS, count] float64 weights in [-0.5, 0.5) for indices
+    k0 .. k0 + count - 1 (exactly representable: 16-bit fractions)."""
+    with np.errstate(over="ignore"):
+        z = _mix64_np(np.arange(k0, k0 + count, dtype=np.uint64))
+    w = np.empty((NUM_PROJECTIONS, count), dtype=np.float64)
+    for j in range(NUM_PROJECTIONS):
+        w[j] = ((z >> np.uint64(16 * j)) & np.uint64(0xFFFF)).astype(np.float64) / 65536.0 - 0.5
+    return w
+
+
+def state_projections(eng, state, size: int, chunk: int = 1 << 24) -> np.ndarray:
+    """Complex projections P_j of a state (any engine implementing
+    state_download_range), streamed in chunks."""
+    acc = np.zeros(NUM_PROJECTIONS, dtype=np.complex128)
+    buf = np.empty(min(chunk, size), dtype=np.complex128)
+    for k0 in range(0, size, chunk):
+        c = min(chunk, size - k0)
+        a = eng.download_range(state, k0, c, buf[:c])
+        acc += projection_weights(k0, c) @ a
+    return acc
+
+
+def sample_indices(n_bits: int, count: int = 4096, seed: int = 12345) -> np.ndarray:
+    """Sorted distinct flat indices: the first 64 plus `count` hashed ones."""
+    with np.errstate(over="ignore"):
+        z = _mix64_np(np.arange(count, dtype=np.uint64) + np.uint64(seed))
+    idx = (z >> np.uint64(64 - n_bits)).astype(np.int64) if n_bits < 64 else z.astype(np.int64)
+    return np.unique(np.concatenate([np.arange(min(64, 1 << n_bits)), idx]))
+
+
+def sample_amplitudes(eng, state, idx: np.ndarray) -> np.ndarray:
+    out = np.empty(len(idx), dtype=np.complex128)
+    one = np.empty(1, dtype=np.complex128)
+    # runs of consecutive indices in one call each
+    i = 0
+    while i < len(idx):
+        j = i
+        while j + 1 < len(idx) and idx[j + 1] == idx[j] + 1:
+            j += 1
+        out[i:j + 1] = eng.download_range(state, int(idx[i]), j - i + 1)
+        i = j + 1
+    del one
+    return out

@@ -68,3 +68,39 @@ def test_clock_sampler_summary_without_samples():
 def test_hbm_peak_reads_measured_file():
     peak, kind = bench.hbm_peak()
     assert peak > 1000 and kind in ("measured", "fallback")
+
+
+def test_sharded_value_counts_one_circuit_per_step():
+    """A sharded run processes ONE circuit per step across all ranks (no
+    factor N); replicas each process their own."""
+    for world in (2, 4, 8):
+        w = wl("rqc33", world)
+        assert w.sharded and w.job_units(5) == 5 * w.gates
+        q = wl("qaoa30", world)
+        assert q.sharded and q.job_units(5) == 5
+        r = wl("rqc28", world)
+        assert not r.sharded and r.job_units(5) == 5 * r.gates * world
+    assert wl("rqc28").job_units(3) == 3 * 785
+
+
+def test_reference_sample_uses_harness_protocol():
+    """Allocated once, std::fill reset per run (src/bench.cpp:128-151)."""
+    import oracle
+    w = bench.Workload("rqc28", argparse.Namespace(unfused=False), 1)
+    smp = bench.ReferenceSample(w)
+    smp.n = 8  # shrink for the CPU test; the protocol is what is checked
+    smp.circ = bench.Circuit(circ_small())
+    eng = oracle.restatement()
+    smp.prepare(eng)
+    h = smp.state.handle
+    smp.run(eng)
+    a = eng.download(smp.state)
+    smp.run(eng)
+    assert smp.state.handle == h  # same allocation
+    assert (eng.download(smp.state) == a).all()  # reset to |0...0> before each run
+    smp.free()
+
+
+def circ_small():
+    from paper_2406_19212_b200 import circuits
+    return circuits.config1(rows=2, cols=4, cycles=3).circuit.elements

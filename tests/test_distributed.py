@@ -98,6 +98,9 @@ def worker(rank, world, port, n, seed, failures):
             assert abs(e - o.expectation(op, ref)) <= 1e-12
             assert abs(nrm - 1) <= 1e-12
             assert st.swaps > 0
+        # transfer buffers stay within chunk_amps (16) although the shard's
+        # contiguous runs are longer (swaps pick high local bits)
+        assert st.max_buffer_amps <= 16 and st.inflight_amps <= 16, (st.max_buffer_amps, st.inflight_amps)
         # the RQC generator on a grid whose top qubits are global
         w = circuits.config1(rows=3, cols=3, cycles=6, seed=seed)
         st2 = ShardedState(9, dist, OracleEngine(),
@@ -119,7 +122,7 @@ def worker(rank, world, port, n, seed, failures):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n", [(2, 8), (4, 9)])
+@pytest.mark.parametrize("world,n", [(2, 8), (4, 9), (8, 10)])
 def test_sharded_circuit_matches_unsharded(world, n):
     mgr = mp.Manager()
     failures = mgr.list()
@@ -173,7 +176,7 @@ def grad_worker(rank, world, port, n, seed, failures):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n", [(2, 8), (4, 10)])
+@pytest.mark.parametrize("world,n", [(2, 8), (4, 10), (8, 10)])
 def test_sharded_gradient_matches_unsharded(world, n):
     mgr = mp.Manager()
     failures = mgr.list()
