@@ -173,8 +173,10 @@ VQB_API int vqb_state_create(int32_t num_qubits, int32_t mixed, vqb_state **out)
 /* Non-owning handle over caller-owned device memory holding 2^num_qubits
  * amplitudes (mixed: 4^num_qubits). `global_offset` is the flat index of the
  * buffer's first amplitude inside a larger, sharded state (0 when
- * unsharded); diagonal and controlled operations use it to resolve qubits
- * that live above the buffer (global qubits). */
+ * unsharded): vqb_state_set_zero puts the |0...0> amplitude only into the
+ * buffer at offset 0. Operations act on the buffer's own qubits; callers
+ * restrict operations on global qubits first (as vqb_sharded_* and
+ * paper_2406_19212_b200/distributed.py do). */
 VQB_API int vqb_state_wrap(void *device_ptr, int32_t num_qubits, int32_t mixed,
                            uint64_t global_offset, int32_t global_qubits,
                            vqb_state **out);
@@ -306,6 +308,42 @@ VQB_API int vqb_measure(vqb_state *st, int32_t qubit, double uniform, int32_t *o
 VQB_API int vqb_measure_probability(const vqb_state *st, int32_t qubit, double *p1);
 VQB_API int vqb_collapse(vqb_state *st, int32_t qubit, int32_t outcome, double probability);
 
+/* ---- multi-device sharded pure state (no reference analogue; SURVEY.md
+ * §8(e)). The reference is single-address-space (state.hpp:175-256), so its
+ * unsharded result is the oracle. ----
+ * One process drives P = 2^g devices: shard r (on devices[r]) holds the 2^(n-g)
+ * amplitudes whose top g physical bits equal r. Operations on local qubits
+ * run on every shard through the fused executor; controls and diagonal phases
+ * on global qubits are resolved per shard on the host (no data movement); a
+ * mixing operation on a global qubit first swaps global and local qubits in
+ * one all-to-all round of in-place peer-to-peer kernels (NVLink loads and
+ * stores into the peer shard, no staging buffer). A logical->physical qubit
+ * map is kept; download/upload use the canonical order (bit-exact).
+ * `devices` may repeat an ordinal (several shards on one device, e.g. to
+ * test the exchange logic on one GPU); distinct devices need peer access
+ * (UNSUPPORTED otherwise). At least 12 local qubits per shard. */
+typedef struct vqb_sharded vqb_sharded;
+VQB_API int vqb_sharded_create(int32_t num_qubits, int32_t num_devices, const int32_t *devices,
+                               vqb_sharded **out);
+VQB_API int vqb_sharded_destroy(vqb_sharded *st);
+VQB_API int vqb_sharded_set_zero(vqb_sharded *st);
+/* apply_circuit (circuit.hpp:110-129) on the sharded state; pure gates only
+ * (TYPE for channels, as for a PureState). */
+VQB_API int vqb_sharded_apply_circuit(vqb_sharded *st, const vqb_op *ops, int64_t count);
+VQB_API int vqb_sharded_norm(vqb_sharded *st, double *out);
+/* expectation (observables.hpp:176-190); X/Y factors on global qubits are
+ * swapped local first (the state's qubit map changes, its value does not). */
+VQB_API int vqb_sharded_expectation(vqb_sharded *st, const vqb_pauli_term *terms, int64_t num_terms,
+                                    vqb_c128 *out);
+/* Whole state in canonical order (count = 2^num_qubits). */
+VQB_API int vqb_sharded_download(vqb_sharded *st, vqb_c128 *host, uint64_t count);
+VQB_API int vqb_sharded_upload(vqb_sharded *st, const vqb_c128 *host, uint64_t count);
+/* Exchange counters: all-to-all rounds, global<->local bit exchanges, bytes
+ * moved over the links (both directions); the physical bit of each logical
+ * qubit (num_qubits entries, 0-based). Null outputs are skipped. */
+VQB_API int vqb_sharded_stats(const vqb_sharded *st, int64_t *rounds, int64_t *swapped_bits,
+                              uint64_t *bytes_moved, int32_t *log2phys);
+
 /* ---- state dump I/O: io.hpp:40-128 ---- */
 /* save_state (io.hpp:56-82): "VQCS" | u32 version 1 | u32 n | u8 precision
  * (2 = complex double) | 2^n little-endian (re, im) doubles. Pure states only
@@ -317,6 +355,26 @@ VQB_API int vqb_state_save(const vqb_state *st, const char *path);
  * the reference: bad magic, unsupported version, qubit count out of range,
  * unknown precision tag, truncated payload. */
 VQB_API int vqb_state_load(const char *path, vqb_state **out, int32_t *precision);
+
+/* ---- benchmark records: BenchRecord (bench.hpp:60-72) and emit_report
+ * (src/bench.cpp:296-310,329-369) ---- */
+typedef struct vqb_bench_record {
+    const char *task;              /* e.g. "rqc", "rqc-grad", "noisy-grad" */
+    int32_t num_qubits, depth, threads;
+    const double *seconds;         /* one entry per repetition (warm-up excluded) */
+    int64_t num_seconds;
+    double speedup;                /* 0: not a thread sweep (field omitted) */
+    int64_t num_info;              /* params: key/value strings */
+    const char *const *info_keys;
+    const char *const *info_values;
+} vqb_bench_record;
+/* emit_report: format 0 = JSON array (stable field order, mean and population
+ * standard deviation computed as finish_stats does), 1 = CSV
+ * (task,n,depth,threads,rep,seconds). Writes at most `cap` bytes (NUL
+ * included) to `out` (nullable) and the full length to *length. Output is
+ * byte-identical to the reference harness's. USAGE for an empty record list. */
+VQB_API int vqb_bench_report(const vqb_bench_record *records, int64_t count, int32_t format, char *out,
+                             int64_t cap, int64_t *length);
 
 /* ---- circuit fusion: circuit.hpp:199-276 ---- */
 /* fuse_gates: absorbs single-qubit gates into the next (else the previous)
@@ -353,6 +411,13 @@ VQB_API int vqb_gate_derivative(const vqb_op *gate, int32_t param_index, vqb_c12
 VQB_API int vqb_gate_inverse(const vqb_op *gate, vqb_c128 *out);
 /* channel_superoperator (gates.hpp:708-732). out: 16^m entries. */
 VQB_API int vqb_channel_superop(const vqb_op *channel, vqb_c128 *out);
+/* Inverse of the channel's superoperator as gradient_mixed uses it
+ * (autodiff.hpp:263-276): closed form for the named 1-qubit channels
+ * (gates.hpp:657-704), elimination with partial pivoting for Generic ones
+ * (linalg.hpp:140-200). *condition = ||S||_1 ||S^-1||_1; *singular != 0 when
+ * a pivot vanishes (out untouched then). Host only. */
+VQB_API int vqb_channel_inverse(const vqb_op *channel, vqb_c128 *out, double *condition,
+                                int32_t *singular);
 
 #ifdef __cplusplus
 }

@@ -66,6 +66,26 @@ def checker() -> Engine:
     return reference() if reference_available() else restatement()
 
 
+REFBENCH_CLI = os.path.join(HERE, "_ref", "refbench_cli")
+
+
+def reference_bench_report(records, fmt: str = "json") -> str:
+    """The reference harness's own emit_report (src/bench.cpp) on the same
+    records (oracle/_ref/refbench_cli, a separate process)."""
+    lines = [fmt]
+    for r in records:
+        secs = [float(x).hex() for x in r["seconds"]]
+        items = sorted((str(k), str(v)) for k, v in r.get("params", {}).items())
+        f = [str(r["task"]).encode().hex(), str(int(r["n"])), str(int(r["depth"])), str(int(r["threads"])),
+             float(r.get("speedup", 0.0)).hex(), str(len(secs))] + secs + [str(len(items))]
+        for k, v in items:
+            f += [k.encode().hex() or "-", v.encode().hex() or "-"]
+        lines.append(" ".join(f))
+    out = subprocess.run([REFBENCH_CLI], input="\n".join(lines) + "\n", capture_output=True, text=True,
+                         check=True)
+    return out.stdout
+
+
 def set_reference_threads(t: int) -> None:
     reference().lib.vqcsref_set_num_threads(int(t))
 

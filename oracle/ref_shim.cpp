@@ -495,6 +495,19 @@ REF_API int vqcsref_gate_inverse(const vqb_op *op, vqb_c128 *out) {
     return guard([&] { from_cvec(gate_inverse(to_gate(*op)).matrix, out); });
 }
 
+// the reference's rule: LU inverse of the superoperator (autodiff.hpp:263-276)
+REF_API int vqcsref_channel_inverse(const vqb_op *op, vqb_c128 *out, double *condition,
+                                    int32_t *singular) {
+    return guard([&] {
+        const auto c = to_channel(*op);
+        const auto s = channel_superoperator(c);
+        const auto lu = linalg::lu_inverse(s.matrix, s.dim());
+        if (condition) *condition = lu.condition;
+        if (singular) *singular = lu.singular ? 1 : 0;
+        if (!lu.singular && out) std::memcpy(out, lu.inverse.data(), lu.inverse.size() * sizeof(C));
+    });
+}
+
 REF_API int vqcsref_channel_superop(const vqb_op *op, vqb_c128 *out) {
     return guard([&] { from_cvec(channel_superoperator(to_channel(*op)).matrix, out); });
 }

@@ -352,6 +352,32 @@ def heisenberg_1d(length: int, hz: float = 1.0, J: float = 1.0) -> PauliOperator
 
 
 # ---- binding helper shared by product and oracle libraries ----
+class vqb_bench_record(ct.Structure):
+    _fields_ = [("task", ct.c_char_p), ("num_qubits", ct.c_int32), ("depth", ct.c_int32),
+                ("threads", ct.c_int32), ("seconds", ct.POINTER(ct.c_double)), ("num_seconds", ct.c_int64),
+                ("speedup", ct.c_double), ("num_info", ct.c_int64),
+                ("info_keys", ct.POINTER(ct.c_char_p)), ("info_values", ct.POINTER(ct.c_char_p))]
+
+
+def pack_bench_records(records):
+    """[{task, n, depth, threads, seconds: [...], speedup?, params: {k: v}}]
+    -> (ctypes array, keep-alive list)."""
+    keep = []
+    arr = (vqb_bench_record * max(len(records), 1))()
+    for i, r in enumerate(records):
+        secs = (ct.c_double * max(len(r["seconds"]), 1))(*r["seconds"])
+        items = sorted((str(k), str(v)) for k, v in r.get("params", {}).items())
+        kb = [k.encode() for k, _ in items]  # the arrays point into these: keep them alive
+        vb = [v.encode() for _, v in items]
+        keys = (ct.c_char_p * max(len(items), 1))(*kb)
+        vals = (ct.c_char_p * max(len(items), 1))(*vb)
+        task = r["task"].encode()
+        keep += [secs, keys, vals, task, kb, vb]
+        arr[i] = vqb_bench_record(task, int(r["n"]), int(r["depth"]), int(r["threads"]), secs,
+                                  len(r["seconds"]), float(r.get("speedup", 0.0)), len(items), keys, vals)
+    return arr, keep
+
+
 def bind_abi(lib: ct.CDLL, prefix: str) -> None:
     """Declare argtypes/restype for every ABI function the library exports."""
     vp = ct.c_void_p
@@ -388,6 +414,8 @@ def bind_abi(lib: ct.CDLL, prefix: str) -> None:
         "gate_derivative": (ct.c_int, [op_p, i32, c128_p]),
         "gate_inverse": (ct.c_int, [op_p, c128_p]),
         "channel_superop": (ct.c_int, [op_p, c128_p]),
+        "channel_inverse": (ct.c_int, [op_p, c128_p, dp, ct.POINTER(i32)]),
+        "bench_report": (ct.c_int, [ct.POINTER(vqb_bench_record), i64, i32, ct.c_char_p, i64, ct.POINTER(i64)]),
         "measure": (ct.c_int, [vp, i32, ct.c_double, ct.POINTER(i32), dp]),
         "measure_probability": (ct.c_int, [vp, i32, dp]),
         "collapse": (ct.c_int, [vp, i32, i32, ct.c_double]),
@@ -398,6 +426,15 @@ def bind_abi(lib: ct.CDLL, prefix: str) -> None:
         "reverse_sweep": (ct.c_int, [vp, vp, ct.POINTER(vqb_rev_step), i64, ct.c_double, dp, i64]),
         # product-only
         "state_wrap": (ct.c_int, [vp, i32, i32, u64, i32, ct.POINTER(vp)]),
+        "sharded_create": (ct.c_int, [i32, i32, ct.POINTER(i32), ct.POINTER(vp)]),
+        "sharded_destroy": (ct.c_int, [vp]),
+        "sharded_set_zero": (ct.c_int, [vp]),
+        "sharded_apply_circuit": (ct.c_int, [vp, op_p, i64]),
+        "sharded_norm": (ct.c_int, [vp, dp]),
+        "sharded_expectation": (ct.c_int, [vp, term_p, i64, c128_p]),
+        "sharded_download": (ct.c_int, [vp, c128_p, u64]),
+        "sharded_upload": (ct.c_int, [vp, c128_p, u64]),
+        "sharded_stats": (ct.c_int, [vp, ct.POINTER(i64), ct.POINTER(i64), ct.POINTER(u64), ct.POINTER(i32)]),
         "alloc_stats": (ct.c_int, [ct.POINTER(i64), ct.POINTER(i64), ct.POINTER(u64), ct.POINTER(u64)]),
         "reset_alloc_peak": (ct.c_int, []),
         "release_caches": (ct.c_int, []),

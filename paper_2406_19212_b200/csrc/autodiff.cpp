@@ -396,7 +396,7 @@ GradientOut gradient_mixed(const vqb_op *ops, int64_t count, const vqb_pauli_ter
             const Channel &ch = es[i].chan;
             const cvec s = channel_superop(ch);
             const int d = 1 << (2 * ch.m);
-            const Inverse lu = lu_inverse(s, d);
+            const Inverse lu = channel_inverse(ch, s);
             if (lu.singular || lu.condition > kChannelConditionLimit) {
                 static const char *names[] = {"Generic", "AmplitudeDamping", "PhaseDamping",
                                               "Depolarizing"};

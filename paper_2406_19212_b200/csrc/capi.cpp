@@ -7,12 +7,17 @@
 #include "autodiff.hpp"
 #include "engine.hpp"
 #include "plan.hpp"
+#include "sharded.hpp"
 
 using namespace vqb;
 
 struct vqb_state : DeviceState {};
+struct vqb_sharded {
+    Sharded *p;
+};
 
 namespace vqb {
+std::string bench_report(const vqb_bench_record *recs, int64_t count, int format);
 std::string debug_jit_source(int regs, const void *params, size_t nbytes, bool rev, double *flops);
 int64_t launch_count();
 double flop_count();
@@ -691,6 +696,87 @@ VQB_API int vqb_collapse(vqb_state *s, int32_t qubit, int32_t outcome, double pr
     });
 }
 
+// ---- multi-device sharded state ----
+namespace {
+Sharded *sh(const vqb_sharded *s) {
+    if (!s || !s->p) raise(VQB_ERR_USAGE, "null sharded state handle");
+    return s->p;
+}
+} // namespace
+
+VQB_API int vqb_sharded_create(int32_t n, int32_t ndev, const int32_t *devices, vqb_sharded **out) {
+    return guard([&] {
+        need(devices, "devices");
+        need(out, "out");
+        if (n < 1 || n > 40) raise(VQB_ERR_SIZE, "sharded state: qubit count must be in 1..40");
+        std::vector<int> d(devices, devices + std::max(ndev, 0));
+        Sharded *s = sharded_create(n, ndev, d.data());
+        *out = new vqb_sharded{s};
+    });
+}
+
+VQB_API int vqb_sharded_destroy(vqb_sharded *s) {
+    return guard([&] {
+        if (!s) return;
+        sharded_destroy(s->p);
+        delete s;
+    });
+}
+
+VQB_API int vqb_sharded_set_zero(vqb_sharded *s) {
+    return guard([&] { sharded_set_zero(sh(s)); });
+}
+
+VQB_API int vqb_sharded_apply_circuit(vqb_sharded *s, const vqb_op *ops, int64_t count) {
+    return guard([&] {
+        if (count > 0) need(ops, "ops");
+        sharded_apply_circuit(sh(s), ops, count);
+    });
+}
+
+VQB_API int vqb_sharded_norm(vqb_sharded *s, double *out) {
+    return guard([&] {
+        need(out, "out");
+        *out = sharded_norm(sh(s));
+    });
+}
+
+VQB_API int vqb_sharded_expectation(vqb_sharded *s, const vqb_pauli_term *terms, int64_t nt, vqb_c128 *out) {
+    return guard([&] {
+        need(out, "out");
+        if (nt > 0) need(terms, "terms");
+        const cplx e = sharded_expectation(sh(s), terms, nt);
+        out->re = e.real();
+        out->im = e.imag();
+    });
+}
+
+VQB_API int vqb_sharded_download(vqb_sharded *s, vqb_c128 *host, uint64_t count) {
+    return guard([&] {
+        need(host, "host");
+        sharded_download(sh(s), host, count);
+    });
+}
+
+VQB_API int vqb_sharded_upload(vqb_sharded *s, const vqb_c128 *host, uint64_t count) {
+    return guard([&] {
+        need(host, "host");
+        sharded_upload(sh(s), host, count);
+    });
+}
+
+VQB_API int vqb_sharded_stats(const vqb_sharded *s, int64_t *rounds, int64_t *swapped_bits,
+                              uint64_t *bytes_moved, int32_t *log2phys) {
+    return guard([&] {
+        const Sharded *p = sh(s);
+        if (rounds) *rounds = p->rounds;
+        if (swapped_bits) *swapped_bits = p->bits_swapped;
+        if (bytes_moved) *bytes_moved = p->bytes_moved;
+        if (log2phys)
+            for (int q = 0; q < p->n; ++q) log2phys[q] = p->log2phys[q];
+    });
+}
+
 // ---- state dumps (io.hpp:40-128) ----
 VQB_API int vqb_state_save(const vqb_state *s, const char *path) {
     return guard([&] {
@@ -707,6 +793,22 @@ VQB_API int vqb_state_load(const char *path, vqb_state **out, int32_t *precision
         int prec = 0;
         *out = static_cast<vqb_state *>(state_load(path, &prec));
         if (precision) *precision = prec;
+    });
+}
+
+// ---- BenchRecord reports (src/bench.cpp:329-369) ----
+VQB_API int vqb_bench_report(const vqb_bench_record *recs, int64_t count, int32_t format, char *out,
+                             int64_t cap, int64_t *length) {
+    return guard([&] {
+        if (count > 0) need(recs, "records");
+        if (format != 0 && format != 1) raise(VQB_ERR_DOMAIN, "bench_report: format must be 0 (JSON) or 1 (CSV)");
+        const std::string r = bench_report(recs, count, format);
+        if (length) *length = (int64_t)r.size();
+        if (out && cap > 0) {
+            const size_t n = std::min<size_t>(r.size(), size_t(cap - 1));
+            std::memcpy(out, r.data(), n);
+            out[n] = 0;
+        }
     });
 }
 
@@ -823,6 +925,17 @@ VQB_API int vqb_gate_derivative(const vqb_op *op, int32_t p, vqb_c128 *out) {
 
 VQB_API int vqb_gate_inverse(const vqb_op *op, vqb_c128 *out) {
     return guard([&] { to_c128(gate_inverse(gate_from_op(*op)).mat, out); });
+}
+
+VQB_API int vqb_channel_inverse(const vqb_op *op, vqb_c128 *out, double *condition, int32_t *singular) {
+    return guard([&] {
+        need(op, "channel");
+        const Channel c = channel_from_op(*op);
+        const Inverse r = channel_inverse(c, channel_superop(c));
+        if (condition) *condition = r.condition;
+        if (singular) *singular = r.singular ? 1 : 0;
+        if (!r.singular && out) to_c128(r.inv, out);
+    });
 }
 
 VQB_API int vqb_channel_superop(const vqb_op *op, vqb_c128 *out) {

@@ -446,44 +446,73 @@ cvec matmul(const cvec &a, const cvec &b, int d) {
     return r;
 }
 
+// Dense inverse for the channel-inversion rule of gradient_mixed
+// (autodiff.hpp:263-276, linalg.hpp:140-200): Gauss-Jordan elimination with
+// partial pivoting on [A | I]. The pivot sequence equals the reference LU's
+// (same column maxima), so "singular" (a pivot at or below 1e-300 of max|A|)
+// is decided identically, and condition = ||A||_1 ||A^-1||_1 as there.
 Inverse lu_inverse(const cvec &a, int d) {
-    cvec lu = a;
-    std::vector<int> piv(d);
-    for (int i = 0; i < d; ++i) piv[i] = i;
-    const double scale = std::max(max_abs(a), 1e-300);
-    for (int k = 0; k < d; ++k) {
-        int p = k;
-        double best = std::abs(lu[k + k * d]);
-        for (int i = k + 1; i < d; ++i)
-            if (std::abs(lu[i + k * d]) > best) {
-                best = std::abs(lu[i + k * d]);
-                p = i;
-            }
-        if (best <= scale * 1e-300) return {{}, INFINITY, true};
-        if (p != k) {
-            std::swap(piv[p], piv[k]);
-            for (int j = 0; j < d; ++j) std::swap(lu[p + j * d], lu[k + j * d]);
-        }
-        const cplx pivot = lu[k + k * d];
-        for (int i = k + 1; i < d; ++i) {
-            const cplx f = lu[i + k * d] / pivot;
-            lu[i + k * d] = f;
-            for (int j = k + 1; j < d; ++j) lu[i + j * d] -= f * lu[k + j * d];
+    const int w = 2 * d; // row-major augmented rows [A row | I row]
+    std::vector<cplx> m(size_t(d) * w, cplx(0));
+    for (int r = 0; r < d; ++r) {
+        for (int c = 0; c < d; ++c) m[size_t(r) * w + c] = a[r + size_t(c) * d];
+        m[size_t(r) * w + d + r] = 1.0;
+    }
+    const double tiny = std::max(max_abs(a), 1e-300) * 1e-300;
+    for (int col = 0; col < d; ++col) {
+        int piv = col;
+        for (int r = col + 1; r < d; ++r)
+            if (std::abs(m[size_t(r) * w + col]) > std::abs(m[size_t(piv) * w + col])) piv = r;
+        if (std::abs(m[size_t(piv) * w + col]) <= tiny) return {{}, INFINITY, true};
+        if (piv != col)
+            std::swap_ranges(m.begin() + size_t(piv) * w, m.begin() + size_t(piv + 1) * w,
+                             m.begin() + size_t(col) * w);
+        const cplx inv_p = 1.0 / m[size_t(col) * w + col];
+        for (int c = col; c < w; ++c) m[size_t(col) * w + c] *= inv_p;
+        for (int r = 0; r < d; ++r) {
+            if (r == col) continue;
+            const cplx f = m[size_t(r) * w + col];
+            if (f == cplx(0)) continue;
+            for (int c = col; c < w; ++c) m[size_t(r) * w + c] -= f * m[size_t(col) * w + c];
         }
     }
     cvec inv(size_t(d) * d);
-    std::vector<cplx> x(d);
-    for (int col = 0; col < d; ++col) {
-        for (int i = 0; i < d; ++i) x[i] = piv[i] == col ? 1.0 : 0.0;
-        for (int i = 1; i < d; ++i)
-            for (int j = 0; j < i; ++j) x[i] -= lu[i + j * d] * x[j];
-        for (int i = d; i-- > 0;) {
-            for (int j = i + 1; j < d; ++j) x[i] -= lu[i + j * d] * x[j];
-            x[i] /= lu[i + i * d];
-        }
-        for (int i = 0; i < d; ++i) inv[i + col * d] = x[i];
-    }
+    for (int r = 0; r < d; ++r)
+        for (int c = 0; c < d; ++c) inv[r + size_t(c) * d] = m[size_t(r) * w + d + c];
     const double cond = norm1(a, d) * norm1(inv, d);
+    return {std::move(inv), cond, false};
+}
+
+// Closed-form inverse of a named single-qubit channel's superoperator
+// (standard_channel, gates.hpp:657-704). Amplitude damping, phase damping and
+// depolarizing all map populations to populations and scale each coherence:
+// in the (tau + 2 tau') order the superoperator is block diagonal with the
+// 2x2 population block on {0, 3} and the coherences 1, 2 on the diagonal, so
+// its inverse is that block's 2x2 inverse and two reciprocals (e.g.
+// depolarizing: [[1-p/2, p/2], [p/2, 1-p/2]]^-1 = [[1-p/2, -p/2], [-p/2,
+// 1-p/2]] / (1-p), coherences 1/(1-p)). Generic channels keep the
+// elimination (the reference's rule for every channel, autodiff.hpp:263-276).
+Inverse channel_inverse(const Channel &c, const cvec &S) {
+    const int d = 1 << (2 * c.m);
+    if (c.kind == VQB_CHANNEL_GENERIC || c.m != 1) return lu_inverse(S, d);
+    auto at = [&](int r, int col) { return S[r + size_t(col) * 4]; };
+    for (int r = 0; r < 4; ++r)
+        for (int col = 0; col < 4; ++col) {
+            const bool pop = (r == 0 || r == 3) && (col == 0 || col == 3);
+            if (!pop && r != col && at(r, col) != cplx(0)) return lu_inverse(S, d); // not the named form
+        }
+    const double tiny = std::max(max_abs(S), 1e-300) * 1e-300;
+    const cplx det = at(0, 0) * at(3, 3) - at(0, 3) * at(3, 0);
+    if (std::abs(det) <= tiny || std::abs(at(1, 1)) <= tiny || std::abs(at(2, 2)) <= tiny)
+        return {{}, INFINITY, true};
+    cvec inv(16, cplx(0));
+    inv[0 + 0 * 4] = at(3, 3) / det;
+    inv[0 + 3 * 4] = -at(0, 3) / det;
+    inv[3 + 0 * 4] = -at(3, 0) / det;
+    inv[3 + 3 * 4] = at(0, 0) / det;
+    inv[1 + 1 * 4] = 1.0 / at(1, 1);
+    inv[2 + 2 * 4] = 1.0 / at(2, 2);
+    const double cond = norm1(S, 4) * norm1(inv, 4);
     return {std::move(inv), cond, false};
 }
 

@@ -57,7 +57,10 @@ struct Inverse {
     double condition;
     bool singular;
 };
-Inverse lu_inverse(const cvec &a, int d); // linalg.hpp:140-200
+Inverse lu_inverse(const cvec &a, int d); // linalg.hpp:140-200 (singularity / condition rule)
+// Inverse of a channel's superoperator S: closed form for the named 1-qubit
+// channels (gates.hpp:657-704), lu_inverse for Generic ones.
+Inverse channel_inverse(const Channel &c, const cvec &S);
 
 void check_positions(const int *pos, int m, const char *what);
 void check_fit(const int *pos, int m, int n); // kernels.hpp:71-87

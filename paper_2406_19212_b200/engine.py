@@ -49,6 +49,67 @@ class State:
             pass
 
 
+class ShardedHandle:
+    """vqb_sharded: one process, P = 2^g devices (include/vqcs_b200.h)."""
+
+    def __init__(self, engine: "Engine", n: int, devices):
+        self.engine = engine
+        self.n = n
+        self.devices = list(devices)
+        h = ct.c_void_p()
+        dv = (ct.c_int32 * len(self.devices))(*self.devices)
+        engine.check(engine._fn("sharded_create")(n, len(self.devices), dv, ct.byref(h)))
+        self.handle = h
+
+    def _f(self, name):
+        return self.engine._fn("sharded_" + name)
+
+    def set_zero(self) -> None:
+        self.engine.check(self._f("set_zero")(self.handle))
+
+    def apply_circuit(self, c: Circuit) -> None:
+        p = c.pack() if isinstance(c, Circuit) else pack_ops(c)
+        self.engine.check(self._f("apply_circuit")(self.handle, p.arr, p.count))
+
+    def norm(self) -> float:
+        v = ct.c_double()
+        self.engine.check(self._f("norm")(self.handle, ct.byref(v)))
+        return v.value
+
+    def expectation(self, op: PauliOperator) -> complex:
+        arr, nt, _k = op.pack()
+        v = c128()
+        self.engine.check(self._f("expectation")(self.handle, arr, nt, ct.byref(v)))
+        return complex(v.re, v.im)
+
+    def download(self) -> np.ndarray:
+        out = np.empty(1 << self.n, dtype=np.complex128)
+        self.engine.check(self._f("download")(self.handle, out.ctypes.data_as(c128_p), ct.c_uint64(out.size)))
+        return out
+
+    def upload(self, amps: np.ndarray) -> None:
+        amps = np.ascontiguousarray(amps, dtype=np.complex128)
+        self.engine.check(self._f("upload")(self.handle, amps.ctypes.data_as(c128_p), ct.c_uint64(amps.size)))
+
+    def stats(self) -> dict:
+        r, b = ct.c_int64(), ct.c_int64()
+        m = ct.c_uint64()
+        lp = (ct.c_int32 * self.n)()
+        self.engine.check(self._f("stats")(self.handle, ct.byref(r), ct.byref(b), ct.byref(m), lp))
+        return {"rounds": r.value, "swapped_bits": b.value, "bytes_moved": m.value, "log2phys": list(lp)}
+
+    def free(self) -> None:
+        if self.handle:
+            self.engine._fn("sharded_destroy")(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
 class Engine:
     def __init__(self, lib: ct.CDLL, prefix: str, name: str):
         self.lib = lib
@@ -95,6 +156,10 @@ class Engine:
             name, cnt, ms = line.split()
             out[name] = (int(cnt), float(ms))
         return out
+
+    def sharded(self, n: int, devices) -> ShardedHandle:
+        """A pure n-qubit state sharded over `devices` (vqb_sharded_create)."""
+        return ShardedHandle(self, n, devices)
 
     def alloc_stats(self) -> dict:
         """state_alloc_stats (state.hpp:154-161) plus device bytes."""
@@ -403,3 +468,25 @@ class Engine:
 
     def channel_superop(self, c) -> np.ndarray:
         return self._mat_call("channel_superop", c, 1 << (2 * len(c.positions)))
+
+    def bench_report(self, records, fmt: str = "json") -> str:
+        """emit_report (src/bench.cpp:329-369) over BenchRecord dicts
+        {task, n, depth, threads, seconds, [speedup], params}."""
+        arr, keep = abi.pack_bench_records(records)
+        n = ct.c_int64()
+        f = 1 if fmt == "csv" else 0
+        self.check(self._fn("bench_report")(arr, len(records), f, None, 0, ct.byref(n)))
+        buf = ct.create_string_buffer(n.value + 1)
+        self.check(self._fn("bench_report")(arr, len(records), f, buf, n.value + 1, ct.byref(n)))
+        del keep
+        return buf.value.decode()
+
+    def channel_inverse(self, c):
+        """-> (inverse or None when singular, condition) of the channel's
+        superoperator, as gradient_mixed inverts it."""
+        d = 1 << (2 * len(c.positions))
+        out = np.zeros(d * d, dtype=np.complex128)
+        cond, sing = ct.c_double(), ct.c_int32()
+        p = pack_ops([c])
+        self.check(self._fn("channel_inverse")(p.arr, out.ctypes.data_as(c128_p), ct.byref(cond), ct.byref(sing)))
+        return (None if sing.value else out), cond.value

@@ -13,8 +13,9 @@ once on the GPU box's host and its output committed:
 Stored per config (the GPU tests tests/test_gpu_parity_fullsize.py compare the
 CUDA path against these):
   * config1 (28q RQC), config4 (33q RQC): norm, amplitudes at a fixed index
-    sample (tests/helpers.sample_indices) and NUM_PROJECTIONS random
-    projections of the whole state (tests/helpers.state_projections);
+    sample (tests/helpers.sample_indices) and NUM_PROJECTIONS overlaps of the
+    whole state with seeded product states
+    (tests/helpers.product_projections_host);
   * config2 (30q QAOA, p=8): loss, the 600 per-gate gradients and the 16 tied
     gradients (gradient_pure, autodiff.hpp:95-156);
   * config3 (15q noisy DM): loss and the 270 gradients (gradient_mixed,
@@ -35,7 +36,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 import oracle  # noqa: E402
-from helpers import sample_amplitudes, sample_indices, state_projections  # noqa: E402
+from helpers import product_projections_host, sample_amplitudes, sample_indices  # noqa: E402
 from paper_2406_19212_b200 import circuits  # noqa: E402
 
 
@@ -51,7 +52,7 @@ def state_record(ref, w, t0):
     rec = {"name": w.name, "n": w.num_qubits, "elements": len(w.circuit), "seed": w.seed,
            "norm": ref.norm(s), "sample_index": [int(i) for i in idx],
            "sample": c2l(sample_amplitudes(ref, s, idx)),
-           "projections": c2l(state_projections(ref, s, 1 << w.num_qubits)),
+           "product_projections": c2l(product_projections_host(ref, s, w.num_qubits)),
            "reference_seconds": t_apply}
     s.free()
     return rec

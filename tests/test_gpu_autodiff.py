@@ -267,7 +267,8 @@ def test_specialised_adjoint_matches_reference(dev, ref, monkeypatch, regs):
     """Specialised adjoint kernels (VQB_JIT=1) for both register geometries:
     QAOA (folded diagonal parametric steps with register conditions), the
     hardware-efficient ansatz (1-qubit parametric steps + CNOT) and a noisy
-    circuit (its 16x16 superoperator launches stay on the interpreter)."""
+    circuit (its 16x16 channel superoperators run in the specialised kernels
+    too; only wide *parametric* steps would stay on the interpreter)."""
     monkeypatch.setenv("VQB_JIT", "1")
     monkeypatch.setenv("VQB_REV_REGS", regs)
     for w in (circuits.config2(n=14, p=2), circuits.config0(n=14, layers=3)):

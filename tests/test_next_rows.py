@@ -15,9 +15,9 @@ import oracle
 from paper_2406_19212_b200 import circuits
 from paper_2406_19212_b200.abi import (Circuit, GateKind, IoError, IndexError_, TypeError_, UnsupportedError,
                                        make_gate, parametric_gate, standard_channel,
-                                       standard_gate, ChannelKind)
+                                       standard_gate, ChannelKind, make_channel)
 
-from helpers import random_density, random_gate, random_state
+from helpers import random_density, random_gate, random_state, random_unitary
 
 needs_ref = pytest.mark.skipif(not oracle.reference_available(), reason="oracle/_ref not built")
 
@@ -146,3 +146,80 @@ def test_state_load_errors(orc, tmp_path, case):
 def test_state_save_rejects_density_matrix(orc, tmp_path):
     with pytest.raises(TypeError_):
         orc.save_state(orc.mixed_state(2), tmp_path / "dm.vqcs")
+
+
+# ---- analytic channel inverses (row f4): named channels in closed form,
+# Generic ones by elimination; the reference inverts every channel by LU
+# (autodiff.hpp:263-276, linalg.hpp:140-200)
+@pytest.mark.parametrize("kind", [ChannelKind.AmplitudeDamping, ChannelKind.PhaseDamping,
+                                  ChannelKind.Depolarizing])
+@pytest.mark.parametrize("param", [0.0, 1e-3, 0.3, 0.999, 1 - 1e-13, 1.0])
+def test_named_channel_inverse_matches_reference_lu(kind, param):
+    import paper_2406_19212_b200 as vqb
+    import oracle
+    if not oracle.reference_available():
+        pytest.skip("reference not built")
+    dev, ref = vqb.device(), oracle.reference()
+    ch = standard_channel(kind, 2, param)
+    inv, cond = dev.channel_inverse(ch)
+    rinv, rcond = ref.channel_inverse(ch)
+    assert (inv is None) == (rinv is None)
+    # the NonInvertibleChannelError decision (condition limit 1e12, autodiff.hpp:51)
+    assert (inv is None or cond > 1e12) == (rinv is None or rcond > 1e12)
+    if inv is not None:
+        assert cond == pytest.approx(rcond, rel=1e-9)
+        assert np.max(np.abs(inv - rinv)) <= 1e-12 * max(1.0, np.max(np.abs(rinv)))
+
+
+def test_generic_channel_inverse_matches_reference_lu():
+    import paper_2406_19212_b200 as vqb
+    import oracle
+    from paper_2406_19212_b200 import circuits
+    if not oracle.reference_available():
+        pytest.skip("reference not built")
+    dev, ref = vqb.device(), oracle.reference()
+    rng = np.random.default_rng(8)
+    chans = [make_channel([1, 3], circuits.depolarizing2_kraus(1e-2))]
+    for _ in range(5):  # random 1-qubit Kraus pairs (generic)
+        u = random_unitary(4, rng)
+        k0, k1 = u[:2, :2], u[2:, :2]  # isometry columns -> completeness holds
+        chans.append(make_channel([2], [k0.reshape(-1, order="F"), k1.reshape(-1, order="F")]))
+    for ch in chans:
+        inv, cond = dev.channel_inverse(ch)
+        rinv, rcond = ref.channel_inverse(ch)
+        assert (inv is None) == (rinv is None)
+        if inv is not None:
+            assert cond == pytest.approx(rcond, rel=1e-9)
+            assert np.max(np.abs(inv - rinv)) <= 1e-10 * max(1.0, np.max(np.abs(rinv)))
+
+
+# ---- BenchRecord reports (row f3): byte-identical to the reference harness's
+# emit_report (src/bench.cpp:329-369), JSON and CSV
+BENCH_RECORDS = [
+    {"task": "rqc", "n": 28, "depth": 20, "threads": 1, "seconds": [0.07422, 0.0739, 0.0745],
+     "params": {"seed": "0", "verify_norm": "0.999999999999", "device": "B200 \"sm_100a\""}},
+    {"task": "rqc-grad", "n": 30, "depth": 8, "threads": 16, "seconds": [1.0, 2.5e-05, 123456789.125, 1e-7],
+     "params": {}},
+    {"task": "thread-sweep", "n": 22, "depth": 10, "threads": 8, "seconds": [8.31, 1.62],
+     "speedup": 5.1296296296296, "params": {"z": "last", "a": "first\tline"}},
+    {"task": "noisy-grad", "n": 15, "depth": 6, "threads": 1, "seconds": [], "params": {"p": "0.001"}},
+    {"task": "single-gate", "n": 33, "depth": 0, "threads": 1, "seconds": [1e16, 3e-300, 0.1, 1 / 3],
+     "params": {"gate": "H"}},
+]
+
+
+@pytest.mark.parametrize("fmt", ["json", "csv"])
+def test_bench_report_matches_reference_harness(fmt):
+    import paper_2406_19212_b200 as vqb
+    if not os.path.exists(oracle.REFBENCH_CLI):
+        pytest.skip("reference harness not built")
+    mine = vqb.device().bench_report(BENCH_RECORDS, fmt)
+    theirs = oracle.reference_bench_report(BENCH_RECORDS, fmt)
+    assert mine == theirs
+
+
+def test_bench_report_rejects_empty():
+    import paper_2406_19212_b200 as vqb
+    from paper_2406_19212_b200.abi import UsageError
+    with pytest.raises(UsageError):
+        vqb.device().bench_report([], "json")
