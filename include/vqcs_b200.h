@@ -343,6 +343,25 @@ VQB_API int vqb_sharded_upload(vqb_sharded *st, const vqb_c128 *host, uint64_t c
  * qubit (num_qubits entries, 0-based). Null outputs are skipped. */
 VQB_API int vqb_sharded_stats(const vqb_sharded *st, int64_t *rounds, int64_t *swapped_bits,
                               uint64_t *bytes_moved, int32_t *log2phys);
+/* save_state / load_state (io.hpp:56-128) of the whole sharded state: the
+ * layout is made canonical first (exchange rounds + local SWAPs), then the
+ * shards are streamed to the file back to back through a pinned chunk, so the
+ * dump is byte-identical to an unsharded save of the same state. Load: the
+ * file's qubit count must equal the state's (SHAPE otherwise); IO errors as
+ * vqb_state_load. */
+VQB_API int vqb_sharded_save(vqb_sharded *st, const char *path);
+/* gradient_pure (autodiff.hpp:95-156) with the sharded state as s0: the
+ * forward pass runs in place, the costate H|Phi> lives in a second set of
+ * shards that follows every exchange round, the reverse sweep runs per shard
+ * through the fused adjoint executor and the per-shard gradient vectors are
+ * summed in shard order. On return the state holds the reverse-swept Phi,
+ * i.e. s0 up to rounding (the reference keeps s0 const and works on copies,
+ * autodiff.hpp:111-124; a third full-size state per device would not fit at
+ * the sizes sharding is for). Outputs as vqb_gradient_pure. */
+VQB_API int vqb_sharded_gradient_pure(vqb_sharded *st, const vqb_op *ops, int64_t count,
+                                      const vqb_pauli_term *terms, int64_t num_terms, double *loss,
+                                      double *grads, int64_t capacity, int64_t *num_grads);
+VQB_API int vqb_sharded_load(vqb_sharded *st, const char *path, int32_t *precision);
 
 /* ---- state dump I/O: io.hpp:40-128 ---- */
 /* save_state (io.hpp:56-82): "VQCS" | u32 version 1 | u32 n | u8 precision

@@ -180,6 +180,44 @@ class DeviceState {
     vqb_state *s_ = nullptr;
 };
 
+// ---- a pure state sharded over the devices of this process (vqb_sharded_*) ----
+// The top log2(devices.size()) qubits are global; every call below has the
+// reference's semantics for a PureState<double> of n qubits (the unsharded
+// result is the oracle), see vqcs_b200.h.
+class ShardedState {
+  public:
+    ShardedState(int n, const std::vector<int> &devices) : n_(n) {
+        std::vector<int32_t> d(devices.begin(), devices.end());
+        check(vqb_sharded_create(n, static_cast<int32_t>(d.size()), d.data(), &s_));
+    }
+    ShardedState(const ShardedState &) = delete;
+    ShardedState &operator=(const ShardedState &) = delete;
+    ~ShardedState() { vqb_sharded_destroy(s_); }
+
+    int num_qubits() const { return n_; }
+    void set_zero() { check(vqb_sharded_set_zero(s_)); }
+    void upload(std::span<const std::complex<double>> a) {
+        check(vqb_sharded_upload(s_, reinterpret_cast<const vqb_c128 *>(a.data()), a.size()));
+    }
+    void download(std::span<std::complex<double>> a) const {
+        check(vqb_sharded_download(s_, reinterpret_cast<vqb_c128 *>(a.data()), a.size()));
+    }
+    double norm() const {
+        double v = 0;
+        check(vqb_sharded_norm(s_, &v));
+        return v;
+    }
+    void save(const std::string &path) { check(vqb_sharded_save(s_, path.c_str())); }
+    vqb_sharded *get() const { return s_; }
+
+  private:
+    int n_;
+    vqb_sharded *s_ = nullptr;
+};
+
+inline void apply_circuit(const vqcs::Circuit<double> &c, ShardedState &s);
+inline std::complex<double> expectation(const vqcs::PauliOperator &op, ShardedState &s);
+
 // ---- the replaced reference calls (same names and semantics) ----
 inline void apply_circuit(const vqcs::Circuit<double> &c, DeviceState &s) {
     const auto L = lower(c);
@@ -298,6 +336,22 @@ inline vqcs::GradientResult gradient_pure(const vqcs::PauliOperator &op,
     return detail::gradient(vqb_gradient_pure, op, c, s0, diag);
 }
 
+// gradient_pure on a sharded s0 (left as the reverse-swept Phi = s0 up to
+// rounding; see vqb_sharded_gradient_pure)
+inline vqcs::GradientResult gradient_pure(const vqcs::PauliOperator &op, const vqcs::Circuit<double> &c,
+                                          ShardedState &s0) {
+    const auto L = lower(c);
+    const auto O = lower(op);
+    vqcs::GradientResult r;
+    r.grads.assign(vqcs::active_parameters(c).size(), 0.0);
+    int64_t ng = 0;
+    check(vqb_sharded_gradient_pure(s0.get(), L.ops.data(), static_cast<int64_t>(L.ops.size()),
+                                    O.terms.data(), static_cast<int64_t>(O.terms.size()), &r.loss,
+                                    r.grads.data(), static_cast<int64_t>(r.grads.size()), &ng));
+    r.grads.resize(static_cast<size_t>(ng));
+    return r;
+}
+
 inline vqcs::GradientResult gradient_mixed(const vqcs::PauliOperator &op,
                                            const vqcs::Circuit<double> &c,
                                            const vqcs::MixedState<double> &dm0,
@@ -368,6 +422,18 @@ inline std::unique_ptr<DeviceState> load_state(const std::string &path,
     check(vqb_state_load(path.c_str(), &h, &prec));
     if (precision) *precision = static_cast<vqcs::Precision>(prec);
     return DeviceState::adopt(h);
+}
+
+inline void apply_circuit(const vqcs::Circuit<double> &c, ShardedState &s) {
+    const auto L = lower(c);
+    check(vqb_sharded_apply_circuit(s.get(), L.ops.data(), static_cast<int64_t>(L.ops.size())));
+}
+
+inline std::complex<double> expectation(const vqcs::PauliOperator &op, ShardedState &s) {
+    const auto O = lower(op);
+    vqb_c128 v{};
+    check(vqb_sharded_expectation(s.get(), O.terms.data(), static_cast<int64_t>(O.terms.size()), &v));
+    return {v.re, v.im};
 }
 
 } // namespace vqb

@@ -434,6 +434,9 @@ def bind_abi(lib: ct.CDLL, prefix: str) -> None:
         "sharded_expectation": (ct.c_int, [vp, term_p, i64, c128_p]),
         "sharded_download": (ct.c_int, [vp, c128_p, u64]),
         "sharded_upload": (ct.c_int, [vp, c128_p, u64]),
+        "sharded_save": (ct.c_int, [vp, ct.c_char_p]),
+        "sharded_gradient_pure": (ct.c_int, [vp, op_p, i64, term_p, i64, dp, dp, i64, ct.POINTER(i64)]),
+        "sharded_load": (ct.c_int, [vp, ct.c_char_p, ct.POINTER(i32)]),
         "sharded_stats": (ct.c_int, [vp, ct.POINTER(i64), ct.POINTER(i64), ct.POINTER(u64), ct.POINTER(i32)]),
         "alloc_stats": (ct.c_int, [ct.POINTER(i64), ct.POINTER(i64), ct.POINTER(u64), ct.POINTER(u64)]),
         "reset_alloc_peak": (ct.c_int, []),

@@ -777,6 +777,40 @@ VQB_API int vqb_sharded_stats(const vqb_sharded *s, int64_t *rounds, int64_t *sw
     });
 }
 
+VQB_API int vqb_sharded_gradient_pure(vqb_sharded *s, const vqb_op *ops, int64_t count,
+                                      const vqb_pauli_term *terms, int64_t nt, double *loss, double *grads,
+                                      int64_t cap, int64_t *ng) {
+    return guard([&] {
+        need(loss, "loss");
+        need(ng, "num_grads");
+        if (count > 0) need(ops, "ops");
+        if (nt > 0) need(terms, "terms");
+        const ShardedGradient r = sharded_gradient_pure(sh(s), ops, count, terms, nt);
+        if ((int64_t)r.grads.size() > cap)
+            raise(VQB_ERR_SHAPE, "gradient buffer too small: need " + std::to_string(r.grads.size()));
+        if (!r.grads.empty()) need(grads, "grads");
+        *loss = r.loss;
+        if (!r.grads.empty()) std::memcpy(grads, r.grads.data(), sizeof(double) * r.grads.size());
+        *ng = (int64_t)r.grads.size();
+    });
+}
+
+VQB_API int vqb_sharded_save(vqb_sharded *s, const char *path) {
+    return guard([&] {
+        need(path, "path");
+        sharded_save(sh(s), path);
+    });
+}
+
+VQB_API int vqb_sharded_load(vqb_sharded *s, const char *path, int32_t *precision) {
+    return guard([&] {
+        need(path, "path");
+        int prec = 0;
+        sharded_load(sh(s), path, &prec);
+        if (precision) *precision = prec;
+    });
+}
+
 // ---- state dumps (io.hpp:40-128) ----
 VQB_API int vqb_state_save(const vqb_state *s, const char *path) {
     return guard([&] {

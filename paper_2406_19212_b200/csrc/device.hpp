@@ -73,6 +73,8 @@ void collapse(DeviceState *s, int qubit, int outcome, double scale);
 // state dumps (io.hpp:40-128), streamed through a pinned chunk buffer
 void state_save(DeviceState *s, const char *path);
 DeviceState *state_load(const char *path, int *precision);
+void save_segments(const char *path, int n, const std::vector<DeviceState *> &segs);
+void load_segments(const char *path, int n, const std::vector<DeviceState *> &segs, int *precision);
 
 // ---- Pauli operator packing (observables.hpp:38-110) ----
 struct PauliGroupDev {

@@ -69,6 +69,13 @@ std::vector<int> mixing_bits(const Gate &phys_gate) {
 }
 
 void barrier(Sharded *s) {
+    // follower shards' streams first join their main shard's stream
+    for (const auto &set : s->followers)
+        for (int r = 0; r < s->P; ++r) {
+            DevScope on(s->devs[r]);
+            VQB_CUDA(cudaEventRecord(s->events[r], set[r]->stream));
+            VQB_CUDA(cudaStreamWaitEvent(s->shards[r]->stream, s->events[r], 0));
+        }
     for (int r = 0; r < s->P; ++r) {
         DevScope on(s->devs[r]);
         VQB_CUDA(cudaEventRecord(s->events[r], s->shards[r]->stream));
@@ -77,6 +84,7 @@ void barrier(Sharded *s) {
         DevScope on(s->devs[r]);
         for (int q = 0; q < s->P; ++q)
             if (q != r) VQB_CUDA(cudaStreamWaitEvent(s->shards[r]->stream, s->events[q], 0));
+        for (const auto &set : s->followers) VQB_CUDA(cudaStreamWaitEvent(set[r]->stream, s->events[r], 0));
     }
 }
 
@@ -199,15 +207,18 @@ void sharded_swap(Sharded *s, const std::vector<std::pair<int, int>> &pairs_in) 
                 int who, peer;
                 uint64_t j0, j1, sm, st;
             } parts[2] = {{r, r2, 0, half, sel(b), sel(a)}, {r2, r, half, count, sel(a), sel(b)}};
-            for (const auto &p : parts) {
-                DevScope on(s->devs[p.who]);
-                DeviceState *me = s->shards[p.who];
-                const ProfMark pf = prof_begin(me->stream);
-                k_swap_peer<<<148 * 4, 256, 0, me->stream>>>(me->amps, s->shards[p.peer]->amps, p.j0, p.j1,
-                                                             args, p.sm, p.st);
-                check_launch("k_swap_peer", pf);
+            for (size_t set = 0; set <= s->followers.size(); ++set) {
+                const std::vector<DeviceState *> &sh = set == 0 ? s->shards : s->followers[set - 1];
+                for (const auto &p : parts) {
+                    DevScope on(s->devs[p.who]);
+                    DeviceState *me = s->shards[p.who]; // its stream orders every set's swap
+                    const ProfMark pf = prof_begin(me->stream);
+                    k_swap_peer<<<148 * 4, 256, 0, me->stream>>>(sh[p.who]->amps, sh[p.peer]->amps, p.j0, p.j1,
+                                                                 args, p.sm, p.st);
+                    check_launch("k_swap_peer", pf);
+                }
+                s->bytes_moved += 2 * count * sizeof(double2);
             }
-            s->bytes_moved += 2 * count * sizeof(double2);
         }
     }
     barrier(s);
@@ -337,6 +348,242 @@ void sharded_apply_circuit(Sharded *s, const vqb_op *ops, int64_t count) {
     sharded_sync(s);
 }
 
+void sharded_canonicalize(Sharded *s) {
+    auto where = [&](int logical) { return s->log2phys[logical]; };
+    // global positions: logical p must sit at physical p
+    for (int p = s->n_loc; p < s->n; ++p) {
+        int cur = where(p);
+        if (cur == p) continue;
+        if (cur >= s->n_loc) { // on another global bit: bring it local first
+            int l = s->n_loc - 1;
+            sharded_swap(s, {{cur, l}});
+            cur = where(p);
+        }
+        sharded_swap(s, {{p, cur}});
+    }
+    // local positions: transpositions by SWAP gates on every shard
+    std::vector<Gate> swaps;
+    for (int l = 0; l < s->n_loc; ++l) {
+        const int cur = where(l);
+        if (cur == l) continue;
+        Gate g;
+        g.kind = VQB_GATE_SWAP;
+        g.m = 2;
+        g.pos[0] = l + 1;
+        g.pos[1] = cur + 1;
+        g.mat.assign(16, cplx(0));
+        g.mat[0] = g.mat[1 + 2 * 4] = g.mat[2 + 1 * 4] = g.mat[15] = 1.0;
+        swaps.push_back(g);
+        const int other = (int)(std::find(s->log2phys.begin(), s->log2phys.end(), l) - s->log2phys.begin());
+        s->log2phys[other] = cur;
+        s->log2phys[l] = l;
+    }
+    if (!swaps.empty())
+        for (int r = 0; r < s->P; ++r) {
+            DevScope on(s->devs[r]);
+            run_program(s->shards[r], swaps, true);
+        }
+    sharded_sync(s);
+}
+
+void sharded_save(Sharded *s, const char *path) {
+    sharded_canonicalize(s);
+    save_segments(path, s->n, s->shards);
+}
+
+void sharded_load(Sharded *s, const char *path, int *precision) {
+    sharded_sync(s);
+    load_segments(path, s->n, s->shards, precision);
+    for (int q = 0; q < s->n; ++q) s->log2phys[q] = q;
+}
+
+namespace {
+// this shard's share of a Pauli sum (X/Y factors already on local bits):
+// Z factors on global bits fold into the shard's sign
+PauliPack local_operator(const Sharded *s, int r, const vqb_pauli_term *terms, int64_t nterms) {
+    std::vector<vqb_pauli_term> lt(nterms);
+    std::vector<std::vector<int32_t>> qs(nterms);
+    std::vector<std::string> ls(nterms);
+    for (int64_t t = 0; t < nterms; ++t) {
+        double sign = 1;
+        for (int k = 0; k < terms[t].num_factors; ++k) {
+            const int p = s->log2phys[terms[t].qubits[k] - 1];
+            if (p >= s->n_loc) {
+                if ((r >> (p - s->n_loc)) & 1) sign = -sign;
+            } else {
+                qs[t].push_back(p + 1);
+                ls[t].push_back(terms[t].labels[k]);
+            }
+        }
+        lt[t].coeff.re = sign * terms[t].coeff.re;
+        lt[t].coeff.im = sign * terms[t].coeff.im;
+        lt[t].num_factors = (int32_t)qs[t].size();
+        lt[t].qubits = qs[t].data();
+        lt[t].labels = ls[t].data();
+    }
+    return pack_operator(lt.data(), nterms, false);
+}
+
+// the reverse step of element g restricted to shard r: positions on local
+// bits, matrices with the global (condition) bits fixed; false = identity
+bool local_step(const Sharded *s, int r, const Gate &pg, const cvec &inv, const std::vector<cvec> &dmats,
+                RevOp &out) {
+    unsigned fixed = 0, vals = 0;
+    for (int q = 0; q < pg.m; ++q) {
+        const int b = pg.pos[q] - 1;
+        if (b >= s->n_loc) {
+            fixed |= 1u << q;
+            vals |= (unsigned)((r >> (b - s->n_loc)) & 1) << q;
+        }
+    }
+    int nk = 0;
+    Gate g;
+    g.kind = VQB_GATE_GENERIC;
+    for (int q = 0; q < pg.m; ++q)
+        if (!((fixed >> q) & 1)) g.pos[nk++] = pg.pos[q];
+    auto sub = [&](const cvec &M) { return fixed ? restrict_matrix(M, pg.m, fixed, vals) : M; };
+    if (nk == 0) { // fully global diagonal: scalars, applied as a 1-bit op on bit 0
+        g.m = 1;
+        g.pos[0] = 1;
+        const cplx a = sub(inv)[0];
+        g.mat = {a, 0.0, 0.0, a};
+        out.phi_op = out.psi_op = g;
+        out.dmats.clear();
+        for (const cvec &d : dmats) {
+            const cplx x = sub(d)[0];
+            out.dmats.push_back({x, 0.0, 0.0, x});
+        }
+        return true;
+    }
+    g.m = nk;
+    g.mat = sub(inv);
+    out.phi_op = out.psi_op = g;
+    out.dmats.clear();
+    for (const cvec &d : dmats) out.dmats.push_back(sub(d));
+    if (out.dmats.empty()) {
+        const int d = 1 << nk;
+        for (int a = 0; a < d; ++a)
+            for (int b = 0; b < d; ++b)
+                if (g.mat[a + size_t(b) * d] != (a == b ? cplx(1) : cplx(0))) return true;
+        return false;
+    }
+    return true;
+}
+} // namespace
+
+ShardedGradient sharded_gradient_pure(Sharded *s, const vqb_op *ops, int64_t count,
+                                      const vqb_pauli_term *terms, int64_t nterms) {
+    const auto es = build_elements(ops, count);
+    std::vector<int64_t> base(count);
+    int64_t total = 0;
+    for (int64_t i = 0; i < count; ++i) {
+        if (es[i].channel) raise(VQB_ERR_TYPE, "gradient_pure: noisy circuits need gradient_mixed");
+        check_fit(es[i].gate.pos, es[i].gate.m, s->n);
+        base[i] = total;
+        total += es[i].gate.num_active();
+    }
+    ShardedGradient out;
+    sharded_apply_circuit(s, ops, count);
+    out.loss = sharded_expectation(s, terms, nterms).real(); // X/Y qubits are local from here on
+    out.grads.assign(total, 0.0);
+    if (total == 0) return out;
+    // Psi = H |Phi>, shard by shard
+    std::vector<DeviceState *> psi(s->P, nullptr);
+    struct Guard {
+        Sharded *s;
+        std::vector<DeviceState *> &psi;
+        ~Guard() {
+            s->followers.clear();
+            for (DeviceState *d : psi) state_destroy(d);
+        }
+    } guard{s, psi};
+    std::vector<double *> dgrads(s->P, nullptr);
+    static thread_local DevMem gbuf[kMaxDevices * 2];
+    for (int r = 0; r < s->P; ++r) {
+        DevScope on(s->devs[r]);
+        psi[r] = state_create(s->n_loc, 0);
+        VQB_CUDA(cudaStreamSynchronize(psi[r]->stream));
+        apply_operator(s->shards[r], psi[r]->amps, local_operator(s, r, terms, nterms), false);
+        // per-shard device gradient vector (shards on one device get their own)
+        int slot = 0;
+        for (int q = 0; q < r; ++q) slot += s->devs[q] == s->devs[r];
+        DevMem &m = gbuf[std::min(slot, kMaxDevices * 2 - 1)];
+        m.ensure(sizeof(double) * (size_t)total + 16);
+        dgrads[r] = static_cast<double *>(m.p);
+        VQB_CUDA(cudaMemsetAsync(dgrads[r], 0, sizeof(double) * (size_t)total, s->shards[r]->stream));
+        VQB_CUDA(cudaStreamSynchronize(s->shards[r]->stream)); // psi is read on the shard's stream below
+    }
+    s->followers.push_back(psi);
+    std::vector<std::vector<RevOp>> batch(s->P);
+    auto flush = [&] {
+        for (int r = 0; r < s->P; ++r) {
+            if (batch[r].empty()) continue;
+            DevScope on(s->devs[r]);
+            VQB_CUDA(cudaStreamSynchronize(psi[r]->stream));
+            run_reverse(s->shards[r], psi[r], batch[r], dgrads[r], true);
+            batch[r].clear();
+        }
+    };
+    auto step_mix = [&](const Gate &pg, const cvec &inv, const std::vector<cvec> &dm) {
+        Gate t = pg;
+        std::vector<int> mix;
+        t.mat = inv;
+        for (int b : mixing_bits(t)) mix.push_back(b);
+        for (const cvec &d : dm) {
+            t.mat = d;
+            for (int b : mixing_bits(t))
+                if (std::find(mix.begin(), mix.end(), b) == mix.end()) mix.push_back(b);
+        }
+        return mix;
+    };
+    for (int64_t i = count; i-- > 0;) {
+        const Gate &g = es[i].gate;
+        const cvec inv = gate_inverse(g).mat;
+        std::vector<cvec> dm;
+        for (int p = 0; p < g.np; ++p)
+            if (g.is_param[p]) dm.push_back(gate_derivative(g, p));
+        Gate pg = physical(s, g);
+        std::vector<int> need;
+        for (int b : step_mix(pg, inv, dm))
+            if (b >= s->n_loc) need.push_back(b);
+        if (!need.empty()) {
+            flush();
+            std::vector<std::vector<int>> upcoming;
+            for (int64_t j = i - 1; j >= 0 && j >= i - s->lookahead; --j) {
+                const Gate &h = es[j].gate;
+                std::vector<cvec> hd;
+                for (int p = 0; p < h.np; ++p)
+                    if (h.is_param[p]) hd.push_back(gate_derivative(h, p));
+                upcoming.push_back(step_mix(physical(s, h), gate_inverse(h).mat, hd));
+            }
+            std::vector<int> avoid;
+            for (int q = 0; q < pg.m; ++q) avoid.push_back(pg.pos[q] - 1);
+            bring_local(s, need, upcoming, avoid);
+            pg = physical(s, g);
+        }
+        for (int r = 0; r < s->P; ++r) {
+            RevOp op;
+            if (!local_step(s, r, pg, inv, dm, op)) continue;
+            if (!op.dmats.empty()) {
+                op.grad_base = base[i];
+                op.scale = 2.0; // grads = 2 Re(acc) (autodiff.hpp:147-149)
+            }
+            batch[r].push_back(std::move(op));
+        }
+    }
+    flush();
+    std::vector<double> h((size_t)total);
+    for (int r = 0; r < s->P; ++r) { // shard order: deterministic
+        DevScope on(s->devs[r]);
+        VQB_CUDA(cudaMemcpyAsync(h.data(), dgrads[r], sizeof(double) * (size_t)total, cudaMemcpyDeviceToHost,
+                                 s->shards[r]->stream));
+        VQB_CUDA(cudaStreamSynchronize(s->shards[r]->stream));
+        for (int64_t k = 0; k < total; ++k) out.grads[(size_t)k] += h[(size_t)k];
+    }
+    sharded_sync(s);
+    return out;
+}
+
 double sharded_norm(Sharded *s) {
     double acc = 0;
     for (int r = 0; r < s->P; ++r) {
@@ -370,29 +617,8 @@ cplx sharded_expectation(Sharded *s, const vqb_pauli_term *terms, int64_t nterms
     }
     cplx acc = 0;
     for (int r = 0; r < s->P; ++r) {
-        // this shard's operator: Z factors on global bits fold into a sign
-        std::vector<vqb_pauli_term> lt(nterms);
-        std::vector<std::vector<int32_t>> qs(nterms);
-        std::vector<std::string> ls(nterms);
-        for (int64_t t = 0; t < nterms; ++t) {
-            double sign = 1;
-            for (int k = 0; k < terms[t].num_factors; ++k) {
-                const int p = s->log2phys[terms[t].qubits[k] - 1];
-                if (p >= s->n_loc) {
-                    if ((r >> (p - s->n_loc)) & 1) sign = -sign;
-                } else {
-                    qs[t].push_back(p + 1);
-                    ls[t].push_back(terms[t].labels[k]);
-                }
-            }
-            lt[t].coeff.re = sign * terms[t].coeff.re;
-            lt[t].coeff.im = sign * terms[t].coeff.im;
-            lt[t].num_factors = (int32_t)qs[t].size();
-            lt[t].qubits = qs[t].data();
-            lt[t].labels = ls[t].data();
-        }
         DevScope on(s->devs[r]);
-        acc += expectation(s->shards[r], pack_operator(lt.data(), nterms, false));
+        acc += expectation(s->shards[r], local_operator(s, r, terms, nterms));
     }
     return acc;
 }

@@ -91,6 +91,27 @@ class ShardedHandle:
         amps = np.ascontiguousarray(amps, dtype=np.complex128)
         self.engine.check(self._f("upload")(self.handle, amps.ctypes.data_as(c128_p), ct.c_uint64(amps.size)))
 
+    def save(self, path: str) -> None:
+        self.engine.check(self._f("save")(self.handle, path.encode()))
+
+    def gradient_pure(self, op: PauliOperator, c: Circuit):
+        """gradient_pure with this state as s0 (left as the reverse-swept Phi)
+        -> (loss, grads)."""
+        p = c.pack() if isinstance(c, Circuit) else pack_ops(c)
+        arr, nt, _k = op.pack()
+        cap = max(1, c.num_active_params() if isinstance(c, Circuit) else 4096)
+        grads = np.zeros(cap, dtype=np.float64)
+        loss, ng = ct.c_double(), ct.c_int64()
+        self.engine.check(self._f("gradient_pure")(self.handle, p.arr, p.count, arr, nt, ct.byref(loss),
+                                                   grads.ctypes.data_as(ct.POINTER(ct.c_double)), cap,
+                                                   ct.byref(ng)))
+        return loss.value, grads[:ng.value]
+
+    def load(self, path: str) -> int:
+        p = ct.c_int32()
+        self.engine.check(self._f("load")(self.handle, path.encode(), ct.byref(p)))
+        return p.value
+
     def stats(self) -> dict:
         r, b = ct.c_int64(), ct.c_int64()
         m = ct.c_uint64()

@@ -103,12 +103,38 @@ int main() {
     double iomax = ls.num_qubits == n ? 0 : 1;
     for (std::uint64_t k = 0; k < a.size(); ++k) iomax = std::max(iomax, std::abs(ls.amplitudes[k] - a[k]));
 
+    // the sharded state (four shards; on a one-GPU box all on device 0):
+    // same circuit, same gradient as the unsharded reference
+    const int ns = 14;
+    Circuit<double> cs = bench::generate_rqc<double>(ns, 4, 77);
+    const PauliOperator ops = heisenberg_1d(ns);
+    vqb::ShardedState sh(ns, {0, 0, 0, 0});
+    vqb::apply_circuit(cs, sh);
+    PureState<double> rs(ns);
+    vqcs::apply_circuit(cs, rs, cfg);
+    std::vector<std::complex<double>> got(rs.size());
+    sh.download(got);
+    double smax = 0;
+    for (std::uint64_t k = 0; k < rs.size(); ++k) smax = std::max(smax, std::abs(rs[k] - got[k]));
+    const double se = std::abs(vqb::expectation(ops, sh) - vqcs::expectation(ops, rs, cfg));
+    sh.set_zero();
+    const auto sg = vqb::gradient_pure(ops, cs, sh);
+    const auto rg = vqcs::gradient_pure(ops, cs, PureState<double>(ns), cfg);
+    double sgmax = 0, rgmax = 0;
+    for (size_t i = 0; i < rg.grads.size() && i < sg.grads.size(); ++i) {
+        rgmax = std::max(rgmax, std::abs(rg.grads[i]));
+        sgmax = std::max(sgmax, std::abs(rg.grads[i] - sg.grads[i]));
+    }
+    const bool sh_ok = smax <= 1e-12 && se <= 1e-12 && sg.grads.size() == rg.grads.size() &&
+                       sgmax <= 1e-10 * rgmax && std::abs(sg.loss - rg.loss) <= 1e-10 * std::abs(rg.loss);
+
     std::printf("grad max|d|=%.3e (max|g|=%.3e) state max|d|=%.3e noisy max|d|=%.3e "
                 "non-invertible->vqcs::NonInvertibleChannelError:%d fuse max|d|=%.3e "
-                "measure outcomes equal:%d max|d|=%.3e dump max|d|=%.3e batch max|d|=%.3e\n",
-                dmax, gmax, amax, nmax, threw, fmax, m_ok, mmax, iomax, bmax);
+                "measure outcomes equal:%d max|d|=%.3e dump max|d|=%.3e batch max|d|=%.3e "
+                "sharded state max|d|=%.3e expectation |d|=%.3e gradient max|d|=%.3e\n",
+                dmax, gmax, amax, nmax, threw, fmax, m_ok, mmax, iomax, bmax, smax, se, sgmax);
     return (g_ok && amax <= 1e-12 && nmax <= 1e-10 * ngmax && threw && fmax <= 1e-15 && m_ok &&
-            mmax <= 1e-12 && iomax == 0 && bmax <= 1e-12)
+            mmax <= 1e-12 && iomax == 0 && bmax <= 1e-12 && sh_ok)
                ? 0
                : 1;
 }

@@ -88,3 +88,56 @@ def test_sharded_errors(dev):
     with pytest.raises(TypeError_):
         sh.apply_circuit(Circuit([standard_channel(ChannelKind.Depolarizing, 1, 0.1)]))
     sh.free()
+
+
+def test_sharded_dump_byte_identical(dev, ref, tmp_path):
+    """vqb_sharded_save after swaps = the reference's save_state of the same
+    state (io.hpp:56-82) byte for byte; loading it back restores the state."""
+    w = circuits.config1(rows=3, cols=5, cycles=6)
+    sh = dev.sharded(15, [0] * 4)
+    sh.apply_circuit(w.circuit)
+    assert sh.stats()["rounds"] > 0
+    a = str(tmp_path / "sharded.vqcs")
+    sh.save(a)
+    assert sh.stats()["log2phys"] == list(range(15))  # canonical after the save
+    r = ref.pure_state(15)
+    ref.apply_circuit(w.circuit, r)
+    b = str(tmp_path / "ref.vqcs")
+    ref.save_state(r, b)
+    da, db = open(a, "rb").read(), open(b, "rb").read()
+    assert da[:13] == db[:13]  # header: magic, version, n, precision
+    got = np.frombuffer(da[13:], dtype=np.complex128)
+    assert np.max(np.abs(got - ref.download(r))) <= 1e-12
+    # byte-identical to an unsharded dump of the same amplitudes
+    s = dev.from_amplitudes(got)
+    c = str(tmp_path / "plain.vqcs")
+    dev.save_state(s, c)
+    assert open(c, "rb").read() == da
+    sh2 = dev.sharded(15, [0] * 4)
+    assert sh2.load(a) == 2
+    assert np.array_equal(sh2.download(), got)
+    sh.free()
+    sh2.free()
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_sharded_gradient_matches_reference(dev, ref, P):
+    """gradient_pure on the sharded handle (QAOA: diagonal parametric steps
+    on global qubits; hardware-efficient ansatz with a Heisenberg-like
+    operator: X/Y factors and mixing parametric steps on global qubits)."""
+    rng = np.random.default_rng(30 + P)
+    n = 15
+    cases = [circuits.config2(n=16, p=2), circuits.config0(n=n, layers=2)]
+    for w in cases:
+        op = w.observable if w is cases[0] else random_operator(w.num_qubits, 6, rng)
+        sh = dev.sharded(w.num_qubits, [0] * P)
+        loss, g = sh.gradient_pure(op, w.circuit)
+        rl, rg = ref.gradient_pure(op, w.circuit, ref.pure_state(w.num_qubits))
+        assert abs(loss - rl) <= 1e-10 * max(1.0, abs(rl))
+        assert len(g) == len(rg)
+        assert np.max(np.abs(g - rg)) <= 1e-10 * max(1.0, np.max(np.abs(rg)))
+        back = sh.download()  # the reverse-swept Phi = s0 = |0...0>
+        e0 = np.zeros_like(back)
+        e0[0] = 1
+        assert np.max(np.abs(back - e0)) <= 1e-10
+        sh.free()
