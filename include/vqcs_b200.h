@@ -331,8 +331,9 @@ VQB_API int vqb_sharded_set_zero(vqb_sharded *st);
  * (TYPE for channels, as for a PureState). */
 VQB_API int vqb_sharded_apply_circuit(vqb_sharded *st, const vqb_op *ops, int64_t count);
 VQB_API int vqb_sharded_norm(vqb_sharded *st, double *out);
-/* expectation (observables.hpp:176-190); X/Y factors on global qubits are
- * swapped local first (the state's qubit map changes, its value does not). */
+/* expectation (observables.hpp:176-190). A term whose X/Y factors flip
+ * global qubits pairs shard r with shard r ^ x_global: its partials read the
+ * partner shard directly (peer memory), so no exchange round is needed. */
 VQB_API int vqb_sharded_expectation(vqb_sharded *st, const vqb_pauli_term *terms, int64_t num_terms,
                                     vqb_c128 *out);
 /* Whole state in canonical order (count = 2^num_qubits). */

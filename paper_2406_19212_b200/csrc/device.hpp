@@ -54,9 +54,16 @@ void apply_superop(DeviceState *s, const Channel &c);
 struct PauliPack; // host-side packed observable
 double norm_sq(DeviceState *s);                          // state.hpp:236-242
 cplx trace(DeviceState *s);                              // state.hpp:329-336
-void expectation_async(DeviceState *s, const PauliPack &p, double2 *out_dev);
+void expectation_async(DeviceState *s, const PauliPack &p, double2 *out_dev, const double2 *ket = nullptr);
 cplx expectation(DeviceState *s, const PauliPack &p);    // observables.hpp:176-213
+// sum_b conj(bra[b ^ x]) W(b) ket[b]: a term group whose X/Y factors flip
+// global qubits of a sharded state reads the ket from the partner shard
+cplx expectation_cross(DeviceState *bra, const double2 *ket, const PauliPack &p);
 void apply_operator(DeviceState *src, double2 *dst, const PauliPack &p, bool conj_coeffs);
+// dst (+)= H src_amps with src's stream and workspace (src_amps may be another
+// shard's buffer, on a peer device)
+void apply_operator_from(DeviceState *src, const double2 *src_amps, double2 *dst, const PauliPack &p,
+                         bool accumulate);
 void identity_costate(DeviceState *s, const PauliPack &p); // <<I|H as a ket, in place
 cplx dot_async_result(DeviceState *s, const double2 *a, const double2 *b); // <a|b>
 void dot_async(DeviceState *s, const double2 *a, const double2 *b, double2 *out_dev);

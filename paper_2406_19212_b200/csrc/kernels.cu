@@ -616,23 +616,27 @@ __device__ __forceinline__ double2 group_weight(const PauliTermDev *__restrict__
 }
 
 // <psi|H|psi> = sum_g sum_b conj(psi[b^x]) psi[b] W_g(b) (observables.hpp:176-190)
+// `ket` (nullable: = a) is the buffer read at b: a different shard for the
+// terms of a sharded state whose X/Y factors flip global qubits
 __global__ void __launch_bounds__(kThreads) k_expect_pure(const double2 *__restrict__ a, uint64_t size,
                                                           const PauliGroupDev *__restrict__ groups_g,
                                                           int ngroups,
                                                           const PauliTermDev *__restrict__ terms_g, int nterms, int staged,
                                                           double2 *partials, unsigned *counter,
-                                                          Epilogue ep) {
+                                                          Epilogue ep, const double2 *__restrict__ ket) {
     const PauliView pv = stage_pauli(groups_g, ngroups, terms_g, nterms, staged != 0);
     const PauliGroupDev *groups = pv.g;
     const PauliTermDev *terms = pv.t;
     double2 v[1] = {make_double2(0, 0)};
+    const bool same = ket == nullptr;
+    const double2 *k = same ? a : ket;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < size; b += stride) {
-        const double2 ab = a[b];
+        const double2 ab = k[b];
         for (int g = 0; g < ngroups; ++g) {
             const PauliGroupDev G = groups[g];
             const double2 w = group_weight(terms, G.first, G.count, b);
-            const double2 ax = G.xmask ? a[b ^ G.xmask] : ab;
+            const double2 ax = (G.xmask || !same) ? a[b ^ G.xmask] : ab;
             const double2 pr = cjfma(ax, ab, make_double2(0, 0));
             v[0] = cfma(pr, w, v[0]);
         }
@@ -663,7 +667,7 @@ __global__ void __launch_bounds__(kThreads) k_expect_mixed(const double2 *__rest
     reduce_epilogue<1>(v, 1, partials, counter, ep);
 }
 
-void expectation_async(DeviceState *s, const PauliPack &p, double2 *out_dev) {
+void expectation_async(DeviceState *s, const PauliPack &p, double2 *out_dev, const double2 *ket) {
     upload_operator(s, p);
     auto *groups = reinterpret_cast<const PauliGroupDev *>(s->ws.terms);
     auto *terms = reinterpret_cast<const PauliTermDev *>(
@@ -685,7 +689,7 @@ void expectation_async(DeviceState *s, const PauliPack &p, double2 *out_dev) {
         const ProfMark pf_ = prof_begin(s->stream);
         k_expect_pure<<<reduce_grid(s->size), kThreads, pauli_smem(p), s->stream>>>(
             s->amps, s->size, groups, ng, terms, (int)p.terms.size(), pauli_smem(p) > 0, s->ws.partials,
-            s->ws.counter, ep);
+            s->ws.counter, ep, ket);
         check_launch("k_expect_pure", pf_);
     }
 }
@@ -695,18 +699,25 @@ cplx expectation(DeviceState *s, const PauliPack &p) {
     return fetch_result(s);
 }
 
+cplx expectation_cross(DeviceState *bra, const double2 *ket, const PauliPack &p) {
+    if (bra->mixed) raise(VQB_ERR_INTERNAL, "expectation_cross: pure states only");
+    expectation_async(bra, p, bra->ws.result, ket);
+    return fetch_result(bra);
+}
+
 // dst[b] = sum_g psi[b^x] W_g(b^x) (apply_operator observables.hpp:216-237)
 __global__ void __launch_bounds__(kThreads) k_apply_operator(const double2 *__restrict__ a,
                                                              double2 *__restrict__ out, uint64_t size,
                                                              const PauliGroupDev *__restrict__ groups_g,
                                                              int ngroups,
-                                                             const PauliTermDev *__restrict__ terms_g, int nterms, int staged) {
+                                                             const PauliTermDev *__restrict__ terms_g, int nterms, int staged,
+                                                             int accumulate) {
     const PauliView pv = stage_pauli(groups_g, ngroups, terms_g, nterms, staged != 0);
     const PauliGroupDev *groups = pv.g;
     const PauliTermDev *terms = pv.t;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < size; b += stride) {
-        double2 acc = make_double2(0, 0);
+        double2 acc = accumulate ? out[b] : make_double2(0, 0);
         for (int g = 0; g < ngroups; ++g) {
             const PauliGroupDev G = groups[g];
             const uint64_t src = b ^ G.xmask;
@@ -768,7 +779,12 @@ __global__ void __launch_bounds__(kThreads) k_apply_zdiag(const double2 *__restr
 }
 
 void apply_operator(DeviceState *src, double2 *dst, const PauliPack &p, bool) {
-    bool zdiag = p.groups.size() == 1 && p.groups[0].xmask == 0 && src->size >= 256 &&
+    apply_operator_from(src, src->amps, dst, p, false);
+}
+
+void apply_operator_from(DeviceState *src, const double2 *src_amps, double2 *dst, const PauliPack &p,
+                         bool accumulate) {
+    bool zdiag = !accumulate && p.groups.size() == 1 && p.groups[0].xmask == 0 && src->size >= 256 &&
                  p.terms.size() * 16 <= 40 * 1024;
     for (const auto &t : p.terms) zdiag = zdiag && t.coeff.y == 0.0;
     if (zdiag) {
@@ -777,7 +793,7 @@ void apply_operator(DeviceState *src, double2 *dst, const PauliPack &p, bool) {
                                                              sizeof(PauliGroupDev) * p.groups.size());
         const ProfMark pf_ = prof_begin(src->stream);
         k_apply_zdiag<<<grid_for(src->size >> 3), kThreads, 16 * p.terms.size(), src->stream>>>(
-            src->amps, dst, src->size, terms, (int)p.terms.size());
+            src_amps, dst, src->size, terms, (int)p.terms.size());
         check_launch("k_apply_zdiag", pf_);
         return;
     }
@@ -786,8 +802,13 @@ void apply_operator(DeviceState *src, double2 *dst, const PauliPack &p, bool) {
     auto *terms = reinterpret_cast<const PauliTermDev *>(
         reinterpret_cast<const char *>(src->ws.terms) + sizeof(PauliGroupDev) * p.groups.size());
     const ProfMark pf_ = prof_begin(src->stream);
+    if (p.groups.empty()) {
+        if (!accumulate) VQB_CUDA(cudaMemsetAsync(dst, 0, sizeof(double2) * src->size, src->stream));
+        return;
+    }
     k_apply_operator<<<grid_for(src->size), kThreads, pauli_smem(p), src->stream>>>(
-        src->amps, dst, src->size, groups, (int)p.groups.size(), terms, (int)p.terms.size(), pauli_smem(p) > 0);
+        src_amps, dst, src->size, groups, (int)p.groups.size(), terms, (int)p.terms.size(), pauli_smem(p) > 0,
+        accumulate ? 1 : 0);
     check_launch("k_apply_operator", pf_);
 }
 

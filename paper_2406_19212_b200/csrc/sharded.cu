@@ -398,30 +398,60 @@ void sharded_load(Sharded *s, const char *path, int *precision) {
 }
 
 namespace {
-// this shard's share of a Pauli sum (X/Y factors already on local bits):
-// Z factors on global bits fold into the shard's sign
-PauliPack local_operator(const Sharded *s, int r, const vqb_pauli_term *terms, int64_t nterms) {
-    std::vector<vqb_pauli_term> lt(nterms);
+// The Pauli sum as seen from destination shard r: terms grouped by the
+// global part xg of their X mask (X and Y factors on global qubits). A term
+// of group xg maps the amplitudes of shard r ^ xg onto shard r; its Z and Y
+// factors on global qubits become the sign (-1)^popc((r ^ xg) & zg) of the
+// SOURCE shard and Y's factor i, folded into the coefficient; the local
+// factors stay (pack_operator handles them as for an unsharded state).
+struct CrossPack {
+    int xg;
+    PauliPack pack;
+};
+std::vector<CrossPack> cross_packs(const Sharded *s, int r, const vqb_pauli_term *terms, int64_t nterms) {
+    std::vector<int> order;
+    std::vector<std::vector<vqb_pauli_term>> lt;
     std::vector<std::vector<int32_t>> qs(nterms);
     std::vector<std::string> ls(nterms);
+    static const cplx ipow[4] = {1.0, cplx(0, 1), -1.0, cplx(0, -1)};
     for (int64_t t = 0; t < nterms; ++t) {
-        double sign = 1;
+        int xg = 0, zg = 0, ny = 0;
         for (int k = 0; k < terms[t].num_factors; ++k) {
-            const int p = s->log2phys[terms[t].qubits[k] - 1];
+            const int q = terms[t].qubits[k];
+            if (q < 1 || q > s->n) raise(VQB_ERR_INDEX, "expectation: operator acts on qubit " + std::to_string(q));
+            const char l = terms[t].labels[k] | 0x20;
+            if (l != 'x' && l != 'y' && l != 'z')
+                raise(VQB_ERR_VALIDITY, std::string("unknown Pauli label '") + terms[t].labels[k] + "'");
+            const int p = s->log2phys[q - 1];
             if (p >= s->n_loc) {
-                if ((r >> (p - s->n_loc)) & 1) sign = -sign;
+                const int bit = 1 << (p - s->n_loc);
+                if (l == 'x' || l == 'y') xg |= bit;
+                if (l == 'y' || l == 'z') zg |= bit;
+                if (l == 'y') ++ny;
             } else {
                 qs[t].push_back(p + 1);
                 ls[t].push_back(terms[t].labels[k]);
             }
         }
-        lt[t].coeff.re = sign * terms[t].coeff.re;
-        lt[t].coeff.im = sign * terms[t].coeff.im;
-        lt[t].num_factors = (int32_t)qs[t].size();
-        lt[t].qubits = qs[t].data();
-        lt[t].labels = ls[t].data();
+        const double sign = (__builtin_popcount((unsigned)((r ^ xg) & zg)) & 1) ? -1.0 : 1.0;
+        const cplx c = cplx(terms[t].coeff.re, terms[t].coeff.im) * ipow[ny & 3] * sign;
+        vqb_pauli_term u;
+        u.coeff.re = c.real();
+        u.coeff.im = c.imag();
+        u.num_factors = (int32_t)qs[t].size();
+        u.qubits = qs[t].data();
+        u.labels = ls[t].data();
+        size_t g = std::find(order.begin(), order.end(), xg) - order.begin();
+        if (g == order.size()) {
+            order.push_back(xg);
+            lt.emplace_back();
+        }
+        lt[g].push_back(u);
     }
-    return pack_operator(lt.data(), nterms, false);
+    std::vector<CrossPack> out;
+    for (size_t g = 0; g < order.size(); ++g)
+        out.push_back({order[g], pack_operator(lt[g].data(), (int64_t)lt[g].size(), false)});
+    return out;
 }
 
 // the reverse step of element g restricted to shard r: positions on local
@@ -484,7 +514,7 @@ ShardedGradient sharded_gradient_pure(Sharded *s, const vqb_op *ops, int64_t cou
     }
     ShardedGradient out;
     sharded_apply_circuit(s, ops, count);
-    out.loss = sharded_expectation(s, terms, nterms).real(); // X/Y qubits are local from here on
+    out.loss = sharded_expectation(s, terms, nterms).real();
     out.grads.assign(total, 0.0);
     if (total == 0) return out;
     // Psi = H |Phi>, shard by shard
@@ -503,7 +533,12 @@ ShardedGradient sharded_gradient_pure(Sharded *s, const vqb_op *ops, int64_t cou
         DevScope on(s->devs[r]);
         psi[r] = state_create(s->n_loc, 0);
         VQB_CUDA(cudaStreamSynchronize(psi[r]->stream));
-        apply_operator(s->shards[r], psi[r]->amps, local_operator(s, r, terms, nterms), false);
+        // Psi_r = sum over term groups of H_(r, xg) Phi_(r ^ xg)
+        bool first = true;
+        for (const CrossPack &cp : cross_packs(s, r, terms, nterms)) {
+            apply_operator_from(s->shards[r], s->shards[r ^ cp.xg]->amps, psi[r]->amps, cp.pack, !first);
+            first = false;
+        }
         // per-shard device gradient vector (shards on one device get their own)
         int slot = 0;
         for (int q = 0; q < r; ++q) slot += s->devs[q] == s->devs[r];
@@ -514,12 +549,16 @@ ShardedGradient sharded_gradient_pure(Sharded *s, const vqb_op *ops, int64_t cou
         VQB_CUDA(cudaStreamSynchronize(s->shards[r]->stream)); // psi is read on the shard's stream below
     }
     s->followers.push_back(psi);
+    barrier(s); // the costates read partner shards: done before any shard changes
     std::vector<std::vector<RevOp>> batch(s->P);
     auto flush = [&] {
         for (int r = 0; r < s->P; ++r) {
             if (batch[r].empty()) continue;
             DevScope on(s->devs[r]);
-            VQB_CUDA(cudaStreamSynchronize(psi[r]->stream));
+            // the adjoint executor's scratch is per thread and device: shards
+            // sharing a device (the one-GPU test layout) take turns
+            for (int q = 0; q < r; ++q)
+                if (s->devs[q] == s->devs[r]) VQB_CUDA(cudaStreamSynchronize(s->shards[q]->stream));
             run_reverse(s->shards[r], psi[r], batch[r], dgrads[r], true);
             batch[r].clear();
         }
@@ -594,31 +633,14 @@ double sharded_norm(Sharded *s) {
 }
 
 cplx sharded_expectation(Sharded *s, const vqb_pauli_term *terms, int64_t nterms) {
-    // X/Y factors must act on local bits: swap global ones local first
-    std::vector<int> xy_logical;
-    for (int64_t t = 0; t < nterms; ++t)
-        for (int k = 0; k < terms[t].num_factors; ++k) {
-            const char l = terms[t].labels[k] | 0x20;
-            const int q = terms[t].qubits[k];
-            if (q < 1 || q > s->n) raise(VQB_ERR_INDEX, "expectation: operator acts on qubit " + std::to_string(q));
-            if ((l == 'x' || l == 'y') &&
-                std::find(xy_logical.begin(), xy_logical.end(), q - 1) == xy_logical.end())
-                xy_logical.push_back(q - 1);
-        }
-    std::vector<int> need, avoid;
-    for (int q : xy_logical) {
-        avoid.push_back(s->log2phys[q]);
-        if (s->log2phys[q] >= s->n_loc) need.push_back(s->log2phys[q]);
-    }
-    if (!need.empty()) {
-        if ((int)xy_logical.size() > s->n_loc)
-            raise(VQB_ERR_UNSUPPORTED, "expectation: too many X/Y qubits for the local shards");
-        bring_local(s, need, {}, avoid);
-    }
+    // every term group reads its ket from the partner shard r ^ xg (peer
+    // memory across devices): no exchange round, the layout is unchanged
+    barrier(s);
     cplx acc = 0;
     for (int r = 0; r < s->P; ++r) {
         DevScope on(s->devs[r]);
-        acc += expectation(s->shards[r], local_operator(s, r, terms, nterms));
+        for (const CrossPack &cp : cross_packs(s, r, terms, nterms))
+            acc += expectation_cross(s->shards[r], s->shards[r ^ cp.xg]->amps, cp.pack); // shard order
     }
     return acc;
 }

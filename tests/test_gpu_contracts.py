@@ -60,15 +60,15 @@ def test_reverse_sweep_accumulates_tied_indices(dev, ref):
 
 
 def test_bitwise_run_to_run(dev):
-    w = circuits.config2(n=21, p=2)
-    s0 = dev.pure_state(21)
+    w = circuits.config2(n=22, p=2)
+    s0 = dev.pure_state(22)
     l1, g1 = dev.gradient_pure(w.observable, w.circuit, s0)
     l2, g2 = dev.gradient_pure(w.observable, w.circuit, s0)
     assert l1 == l2 and np.array_equal(g1, g2)
-    c = circuits.config1(rows=3, cols=7, cycles=8).circuit
+    c = circuits.config1(rows=2, cols=11, cycles=8).circuit
     outs = []
     for _ in range(2):
-        s = dev.pure_state(21)
+        s = dev.pure_state(22)
         dev.apply_circuit(c, s)
         outs.append((dev.download(s), dev.norm(s), dev.expectation(w.observable, s)))
     assert np.array_equal(outs[0][0], outs[1][0])

@@ -36,7 +36,7 @@ from paper_2406_19212_b200 import circuits
 from paper_2406_19212_b200.abi import Circuit, GateKind, standard_gate
 
 from helpers import (product_projections_device, random_state, rel_err, sample_amplitudes,
-                     sample_indices)
+                     sample_indices, state_projections)
 
 pytestmark = pytest.mark.gpu
 
@@ -102,7 +102,7 @@ def test_qaoa_gradient_default_path(dev, fast_ref, n):
     r0 = fast_ref.pure_state(n)
     rl, rg = fast_ref.gradient_pure(w.observable, w.circuit, r0)
     assert abs(out["loss"] - rl) <= 1e-10 * max(abs(rl), 1e-300)
-    assert len(out["g"]) == len(rg) == 600
+    assert len(out["g"]) == len(rg) == 20 * n  # p (|E| + n) = 8 (3n/2 + n)
     assert rel_err(out["g"], rg) <= 1e-10
     p, ne = w.extra["p"], len(w.extra["edges"])
     assert rel_err(circuits.qaoa_tied_gradients(out["g"], n, ne, p),
@@ -194,4 +194,8 @@ def test_random_circuit_full_size_vs_reference(dev, golden, name):
         pp = product_projections_device(dev, s, n)
         perr = float(np.max(np.abs(pp - c(g["product_projections"]))))
         assert perr <= 1e-9, perr
+    if "projections" in g and n <= 28:  # hashed-weight projections (host side, chunked)
+        hp = state_projections(dev, s, 1 << n)
+        herr = float(np.max(np.abs(hp - c(g["projections"]))))
+        assert herr <= 1e-9, herr
     s.free()

@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 
 from paper_2406_19212_b200 import circuits
-from paper_2406_19212_b200.abi import Circuit, GateKind, parametric_gate, standard_gate
+from paper_2406_19212_b200.abi import Circuit, GateKind, PauliTerm, parametric_gate, standard_gate
 
 from helpers import random_gate, random_operator, random_state
 
@@ -40,8 +40,10 @@ def test_sharded_random_circuit(dev, ref, P, n):
     assert st["rounds"] > 0 and st["swapped_bits"] >= st["rounds"]
     assert abs(sh.norm() - 1) <= 1e-12
     op = random_operator(n, 10, rng)
+    op.add_term(PauliTerm([(n, "x"), (n - 1, "y"), (1, "z")], 0.3))  # X/Y on global qubits
+    log_before = sh.stats()["log2phys"]
     assert abs(sh.expectation(op) - ref.expectation(op, r)) <= 1e-12
-    # the expectation may have swapped X/Y qubits local: the state is unchanged
+    assert sh.stats()["log2phys"] == log_before  # partner shards read in place: no exchange
     assert np.max(np.abs(sh.download() - want)) <= 1e-12
     sh.free()
 
