@@ -759,7 +759,6 @@ void execute(DeviceState *sphi, DeviceState *spsi, const std::vector<FusedOp> &f
     }
 VQB_DECLARE_REGSTAGE(rs16)
 VQB_DECLARE_REGSTAGE(rs8)
-VQB_DECLARE_REGSTAGE(rs16w)
 #undef VQB_DECLARE_REGSTAGE
 
 std::string debug_jit_source(int regs, const void *params, size_t nbytes, bool rev, double *flops) {
@@ -798,11 +797,6 @@ void run_program_fused(DeviceState *s, const std::vector<Gate> &prog) {
     // register-resident executor for states of >= 2^12 amplitudes
     // (VQB_EXECUTOR=smem selects the shared-memory interpreter instead)
     if (!smem_forced()) {
-        const char *rg = std::getenv("VQB_REGS");
-        if (rg && std::strcmp(rg, "16w") == 0 && rs16w::regstage_available(s->pn)) {
-            rs16w::run_program_reg(s, prog);
-            return;
-        }
         if (use_rs8(false) ? rs8::regstage_available(s->pn) : rs16::regstage_available(s->pn)) {
             if (use_rs8(false)) rs8::run_program_reg(s, prog);
             else rs16::run_program_reg(s, prog);

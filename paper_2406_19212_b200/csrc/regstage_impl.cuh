@@ -843,7 +843,11 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
     // elements untouched); the scalars' product is applied once at the end
     // of the launch by one extra op (a 1x1 "diagonal" without conditions).
     // Results equal the unfactored product up to rounding.
-    factor = factor && !rev;
+    // Adjoint sweeps (same scalar on Phi and Psi, non-pair steps only): the
+    // states run as true / c; a parametric step is factored only when its
+    // contribution is taken before its update (derivative generator G_p),
+    // and that contribution is rescaled by |c|^2 through its slot scale;
+    // the launch ends with both states multiplied by c.
     cplx scale = 1.0;
     const int ops_cap = factor ? kMaxOps - 1 : kMaxOps;
     const int pool_cap = factor ? kMaxPool - 1 : kMaxPool;
@@ -917,46 +921,9 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
             const unsigned mix = mixmask(*blocks[i]);
             if (__builtin_popcount(rset | mix) <= RB) rset |= mix;
         }
-        // Stable layouts (opt-in, VQB_STABLE_LAYOUT=1): after the first
-        // sub-stage, bits stay where they are unless they must enter the
-        // registers; an entering bit swaps places with a leaving one, so the
-        // specialised kernels can relayout by warp shuffles when the entering
-        // bits are lane bits. Measured slower than fresh layouts with
-        // conflict-free lanes (QAOA adjoint 577 -> 615 ms), hence off.
-        const bool stable = P.nsubs > 0 && env_int("VQB_STABLE_LAYOUT", 0) != 0;
-        if (stable) {
-            const RLayout &A = P.subs[P.nsubs - 1].L;
-            for (int b = 0; b < RB && __builtin_popcount(rset) < RB; ++b) rset |= 1u << A.reg[b];
-        }
         for (int j = K - 1; j >= 0 && __builtin_popcount(rset) < RB; --j) rset |= 1u << j;
         RSub &sb = P.subs[P.nsubs++];
-        if (stable) {
-            const RLayout A = P.subs[P.nsubs - 2].L;
-            RLayout B = A;
-            std::vector<int> leaving, entering;
-            for (int b = 0; b < RB; ++b)
-                if (!((rset >> A.reg[b]) & 1)) leaving.push_back(b);
-            for (int j = 0; j < K; ++j) {
-                if (!((rset >> j) & 1)) continue;
-                bool in = false;
-                for (int b = 0; b < RB; ++b) in |= A.reg[b] == j;
-                if (!in) entering.push_back(j);
-            }
-            // lane bits first (shuffle-able), then warp bits
-            auto thr_pos = [&](int j) {
-                for (int b = 0; b < TB; ++b)
-                    if (A.thr[b] == j) return b;
-                return -1;
-            };
-            std::stable_sort(entering.begin(), entering.end(),
-                             [&](int x, int y) { return (thr_pos(x) >= 5) < (thr_pos(y) >= 5); });
-            for (size_t k2 = 0; k2 < entering.size() && k2 < leaving.size(); ++k2) {
-                const int p = leaving[k2], e = entering[k2], q = thr_pos(e);
-                B.thr[q] = A.reg[p];
-                B.reg[p] = e;
-            }
-            sb.L = B;
-        } else {
+        {
             int nr = 0;
             std::vector<int> free_bits;
             for (int j = 0; j < K; ++j) {
@@ -1012,6 +979,39 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
                 }
             }
             const int D = 1 << f.nt, dd = D * D;
+            cplx scale_before = scale; // Phi and Psi computed = true / scale before this op
+            // Derivative generators: the contribution Re<psi|D_p inv phi>
+            // can be taken before the update with G_p = D_p inv; for
+            // rotations G_p is a scaled Pauli (dRx inv = -i X / 2), for
+            // superoperator steps a diagonal -- much sparser than D_p.
+            // Store whichever has fewer nonzero real/imaginary parts
+            // (ROp::unit bit 1 marks G; specialised kernels only).
+            bool use_g = false;
+            cvec G;
+            if (o.np > 0 && gdiff && f.nt >= 1 && f.nt <= 2 && !f.pair) {
+                const int nsubm = 1 << f.nc;
+                G.assign(f.sub_d.size(), cplx(0));
+                auto weight = [](const cplx &x) { return (x.real() != 0.0) + (x.imag() != 0.0); };
+                int wd = 0, wg = 0;
+                for (int p = 0; p < f.np; ++p)
+                    for (int c = 0; c < nsubm; ++c) {
+                        const cplx *Dm = f.sub_d.data() + ((size_t(p) << f.nc) + c) * dd;
+                        const cplx *U = f.sub_phi.data() + size_t(c) * dd;
+                        cplx *Gm = G.data() + ((size_t(p) << f.nc) + c) * dd;
+                        for (int col = 0; col < D; ++col)
+                            for (int row = 0; row < D; ++row) {
+                                cplx acc = 0;
+                                for (int k2 = 0; k2 < D; ++k2) acc += Dm[row + k2 * D] * U[k2 + col * D];
+                                // entries at rounding level of an exact zero are zero
+                                if (std::abs(acc.real()) < 1e-15 * 4) acc.real(0.0);
+                                if (std::abs(acc.imag()) < 1e-15 * 4) acc.imag(0.0);
+                                Gm[row + col * D] = acc;
+                                wg += weight(acc);
+                                wd += weight(Dm[row + col * D]);
+                            }
+                    }
+                use_g = wg < wd;
+            }
             // push 2^nc sub-matrices of `src` (permuted to ascending register
             // order); returns the pool offset and the identity mask
             auto push = [&](const cvec &src, size_t first_block, unsigned long long *ident) {
@@ -1075,10 +1075,11 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
                 };
                 o.mat = pushx(f.sub_phi, &o.ident);
                 if (f.pair) o.mat_psi = pushx(f.sub_psi, &o.ident_psi);
-            } else if (factor && !f.pair) {
+            } else if (factor && !f.pair && (!rev || f.np == 0 || use_g)) {
                 cvec sub = f.sub_phi;
                 double c = 0;
                 const cplx sc = best_scale(sub.data(), f.nt, f.nc, &c);
+                scale_before = scale;
                 if (sc != cplx(1)) {
                     divide_by(sub.data(), sub.size(), sc);
                     scale *= sc;
@@ -1095,38 +1096,6 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
             }
             if (o.np > 0) {
                 o.mat_d = (unsigned)npool;
-                // Derivative generators: the contribution Re<psi|D_p inv phi>
-                // can be taken before the update with G_p = D_p inv; for
-                // rotations G_p is a scaled Pauli (dRx inv = -i X / 2), for
-                // superoperator steps a diagonal -- much sparser than D_p.
-                // Store whichever has fewer nonzero real/imaginary parts
-                // (ROp::unit bit 1 marks G; specialised kernels only).
-                bool use_g = false;
-                cvec G;
-                if (gdiff && f.nt >= 1 && f.nt <= 2 && !f.pair) {
-                    const int nsubm = 1 << f.nc;
-                    G.assign(f.sub_d.size(), cplx(0));
-                    auto weight = [](const cplx &x) { return (x.real() != 0.0) + (x.imag() != 0.0); };
-                    int wd = 0, wg = 0;
-                    for (int p = 0; p < f.np; ++p)
-                        for (int c = 0; c < nsubm; ++c) {
-                            const cplx *Dm = f.sub_d.data() + ((size_t(p) << f.nc) + c) * dd;
-                            const cplx *U = f.sub_phi.data() + size_t(c) * dd;
-                            cplx *Gm = G.data() + ((size_t(p) << f.nc) + c) * dd;
-                            for (int col = 0; col < D; ++col)
-                                for (int row = 0; row < D; ++row) {
-                                    cplx acc = 0;
-                                    for (int k2 = 0; k2 < D; ++k2) acc += Dm[row + k2 * D] * U[k2 + col * D];
-                                    // entries at rounding level of an exact zero are zero
-                                    if (std::abs(acc.real()) < 1e-15 * 4) acc.real(0.0);
-                                    if (std::abs(acc.imag()) < 1e-15 * 4) acc.imag(0.0);
-                                    Gm[row + col * D] = acc;
-                                    wg += weight(acc);
-                                    wd += weight(Dm[row + col * D]);
-                                }
-                        }
-                    use_g = wg < wd;
-                }
                 if (use_g) o.unit |= 2;
                 for (int p = 0; p < f.np; ++p) push(use_g ? G : f.sub_d, size_t(p) << f.nc, nullptr);
                 if (f.nt == 0) {
@@ -1139,8 +1108,10 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
                 }
                 o.ident = 0;
                 o.slot = nslots;
+                // contributions of the scaled states: <psi/c|G|phi/c> = |1/c|^2 <psi|G|phi>
+                const double corr = std::norm(scale_before);
                 for (int p = 0; p < f.np; ++p) {
-                    slots.scale.push_back(f.scale);
+                    slots.scale.push_back(f.scale * corr);
                     slots.dst.push_back(f.grad_base + p);
                 }
                 nslots += f.np;
@@ -1229,9 +1200,8 @@ template <bool REV, bool WIDE> int grid_size(unsigned long long ntiles, size_t s
 // Lanes per warp that keep a partial sum of a gradient slot (the rest of the
 // warp reduction happens in the block's final sum): VQB_JIT_REDLANES (1, 2,
 // 4, 8); measured best 4 for 8-register adjoints (QAOA 578 -> 556 ms), 2 for
-// 16-register ones (noisy 915 -> 898 ms); 1 for batched reductions.
-int red_lanes_of(bool batch) {
-    if (batch) return 1;
+// 16-register ones (noisy 915 -> 898 ms).
+int red_lanes_of() {
     int v = env_int("VQB_JIT_REDLANES", R >= 16 ? 2 : 4);
     return v >= 8 ? 8 : v >= 4 ? 4 : v >= 2 ? 2 : 1;
 }
@@ -1411,10 +1381,10 @@ std::string jit_wide_op(const RParams &P, int sub, const ROp &op, const std::vec
         sw_off[r] = swz(o);
     }
     // conditioned matrices come from the shared-memory pool copy (run-time
-    // sub-matrix index); unconditioned ones may be parameter-bank operands at
-    // literal offsets (measured: faster in forward kernels, slower in adjoint
-    // kernels, whose larger pools outgrow the constant cache)
-    const bool cond = op.nc > 0 || !param_ok || !env_int("VQB_JIT_WIDE_PARAM", 1);
+    // sub-matrix index); unconditioned ones are parameter-bank operands at
+    // literal offsets where the caller allows it (forward kernels; adjoint
+    // pools outgrow the constant cache)
+    const bool cond = op.nc > 0 || !param_ok;
     if (cond) *needs_spool = true;
     std::string e = "    {\n";
     if (!inplace) {
@@ -2025,50 +1995,11 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
     // slots are pending, so the reduction overlaps the following steps and at
     // most acc_budget accumulators hold registers (dozens of slots per launch
     // would otherwise spill).
-    // Reductions go in batches of 8 slots through a warp transpose-reduce
-    // (9 double shuffles for 8 slots instead of 40; lane l ends with slot
-    // (l >> 2) & 7); VQB_JIT_ACCBATCH=0 reduces slot by slot.
-    const bool acc_batch = env_int("VQB_JIT_ACCBATCH", 0) != 0; // measured: no gain (QAOA), spills (rs16)
-    const int red_lanes = red_lanes_of(acc_batch);
+    const int red_lanes = red_lanes_of();
     // measured: 6 for 8-register sweeps, 3 for the register-heavy 16-register ones
-    const int acc_budget = env_int("VQB_JIT_ACC", acc_batch ? 8 : (R >= 16 ? 3 : 6));
+    const int acc_budget = env_int("VQB_JIT_ACC", R >= 16 ? 3 : 6);
     std::vector<int> open_slots;
-    auto flush_batch = [&](const std::vector<int> &sl) {
-        std::string e = "    {\n      double a0";
-        for (int k = 1; k < 8; ++k) e += ", a" + I(k);
-        e += ";\n";
-        for (int k = 0; k < 8; ++k)
-            e += "      a" + I(k) + " = " + (k < (int)sl.size() ? "acc_s" + I(sl[k]) : std::string("0.0")) + ";\n";
-        e += "      const bool h4 = lane & 16, h3 = lane & 8, h2 = lane & 4;\n";
-        for (int k = 0; k < 4; ++k)
-            e += "      const double b" + I(k) + " = (h4 ? a" + I(k + 4) + " : a" + I(k) +
-                 ") + __shfl_xor_sync(0xffffffffu, h4 ? a" + I(k) + " : a" + I(k + 4) + ", 16);\n";
-        for (int k = 0; k < 2; ++k)
-            e += "      const double c" + I(k) + " = (h3 ? b" + I(k + 2) + " : b" + I(k) +
-                 ") + __shfl_xor_sync(0xffffffffu, h3 ? b" + I(k) + " : b" + I(k + 2) + ", 8);\n";
-        e += "      double d = (h2 ? c1 : c0) + __shfl_xor_sync(0xffffffffu, h2 ? c0 : c1, 4);\n";
-        e += "      d += __shfl_xor_sync(0xffffffffu, d, 2);\n      d += __shfl_xor_sync(0xffffffffu, d, 1);\n";
-        // slot index per lane group
-        e += "      const int q = (lane >> 2) & 7;\n      if ((lane & 3) == 0) {\n";
-        for (int k = 0; k < (int)sl.size(); ++k)
-            e += "        if (q == " + I(k) + ") red[" + I(sl[k] * NW * red_lanes) + " + warp * " + I(red_lanes) +
-                 "] = d;\n";
-        e += "      }\n    }\n";
-        emit(e);
-    };
     auto flush_slots = [&](int keep) {
-        if (acc_batch) {
-            while ((int)open_slots.size() >= 8 && (int)open_slots.size() > keep) {
-                std::vector<int> b(open_slots.begin(), open_slots.begin() + 8);
-                open_slots.erase(open_slots.begin(), open_slots.begin() + 8);
-                flush_batch(b);
-            }
-            if (keep == 0 && !open_slots.empty()) {
-                flush_batch(open_slots);
-                open_slots.clear();
-            }
-            return;
-        }
         while ((int)open_slots.size() > keep) {
             const int sl = open_slots.front();
             open_slots.erase(open_slots.begin());
@@ -2163,15 +2094,8 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
                     const int m = rmask_of(P.ops[sb.op_begin + j]);
                     if (std::find(masks.begin(), masks.end(), m) == masks.end()) masks.push_back(m);
                 }
-                // Phi and Psi stay in registers through the run (VQB_JIT_STASH=1
-                // parks them in shared memory: measured slower since the class
-                // sums replaced per-element z and phase registers)
-                const bool stash = env_int("VQB_JIT_STASH", 0) != 0;
+                // Phi and Psi stay in registers through the run
                 emit("    {\n");
-                if (stash)
-                    for (int i = 0; i < R; ++i)
-                        emit("      xbuf[" + I(i * T) + " + t] = vf[" + I(i) + "]; xbuf2[" + I(i * T) + " + t] = vg[" +
-                             I(i) + "];\n");
                 emit("      double2 z[" + I(R) + "];\n");
                 for (int i = 0; i < R; ++i)
                     emit("      z[" + I(i) + "] = make_double2(fma(vg[" + I(i) + "].x, vf[" + I(i) + "].x, vg[" + I(i) +
@@ -2276,18 +2200,12 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
                             fl += 6;
                         }
                     }
-                    const std::string sf = stash ? "xbuf[" + I(i * T) + " + t]" : "vf[" + I(i) + "]";
-                    const std::string sg = stash ? "xbuf2[" + I(i * T) + " + t]" : "vg[" + I(i) + "]";
-                    if (ph.empty()) {
-                        if (stash) emit("      vf[" + I(i) + "] = " + sf + "; vg[" + I(i) + "] = " + sg + ";\n");
-                        continue;
-                    }
-                    emit("      { const double2 ph = " + ph + "; vf[" + I(i) + "] = cmul(ph, " + sf + "); vg[" + I(i) +
-                         "] = cmul(ph, " + sg + "); }\n");
+                    if (ph.empty()) continue;
+                    emit("      { const double2 ph = " + ph + "; vf[" + I(i) + "] = cmul(ph, vf[" + I(i) +
+                         "]); vg[" + I(i) + "] = cmul(ph, vg[" + I(i) + "]); }\n");
                     fl += 12;
                 }
-                // other threads' later relayout / wide-op writes reuse these slots
-                emit(stash ? "      __syncthreads();\n    }\n" : "    }\n");
+                emit("    }\n");
                 k = run_end - 1;
                 continue;
             }
@@ -2358,11 +2276,13 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
             };
             auto mcls = [&](unsigned off, int cs) {
                 return [=, &P](int k) {
-                    int c = 0;
+                    int c = -1;
                     for (int cc = 0; cc < nsub; ++cc)
-                        if (dynamic ? (cc & rmask) == cs : cc == cs)
-                            c |= pool_cls(P, off + (unsigned)(cc * dd + k), 1, 0);
-                    return c;
+                        if (dynamic ? (cc & rmask) == cs : cc == cs) {
+                            const int e = pool_ucls(P, off + (unsigned)(cc * dd + k), 1, 0);
+                            c = c < 0 ? e : merge_cls(c, e);
+                        }
+                    return c < 0 ? 0 : c;
                 };
             };
             if (dynamic) emit("    {\n      const int cd = 0" + dyn + ";\n");
@@ -2542,7 +2462,7 @@ std::string shape_key(const RParams &P, bool rev) {
             cls[(size_t)i >> 1] = (char)(cls[(size_t)i >> 1] | (pool_ucls(P, (unsigned)i, 1, 0) << (4 * (i & 1))));
         key += cls;
     }
-    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_JIT_WIDE_PARAM", "VQB_WIDE_REGS", "VQB_JIT_GDIFF", "VQB_JIT_ACCBATCH", "VQB_JIT_STASH", "VQB_JIT_SHUFFLE", "VQB_STABLE_LAYOUT", "VQB_JIT_REDLANES", "VQB_JIT_DIRECT", "VQB_JIT_FACTOR"}) {
+    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_WIDE_REGS", "VQB_JIT_GDIFF", "VQB_JIT_SHUFFLE", "VQB_JIT_REDLANES", "VQB_JIT_DIRECT", "VQB_JIT_FACTOR"}) {
         const char *v = std::getenv(e);
         key += '|';
         if (v) key += v;
@@ -2626,7 +2546,8 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
     // structure-aware kernels: merge blocks only where the emitted cost does
     // not grow, factor scalars out of the forward matrices (VQB_JIT_FACTOR=0:
     // merge whenever possible, no factoring)
-    const bool cost_fusion = use_jit && !REV && env_int("VQB_JIT_FACTOR", 1) != 0;
+    const bool factor_on = use_jit && env_int("VQB_JIT_FACTOR", 1) != 0;
+    const bool cost_fusion = factor_on && !REV;
     bool batching = false;
     std::vector<Action> pending;
     auto issue = [&](Action &act) {
@@ -2652,7 +2573,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
         if (act.jit && act.jit->k.e && REV) {
             const JitShape &sh = *act.jit;
             const size_t sm = (size_t)(sh.xtiles * TS + (sh.spool ? P.npool : 0)) * sizeof(double2) +
-                              sizeof(double) * (size_t)P.nslots * NW * red_lanes_of(env_int("VQB_JIT_ACCBATCH", 0) != 0);
+                              sizeof(double) * (size_t)P.nslots * NW * red_lanes_of();
             void *a0 = sphi->amps, *a1 = spsi->amps, *pp = m_jpartial.p;
             void *args[4] = {&a0, &a1, &pp, P.pool};
             jit::launch(sh.k, (unsigned)ntiles, T, sm, st, args);
@@ -2737,7 +2658,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             {
                 HostAcc ha(&t_lower);
                 lower_stage_reg(sg, blocks, remaining, pn, REV, P, slots, regwide,
-                                use_jit && env_int("VQB_JIT_GDIFF", 1) != 0, cost_fusion);
+                                use_jit && env_int("VQB_JIT_GDIFF", 1) != 0, factor_on);
             }
             P.partial_ld = total_slots;
             if (stats) {

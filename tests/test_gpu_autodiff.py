@@ -283,8 +283,7 @@ def test_specialised_adjoint_matches_reference(dev, ref, monkeypatch, regs):
 
 @pytest.mark.parametrize("variant", [{}, {"VQB_JIT_DIAGRUN": "0"}, {"VQB_JIT_ACC": "1000"},
                                      {"VQB_JIT_LAZY": "0"}, {"VQB_PARALLEL_ADJOINT": "0"},
-                                     {"VQB_STABLE_LAYOUT": "1"}, {"VQB_JIT_ACCBATCH": "1"},
-                                     {"VQB_JIT_GDIFF": "0", "VQB_JIT_STASH": "1"},
+                                     {"VQB_JIT_GDIFF": "0"}, {"VQB_JIT_FACTOR": "0"},
                                      {"VQB_JIT_REDLANES": "1"}, {"VQB_JIT_REDLANES": "8"},
                                      {"VQB_JIT_DIRECT": "0"}])
 def test_structure_classes_and_generator_variants(dev, ref, monkeypatch, variant):
@@ -293,9 +292,8 @@ def test_structure_classes_and_generator_variants(dev, ref, monkeypatch, variant
     (Rx(pi): zero real parts; Ry(pi): a zero diagonal; Rz(0): the identity)
     must compile their own kernels and still match the reference, forward and
     adjoint, in every generator variant (diagonal runs off, no accumulator
-    budget, eager relayouts, serial host planning, stable layouts with shuffle
-    relayouts, batched slot reductions, no derivative generators with parked
-    states)."""
+    budget, eager relayouts, serial host planning, no derivative generators,
+    no scalar factoring or cost-model fusion, partial-lane reductions)."""
     monkeypatch.setenv("VQB_JIT", "1")
     for k, v in variant.items():
         monkeypatch.setenv(k, v)
