@@ -146,6 +146,14 @@ cplx best_scale(const cplx *sub, int nt, int nc, double *cost) {
     return bs;
 }
 
+double op_cost(const FusedOp &f) {
+    if (f.cost < 0) {
+        if (!f.fusable) f.cost = 1e30;
+        else best_scale(f.sub_phi.data(), f.nt, f.nc, &f.cost);
+    }
+    return f.cost;
+}
+
 FusedOp analyse_gate(const Gate &g) {
     FusedOp f = analyse(g.pos, g.m, {&g.mat});
     f.gate = g;
@@ -219,6 +227,7 @@ struct Block {
     bool frozen = false; // parametric or too wide: never merged into
     int src = -1;        // original op index (frozen, or a single unmerged op)
     bool merged = false;
+    double cost = -1;    // merged blocks: op_cost of the product (cost model)
 };
 
 } // namespace
@@ -316,6 +325,7 @@ std::vector<const FusedOp *> fuse_blocks_ref(const std::vector<FusedOp> &ops, co
             embed_mul(pair ? f.rev->psi_op.mat.data() : g.mat.data(), P, np, U, nu, acc_psi, tmp);
             std::copy(tmp, tmp + du * du, acc_psi);
         }
+        double merged_cost = -1;
         if (cost_model && !any_pair) {
             // merge only if the specialised kernel's cost does not grow
             auto block_cost = [&](const cplx *M, const int *Ub, int nub) {
@@ -329,17 +339,13 @@ std::vector<const FusedOp *> fuse_blocks_ref(const std::vector<FusedOp> &ops, co
                 best_scale(a.sub_phi.data(), a.nt, a.nc, &c);
                 return c;
             };
-            double parts = 0;
+            double parts = op_cost(f);
             for (int k = 0; k < nc; ++k) {
                 const Block &b = blocks[cands[k]];
-                parts += block_cost(src_mat(b, false), b.U, b.nu);
+                parts += b.merged ? b.cost : op_cost(ops[b.src]);
             }
-            {
-                double c = 0;
-                best_scale(f.sub_phi.data(), f.nt, f.nc, &c);
-                parts += c;
-            }
-            if (block_cost(acc_phi, U, nu) > parts + 1e-9) {
+            merged_cost = block_cost(acc_phi, U, nu);
+            if (merged_cost > parts + 1e-9) {
                 fresh(false);
                 continue;
             }
@@ -354,6 +360,7 @@ std::vector<const FusedOp *> fuse_blocks_ref(const std::vector<FusedOp> &ops, co
         kb.pair = any_pair;
         if (any_pair) std::copy(acc_psi, acc_psi + du * du, kb.psi);
         kb.merged = true;
+        kb.cost = merged_cost;
         for (int i = 0; i < nu; ++i) last[U[i]] = keep;
     }
     std::vector<const FusedOp *> out;

@@ -38,6 +38,7 @@ struct FusedOp {
     bool fusable = true;
     Gate gate;               // original (fallback path)
     const RevOp *rev = nullptr;
+    mutable double cost = -1; // op_cost cache (-1: not computed)
 };
 
 struct Stage {
@@ -81,6 +82,8 @@ double subs_cost(const cplx *sub, int nt, int nc);
 // cost in *cost. Dividing every sub-matrix by s is exact for the entries
 // equal to s (they become exactly 1).
 cplx best_scale(const cplx *sub, int nt, int nc, double *cost);
+// subs_cost after best_scale of an analysed op's matrices (cached in f.cost)
+double op_cost(const FusedOp &f);
 // sub / s entry by entry (textbook complex division, so x / x == 1 exactly)
 void divide_by(cplx *sub, size_t count, const cplx &s);
 

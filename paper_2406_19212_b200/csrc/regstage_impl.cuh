@@ -2546,7 +2546,12 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
     // structure-aware kernels: merge blocks only where the emitted cost does
     // not grow, factor scalars out of the forward matrices (VQB_JIT_FACTOR=0:
     // merge whenever possible, no factoring)
-    const bool factor_on = use_jit && env_int("VQB_JIT_FACTOR", 1) != 0;
+    // (auto: states of >= 2^22 amplitudes, where the planning cost -- about
+    // 0.5 us per operation -- hides behind the kernels; config 0's 2^20
+    // amplitudes are host-bound and measured faster without: 491 vs 414
+    // evals/s. VQB_JIT_FACTOR=1 / 0 forces it on / off.)
+    const int factor_env = env_int("VQB_JIT_FACTOR", -1);
+    const bool factor_on = use_jit && (factor_env < 0 ? pn >= 22 : factor_env != 0);
     const bool cost_fusion = factor_on && !REV;
     bool batching = false;
     std::vector<Action> pending;

@@ -283,7 +283,8 @@ def test_specialised_adjoint_matches_reference(dev, ref, monkeypatch, regs):
 
 @pytest.mark.parametrize("variant", [{}, {"VQB_JIT_DIAGRUN": "0"}, {"VQB_JIT_ACC": "1000"},
                                      {"VQB_JIT_LAZY": "0"}, {"VQB_PARALLEL_ADJOINT": "0"},
-                                     {"VQB_JIT_GDIFF": "0"}, {"VQB_JIT_FACTOR": "0"},
+                                     {"VQB_JIT_GDIFF": "0"}, {"VQB_JIT_FACTOR": "1"},
+                                     {"VQB_JIT_FACTOR": "1", "VQB_JIT_GDIFF": "0"},
                                      {"VQB_JIT_REDLANES": "1"}, {"VQB_JIT_REDLANES": "8"},
                                      {"VQB_JIT_DIRECT": "0"}])
 def test_structure_classes_and_generator_variants(dev, ref, monkeypatch, variant):
@@ -293,7 +294,8 @@ def test_structure_classes_and_generator_variants(dev, ref, monkeypatch, variant
     must compile their own kernels and still match the reference, forward and
     adjoint, in every generator variant (diagonal runs off, no accumulator
     budget, eager relayouts, serial host planning, no derivative generators,
-    no scalar factoring or cost-model fusion, partial-lane reductions)."""
+    scalar factoring and cost-model fusion forced on at this size (they
+    switch on by themselves at >= 2^22 amplitudes), partial-lane reductions)."""
     monkeypatch.setenv("VQB_JIT", "1")
     for k, v in variant.items():
         monkeypatch.setenv(k, v)
