@@ -509,6 +509,9 @@ def roofline_of(eng, wl, prof, launch_recs, step_flops, world):
         t_meas = sum(r[1] for r in launch_recs) / 1e3
         t_floor = sum(max(r[3] / (peak * 1e9), r[2] / (dfma * 1e12)) for r in launch_recs)
         n_hbm = sum(1 for r in launch_recs if r[3] / (peak * 1e9) >= r[2] / (dfma * 1e12))
+        pn = (2 * wl.n if wl.mixed else wl.n) - wl.g
+        roof["per_launch"] = [[round(r[1], 4), round(r[2] / float(1 << pn), 1)] for r in launch_recs]
+        roof["per_launch_what"] = "[ms, executed FP64 flops per amplitude] of every stage launch of one step"
         roof["per_launch_bound"] = {
             "frac": t_floor / t_meas if t_meas else None, "floor_ms": 1e3 * t_floor,
             "measured_ms": 1e3 * t_meas, "launches": len(launch_recs), "hbm_bound_launches": n_hbm,
