@@ -32,6 +32,12 @@ __device__ __forceinline__ int swz(int l) {
     return l ^ ((l >> 3) & 7) ^ ((l >> 6) & 7) ^ ((l >> 9) & 7);
 }
 
+// index check of the VQB_JIT_CHECK instrumentation: traps when i >= n
+__device__ __forceinline__ u64 chk_idx(u64 i, u64 n) {
+    if (i >= n) __trap();
+    return i;
+}
+
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));

@@ -103,14 +103,21 @@ double subs_cost(const cplx *sub, int nt, int nc) {
                 }
         if (ident) continue;
         for (int r = 0; r < D; ++r) {
-            bool first = true;
+            // emission order: a unit entry first (a copy), then the rest
+            bool unit = false, any = false;
+            double row = 0;
             for (int col = 0; col < D; ++col) {
                 const int k = entry_class(M[r + col * D]);
                 if (k == 0) continue;
-                if (first) total += (k >= 4 ? 0 : (k == 3 ? 4 : 2));
-                else total += (k == 3 ? 4 : 2);
-                first = false;
+                any = true;
+                unit |= k >= 4;
+                row += k == 3 ? 4 : 2;
             }
+            if (!any) continue;
+            // the unit term is the row's free first term; any other first term
+            // multiplies instead of accumulating at the same instruction count
+            if (unit) row -= 2;
+            total += row;
         }
     }
     return total / double(D << nc);

@@ -74,9 +74,9 @@ std::vector<const FusedOp *> fuse_blocks_ref(const std::vector<FusedOp> &ops, co
 // 5 exactly -1, 6 exactly +i, 7 exactly -i.
 int entry_class(const cplx &v);
 // FP64 instructions per amplitude of an op's register code: per output row
-// the first nonzero term costs 0 (unit), 2 (real/imaginary) or 4 (complex)
-// instructions, every further term 2 (unit, real, imaginary) or 4; identity
-// sub-matrices cost nothing. Averaged over rows and condition values.
+// a unit entry is emitted first and costs nothing (a copy), every other term
+// 2 (unit, real, imaginary) or 4 (complex); identity sub-matrices cost
+// nothing. Averaged over rows and condition values.
 double subs_cost(const cplx *sub, int nt, int nc);
 // The scalar s (a nonzero entry, or 1) minimising subs_cost(sub / s); its
 // cost in *cost. Dividing every sub-matrix by s is exact for the entries

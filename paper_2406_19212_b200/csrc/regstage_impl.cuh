@@ -1288,6 +1288,19 @@ std::string cterm(const std::string &m, const std::string &x, const std::string 
 
 // v[idx[r]] <- sum_s M[r + s D] v[idx[s]] for one group; M entry k is the
 // expression mat(k) of class cls(k)
+// a row's terms in emission order: a unit entry first (as the first term it
+// is a plain copy), then the others in column order
+template <typename ClsF> void term_order(int r, int D, ClsF cls, int *order) {
+    int n = 0;
+    for (int s = 0; s < D; ++s)
+        if (cls(r + s * D) >= 4) {
+            order[n++] = s;
+            break;
+        }
+    for (int s = 0; s < D; ++s)
+        if (n == 0 || order[0] != s) order[n++] = s;
+}
+
 template <typename MatF, typename ClsF>
 std::string mv_code(const std::string &v, const int *idx, int D, MatF mat, ClsF cls, double &fl) {
     std::string e = "      {\n";
@@ -1296,7 +1309,10 @@ std::string mv_code(const std::string &v, const int *idx, int D, MatF mat, ClsF 
     for (int r = 0; r < D; ++r) {
         e += "        double2 o" + std::to_string(r) + ";\n";
         bool first = true;
-        for (int s = 0; s < D; ++s) {
+        int order[16];
+        term_order(r, D, cls, order);
+        for (int oi = 0; oi < D; ++oi) {
+            const int s = order[oi];
             const int c = cls(r + s * D);
             if (!c) continue;
             e += cterm(mat(r + s * D), "x" + std::to_string(s), "o" + std::to_string(r), c, first, fl);
@@ -1317,7 +1333,10 @@ std::string dot_code(const std::string &acc, const int *idx, int D, MatF mat, Cl
     for (int r = 0; r < D; ++r) {
         std::string row;
         bool first = true;
-        for (int s = 0; s < D; ++s) {
+        int order[16];
+        term_order(r, D, cls, order);
+        for (int oi = 0; oi < D; ++oi) {
+            const int s = order[oi];
             const int c = cls(r + s * D);
             if (!c) continue;
             row += cterm(mat(r + s * D), "vf[" + std::to_string(idx[s]) + "]", "y", c, first, fl);
@@ -1953,6 +1972,62 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
 }
 
 
+// VQB_JIT_CHECK=1 (debugging aid, stands in for compute-sanitizer, which
+// this pool does not allow): every global index of the generated kernel is
+// checked against the state size (2^pn amplitudes) and every shared-memory
+// tile / pool index against its array, trapping on a violation (the call
+// then fails with a CUDA error). Applied to the finished source text.
+std::string instrument_checks(const std::string &src, int pn, int tile, int npool) {
+    if (env_int("VQB_JIT_CHECK", 0) == 0) return src;
+    std::string out;
+    out.reserve(src.size() * 2);
+    const std::string pre = "#define VQB_GCHK(x) vqbjit::chk_idx((u64)(x), " + std::to_string(1ull << pn) +
+                            "ull)\n#define VQB_SCHK(x) ((int)vqbjit::chk_idx((u64)(x), " + std::to_string(tile) +
+                            "ull))\n#define VQB_PCHK(x) ((int)vqbjit::chk_idx((u64)(x), " + std::to_string(npool) +
+                            "ull))\n";
+    size_t i = 0;
+    const size_t inc = src.find("using namespace vqbjit;");
+    auto wrap_at = [&](size_t pos, size_t open, const char *mac) {
+        // copy through `open` ('['), wrap the balanced index expression
+        out.append(src, i, open + 1 - i);
+        int depth = 1;
+        size_t j = open + 1;
+        while (j < src.size() && depth > 0) {
+            if (src[j] == '[') ++depth;
+            else if (src[j] == ']') --depth;
+            ++j;
+        }
+        out += std::string(mac) + "(" + src.substr(open + 1, j - 1 - (open + 1)) + ")]";
+        i = j;
+        (void)pos;
+    };
+    while (i < src.size()) {
+        size_t best = std::string::npos, open = 0;
+        const char *mac = nullptr;
+        for (const auto &pm : {std::make_pair("a[", "VQB_GCHK"), std::make_pair("b2[", "VQB_GCHK"),
+                               std::make_pair("xbuf[", "VQB_SCHK"), std::make_pair("xbuf2[", "VQB_SCHK"),
+                               std::make_pair("spool[", "VQB_PCHK")}) {
+            size_t p = src.find(pm.first, i);
+            // whole identifiers only
+            while (p != std::string::npos && p > 0 && (std::isalnum((unsigned char)src[p - 1]) || src[p - 1] == '_'))
+                p = src.find(pm.first, p + 1);
+            if (p != std::string::npos && p < best) {
+                best = p;
+                open = p + std::strlen(pm.first) - 1;
+                mac = pm.second;
+            }
+        }
+        if (best == std::string::npos) break;
+        wrap_at(best, open, mac);
+    }
+    out.append(src, i, std::string::npos);
+    if (inc != std::string::npos) {
+        const size_t at = out.find("using namespace vqbjit;");
+        out.insert(at + std::strlen("using namespace vqbjit;") + 1, pre);
+    }
+    return out;
+}
+
 // Source of a specialised adjoint stage kernel (the REV mode of k_regstage on
 // one lowered program): Phi and Psi tiles in registers, one tile per block,
 // each parametric step's contributions reduced per warp into shared memory and
@@ -2462,7 +2537,7 @@ std::string shape_key(const RParams &P, bool rev) {
             cls[(size_t)i >> 1] = (char)(cls[(size_t)i >> 1] | (pool_ucls(P, (unsigned)i, 1, 0) << (4 * (i & 1))));
         key += cls;
     }
-    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_WIDE_REGS", "VQB_JIT_GDIFF", "VQB_JIT_SHUFFLE", "VQB_JIT_REDLANES", "VQB_JIT_DIRECT", "VQB_JIT_FACTOR"}) {
+    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_WIDE_REGS", "VQB_JIT_GDIFF", "VQB_JIT_SHUFFLE", "VQB_JIT_REDLANES", "VQB_JIT_DIRECT", "VQB_JIT_FACTOR", "VQB_JIT_CHECK"}) {
         const char *v = std::getenv(e);
         key += '|';
         if (v) key += v;
@@ -2712,6 +2787,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             double fpa = 0;
             int xt = 1;
             std::string src = REV ? jit_reverse_source(*act.P, &sp, &fpa, &xt) : jit_forward_source(*act.P, &sp, &pb, &fpa);
+            if (!src.empty()) src = instrument_checks(src, pn, TS, std::max(act.P->npool, 1));
             if (src.empty()) {
                 // not specialisable: remember that (no kernel), stay on the interpreter
                 std::lock_guard<std::mutex> lk(g_shape_mu);

@@ -91,3 +91,30 @@ def test_second_device_gradient(dev, ref):
         assert abs(loss - rl) <= 1e-10 and rel_err(g, rg) <= 1e-10
     finally:
         torch.cuda.set_device(0)
+
+
+@pytest.mark.parametrize("variant", [{}, {"VQB_JIT_FACTOR": "1"}, {"VQB_REV_REGS": "16"}])
+def test_bounds_checked_kernels(dev, ref, monkeypatch, variant):
+    """VQB_JIT_CHECK=1 compiles every specialised kernel with bounds checks on
+    each global, shared-memory-tile and matrix-pool index (a violation traps
+    and the call fails); with them on, forward, adjoint and density-matrix
+    programs still match the reference. (compute-sanitizer is not allowed on
+    this pool; this is the library's own check.)"""
+    monkeypatch.setenv("VQB_JIT", "1")
+    monkeypatch.setenv("VQB_JIT_CHECK", "1")
+    for k, v in variant.items():
+        monkeypatch.setenv(k, v)
+    w = circuits.config1(rows=3, cols=5, cycles=8)
+    s = dev.pure_state(15)
+    dev.apply_circuit(w.circuit, s)
+    r = ref.pure_state(15)
+    ref.apply_circuit(w.circuit, r)
+    assert np.max(np.abs(dev.download(s) - ref.download(r))) <= 1e-12
+    for q in (circuits.config2(n=14, p=2), circuits.config0(n=13, layers=2)):
+        loss, g = dev.gradient_pure(q.observable, q.circuit, dev.pure_state(q.num_qubits))
+        rl, rg = ref.gradient_pure(q.observable, q.circuit, ref.pure_state(q.num_qubits))
+        assert abs(loss - rl) <= 1e-10 * max(1.0, abs(rl)) and rel_err(g, rg) <= 1e-10
+    d = circuits.config3(n=6, layers=2)
+    loss, g = dev.gradient_mixed(d.observable, d.circuit, dev.mixed_state(6))
+    rl, rg = ref.gradient_mixed(d.observable, d.circuit, ref.mixed_state(6))
+    assert abs(loss - rl) <= 1e-10 * max(1.0, abs(rl)) and rel_err(g, rg) <= 1e-10
