@@ -1565,6 +1565,25 @@ std::string jit_wide_regs(const RParams &P, const ROp &op, const char *v, unsign
     return e;
 }
 
+// One-tile-per-block kernels read run-time-indexed matrices (sub-matrices
+// selected by conditions on thread or global bits) straight from the
+// parameter bank: the constant cache serialises a warp's read only over the
+// distinct addresses (at most 2^k for k thread-bit conditions; one for
+// global-bit conditions, which are block-uniform), whereas copying the pool
+// into shared memory in every block cost a fifth of the QAOA adjoint's stall
+// samples (profiles/r2_ncu_qaoa_rev.txt). Kernels with a tile loop keep the
+// shared-memory copy (parameter-bank operands would be hoisted out of the
+// loop into registers and spill). VQB_JIT_PBANK=0 restores the copy.
+bool pool_reads_from_bank(std::string &body) {
+    if (env_int("VQB_JIT_PBANK", 1) == 0) return false;
+    auto replace_all = [&](const std::string &a, const std::string &b) {
+        for (size_t pos = 0; (pos = body.find(a, pos)) != std::string::npos; pos += b.size()) body.replace(pos, a.size(), b);
+    };
+    replace_all("spool[", "P.pool[");
+    replace_all("spool + ", "P.pool + ");
+    return true;
+}
+
 std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *per_block, double *flops);
 // Source of a kernel equivalent to k_regstage<false, false> on one lowered
 // stage program, with every structural quantity a literal: tile bits, layouts
@@ -1869,6 +1888,7 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
     // matrices are read from a shared-memory copy at constant offsets: loads
     // the compiler cannot hoist out of the tile loop (parameter-bank reads
     // would be hoisted into registers and spill)
+    if (spool && per_block_mode && !pool_smem && pool_reads_from_bank(body)) spool = false;
     spool = spool || pool_smem;
     if (spool)
         out(std::string("  double2 *spool = sm + ") + std::to_string(per_block_mode ? TS : 2 * TS) +
@@ -2416,6 +2436,7 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
     // shared memory: xbuf (relayouts, Phi's wide ops) [| xbuf2 (Psi's wide
     // ops)] [| pool copy] | gradient reduction slots
     const int xt = 2; // xbuf (Phi) and xbuf2 (Psi)
+    if (spool && pool_reads_from_bank(body)) spool = false; // one tile per block
     out("  extern __shared__ __align__(16) double2 sm[];\n  double2 *xbuf = sm;\n");
     out("  double2 *xbuf2 = sm + " + I(TS) + ";\n");
     const int red_at = xt * TS + (spool ? P.npool : 0);
@@ -2537,7 +2558,7 @@ std::string shape_key(const RParams &P, bool rev) {
             cls[(size_t)i >> 1] = (char)(cls[(size_t)i >> 1] | (pool_ucls(P, (unsigned)i, 1, 0) << (4 * (i & 1))));
         key += cls;
     }
-    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_WIDE_REGS", "VQB_JIT_GDIFF", "VQB_JIT_SHUFFLE", "VQB_JIT_REDLANES", "VQB_JIT_DIRECT", "VQB_JIT_FACTOR", "VQB_JIT_CHECK"}) {
+    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_WIDE_REGS", "VQB_JIT_GDIFF", "VQB_JIT_SHUFFLE", "VQB_JIT_REDLANES", "VQB_JIT_DIRECT", "VQB_JIT_FACTOR", "VQB_JIT_CHECK", "VQB_JIT_PBANK"}) {
         const char *v = std::getenv(e);
         key += '|';
         if (v) key += v;
