@@ -1352,6 +1352,159 @@ std::string dot_code(const std::string &acc, const int *idx, int D, MatF mat, Cl
     return e + "        " + acc + " += a;\n      }\n";
 }
 
+// Factored derivative contraction. The entries of a derivative matrix come in
+// few distinct values up to a unit factor: G_p = D_p inv of a rotation is
+// -i/2 times a Pauli matrix (one value), D_p of Rx is {-s/2, -i c/2}. With
+// the entries partitioned into classes {u_k * m_c} (u_k in {1, -1, i, -i}),
+//   Re <psi| D |phi> = sum_c Re(m_c * w_c),  w_c = sum_k u_k conj(psi_r) phi_s,
+// so each entry costs two FMAs per needed component of w_c (only Re w_c for a
+// real m_c, only Im w_c for an imaginary one) straight into a per-thread
+// accumulator, and the products with m_c are taken once per thread and step
+// instead of once per row. The partition is structure (part of the kernel
+// key, dot_signature); the values m_c stay launch parameters.
+struct DotPlan {
+    bool ok = false;
+    int nclass = 0;
+    int ref[4] = {0, 0, 0, 0};  // reference entry of each class
+    int need[4] = {0, 0, 0, 0}; // bit 0: Re w needed (m has a real part), bit 1: Im w
+    int cls_of[16];             // class of entry k, -1: zero
+    int unit_of[16];            // u_k: 0: 1, 1: -1, 2: i, 3: -i
+};
+// u with v == u * r exactly, or -1
+int unit_ratio(double2 v, double2 r) {
+    if (v.x == r.x && v.y == r.y) return 0;
+    if (v.x == -r.x && v.y == -r.y) return 1;
+    if (v.x == -r.y && v.y == r.x) return 2;
+    if (v.x == r.y && v.y == -r.x) return 3;
+    return -1;
+}
+// plan over the sub-matrices `sel` (pool offset off, dd entries each) one
+// thread may select at run time
+DotPlan dot_plan(const RParams &P, unsigned off, int dd, const std::vector<int> &sel) {
+    DotPlan pl;
+    if (dd > 16) return pl;
+    auto val = [&](int cc, int k) { return P.pool[off + (unsigned)(cc * dd + k)]; };
+    auto nz = [](double2 v) { return v.x != 0.0 || v.y != 0.0 || v.x != v.x || v.y != v.y; };
+    int first = -1;
+    for (int cc : sel) {
+        for (int k = 0; k < dd && first < 0; ++k)
+            if (nz(val(cc, k))) first = cc;
+        if (first >= 0) break;
+    }
+    if (first < 0) return pl;
+    for (int k = 0; k < dd; ++k) {
+        pl.cls_of[k] = -1;
+        pl.unit_of[k] = 0;
+        const double2 v = val(first, k);
+        if (v.x != v.x || v.y != v.y) return pl;
+        if (!nz(v)) continue;
+        for (int c = 0; c < pl.nclass && pl.cls_of[k] < 0; ++c) {
+            const int u = unit_ratio(v, val(first, pl.ref[c]));
+            if (u >= 0) {
+                pl.cls_of[k] = c;
+                pl.unit_of[k] = u;
+            }
+        }
+        if (pl.cls_of[k] < 0) {
+            if (pl.nclass == 4) return pl;
+            pl.ref[pl.nclass] = k;
+            pl.cls_of[k] = pl.nclass++;
+        }
+    }
+    for (int cc : sel) {
+        bool any = false;
+        for (int k = 0; k < dd; ++k) any = any || nz(val(cc, k));
+        if (!any) continue; // a zero sub-matrix contributes m_c = 0
+        for (int k = 0; k < dd; ++k) {
+            const double2 v = val(cc, k);
+            if (pl.cls_of[k] < 0) {
+                if (nz(v)) return pl;
+                continue;
+            }
+            if (unit_ratio(v, val(cc, pl.ref[pl.cls_of[k]])) != pl.unit_of[k]) return pl;
+        }
+        for (int c = 0; c < pl.nclass; ++c) {
+            const double2 m = val(cc, pl.ref[c]);
+            if (m.x != 0.0) pl.need[c] |= 1;
+            if (m.y != 0.0) pl.need[c] |= 2;
+        }
+    }
+    pl.ok = true;
+    return pl;
+}
+std::string dot_plan_sig(const DotPlan &pl, int dd) {
+    if (!pl.ok) return "-";
+    std::string s;
+    for (int k = 0; k < dd; ++k) s += (char)('a' + (pl.cls_of[k] < 0 ? 0 : 1 + pl.cls_of[k] * 4 + pl.unit_of[k]));
+    for (int c = 0; c < pl.nclass; ++c) s += (char)('0' + pl.need[c]);
+    return s;
+}
+// sub-matrices selectable by a thread whose register-bit conditions are cs
+std::vector<int> dot_selectable(const ROp &op, int cs) {
+    int rmask = 0;
+    bool dynamic = false;
+    for (int q = 0; q < op.nc; ++q) {
+        if (op.ck[q] == 2) rmask |= 1 << q;
+        else dynamic = true;
+    }
+    std::vector<int> sel;
+    for (int cc = 0; cc < (1 << op.nc); ++cc)
+        if (dynamic ? (cc & rmask) == cs : cc == cs) sel.push_back(cc);
+    return sel;
+}
+// every plan a parametric 0..2-bit step's code depends on (kernel key)
+std::string dot_signature(const RParams &P, const ROp &op) {
+    if (op.np <= 0 || op.nt >= 3) return "";
+    const int dd = 1 << (2 * op.nt), nsub = 1 << op.nc;
+    int rmask = 0;
+    for (int q = 0; q < op.nc; ++q)
+        if (op.ck[q] == 2) rmask |= 1 << q;
+    std::string s;
+    for (int p = 0; p < op.np; ++p)
+        for (int cs = 0; cs < nsub; ++cs) {
+            if (cs & ~rmask) continue;
+            s += dot_plan_sig(dot_plan(P, op.mat_d + (unsigned)(p * nsub * dd), dd, dot_selectable(op, cs)), dd);
+            s += ';';
+        }
+    return s;
+}
+// one group's terms: w_c (+)= u_k conj(vg[idx[r]]) vf[idx[s]], needed components only
+std::string dot_plan_group(const DotPlan &pl, const std::string &wname, const int *idx, int D, double &fl) {
+    std::string e;
+    for (int s = 0; s < D; ++s)
+        for (int r = 0; r < D; ++r) {
+            const int k = r + s * D, c = pl.cls_of[k];
+            if (c < 0) continue;
+            const std::string g = "vg[" + std::to_string(idx[r]) + "]", f = "vf[" + std::to_string(idx[s]) + "]";
+            const std::string wr = wname + "r" + std::to_string(c), wi = wname + "i" + std::to_string(c);
+            // q = conj(g) f: qr = g.x f.x + g.y f.y, qi = g.x f.y - g.y f.x
+            auto add_qr = [&](const std::string &w, bool neg) {
+                const std::string sg = neg ? "-" : "";
+                e += "        " + w + " = fma(" + sg + g + ".x, " + f + ".x, fma(" + sg + g + ".y, " + f + ".y, " + w + "));\n";
+                fl += 4;
+            };
+            auto add_qi = [&](const std::string &w, bool neg) {
+                const std::string sa = neg ? "-" : "", sb = neg ? "" : "-";
+                e += "        " + w + " = fma(" + sa + g + ".x, " + f + ".y, fma(" + sb + g + ".y, " + f + ".x, " + w + "));\n";
+                fl += 4;
+            };
+            const int u = pl.unit_of[k];
+            if (pl.need[c] & 1) { // Re(u q)
+                if (u == 0) add_qr(wr, false);
+                else if (u == 1) add_qr(wr, true);
+                else if (u == 2) add_qi(wr, true);
+                else add_qi(wr, false);
+            }
+            if (pl.need[c] & 2) { // Im(u q)
+                if (u == 0) add_qi(wi, false);
+                else if (u == 1) add_qi(wi, true);
+                else if (u == 2) add_qr(wi, false);
+                else add_qr(wi, true);
+            }
+        }
+    return e;
+}
+
 // register indices of the matrix rows of group i (Pos<NT, P0, P1>::off)
 void group_idx(int nt, int code, int i, int *idx) {
     static const int p0[6] = {0, 0, 0, 1, 1, 2}, p1[6] = {1, 2, 3, 2, 3, 3};
@@ -1669,6 +1822,7 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
         cur_sub = sub;
     };
     const bool lazy = env_int("VQB_JIT_LAZY", 1) != 0;
+    const bool dotplan_on = env_int("VQB_JIT_DOTPLAN", 1) != 0;
     for (int sub = 0; sub < P.nsubs; ++sub) {
         const RSub &sb = P.subs[sub];
         if (!lazy) to_regs(sub);
@@ -2094,17 +2248,60 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
     // measured: 6 for 8-register sweeps, 3 for the register-heavy 16-register ones
     const int acc_budget = env_int("VQB_JIT_ACC", R >= 16 ? 3 : 6);
     std::vector<int> open_slots;
+    // Batches of 4 (2) pending slots share their shuffles: at the first two
+    // (one) levels each lane keeps half of the batch and sends the other half
+    // to its partner, so after them every lane holds one slot's partial and
+    // the remaining levels reduce that one value: 4 (5) double shuffles per
+    // 4 slots instead of 12 (16). Lane l ends with the slot selected by its
+    // top lane bits; the lanes whose middle bits are zero store.
+    const int red_batch = env_int("VQB_JIT_REDBATCH", 4);
     auto flush_slots = [&](int keep) {
         while ((int)open_slots.size() > keep) {
-            const int sl = open_slots.front();
-            open_slots.erase(open_slots.begin());
-            // reduce over the lane bits above log2(PL) only; PL lanes per warp
-            // store partial sums (fewer dependent shuffles per slot)
-            std::string e = "    { double x = acc_s" + I(sl) + ";";
-            for (int sh = 16; sh >= red_lanes; sh >>= 1)
-                e += " x += __shfl_xor_sync(0xffffffffu, x, " + I(sh) + ");";
-            e += " if (lane < " + I(red_lanes) + ") red[" + I(sl * NW * red_lanes) + " + warp * " + I(red_lanes) +
-                 " + lane] = x; }\n";
+            const int avail = (int)open_slots.size();
+            const int B = (red_batch >= 4 && avail >= 4 && red_lanes <= 4) ? 4
+                          : (red_batch >= 2 && avail >= 2 && red_lanes <= 8) ? 2 : 1;
+            std::vector<int> sl(open_slots.begin(), open_slots.begin() + B);
+            open_slots.erase(open_slots.begin(), open_slots.begin() + B);
+            if (B == 1) {
+                // reduce over the lane bits above log2(PL) only; PL lanes per warp
+                // store partial sums (fewer dependent shuffles per slot)
+                std::string e = "    { double x = acc_s" + I(sl[0]) + ";";
+                for (int sh = 16; sh >= red_lanes; sh >>= 1)
+                    e += " x += __shfl_xor_sync(0xffffffffu, x, " + I(sh) + ");";
+                e += " if (lane < " + I(red_lanes) + ") red[" + I(sl[0] * NW * red_lanes) + " + warp * " + I(red_lanes) +
+                     " + lane] = x; }\n";
+                emit(e);
+                continue;
+            }
+            std::string e = "    {\n      const bool h4 = (lane & 16) != 0, h3 = (lane & 8) != 0;\n";
+            auto xchg = [&](const std::string &dst, const std::string &lo, const std::string &hi, const char *flag,
+                            int sh) {
+                // the lane with `flag` keeps hi and sends lo, its partner the reverse
+                e += "      const double " + dst + " = (" + flag + " ? " + hi + " : " + lo +
+                     ") + __shfl_xor_sync(0xffffffffu, " + flag + " ? " + lo + " : " + hi + ", " + I(sh) + ");\n";
+            };
+            int sh = 16;
+            std::string slot_expr;
+            if (B == 4) {
+                xchg("b0", "acc_s" + I(sl[0]), "acc_s" + I(sl[2]), "h4", 16);
+                xchg("b1", "acc_s" + I(sl[1]), "acc_s" + I(sl[3]), "h4", 16);
+                xchg("c0", "b0", "b1", "h3", 8);
+                e += "      double x = c0;\n";
+                slot_expr = "(h4 ? (h3 ? " + I(sl[3]) + " : " + I(sl[2]) + ") : (h3 ? " + I(sl[1]) + " : " + I(sl[0]) + "))";
+                sh = 4;
+            } else {
+                xchg("c0", "acc_s" + I(sl[0]), "acc_s" + I(sl[1]), "h4", 16);
+                e += "      double x = c0;\n";
+                slot_expr = "(h4 ? " + I(sl[1]) + " : " + I(sl[0]) + ")";
+                sh = 8;
+            }
+            int mid = 0;
+            for (; sh >= red_lanes; sh >>= 1) {
+                e += "      x += __shfl_xor_sync(0xffffffffu, x, " + I(sh) + ");\n";
+                mid |= sh;
+            }
+            e += "      if ((lane & " + I(mid) + ") == 0) red[" + slot_expr + " * " + I(NW * red_lanes) + " + warp * " +
+                 I(red_lanes) + " + (lane & " + I(red_lanes - 1) + ")] = x;\n    }\n";
             emit(e);
         }
     };
@@ -2149,12 +2346,25 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
         cur_sub = sub;
     };
     const bool lazy = env_int("VQB_JIT_LAZY", 1) != 0;
+    const bool dotplan_on = env_int("VQB_JIT_DOTPLAN", 1) != 0;
     for (int sub = 0; sub < P.nsubs; ++sub) {
         const RSub &sb = P.subs[sub];
         if (!lazy) to_regs(sub);
         for (int k = 0; k < sb.op_count; ++k) {
             if (P.ops[sb.op_begin + k].nt < 3 || P.ops[sb.op_begin + k].inreg) to_regs(sub);
             const ROp &op = P.ops[sb.op_begin + k];
+            // development aid: FP64 flops per thread each op's code adds
+            struct CostNote {
+                const ROp &o;
+                const double &f, &w;
+                double f0, w0;
+                int sub;
+                ~CostNote() {
+                    if (env_int("VQB_JIT_OPCOST", 0))
+                        std::fprintf(stderr, "[opcost] sub %d nt %d nc %d np %d pair %d inreg %d unit %d: %.0f flops/thread %.0f/tile\n",
+                                     sub, o.nt, o.nc, o.np, o.pair, o.inreg, o.unit, f - f0, w - w0);
+                }
+            } cost_note{op, fl, wfl, fl, wfl, sub};
             // a run of unit-modulus diagonal steps: conj(psi) phi is invariant
             // along it, so every contribution is Re(z e_p) with z taken once,
             // and both states get the product of the phases at the end
@@ -2403,6 +2613,27 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
                 // per-slot accumulators live to the end of the tile; their warp
                 // reductions are issued together there (independent shuffle
                 // chains overlap instead of stalling each parametric step)
+                // factored contraction (DotPlan) per (parameter, register
+                // condition): unit-weighted sums w_c over the thread's groups,
+                // multiplied by the class values once after the last group
+                std::map<std::pair<int, int>, DotPlan> plans;
+                if (dotplan_on)
+                    for (int i = 0; i < R; ++i) {
+                        if (i & mask) continue;
+                        const int cs = cstat(i);
+                        for (int p = 0; p < op.np; ++p) {
+                            if (plans.count({p, cs})) continue;
+                            const DotPlan pl =
+                                dot_plan(P, op.mat_d + (unsigned)(p * nsub * dd), dd, dot_selectable(op, cs));
+                            plans[{p, cs}] = pl;
+                            if (!pl.ok) continue;
+                            const std::string w = "w" + I(p) + "_" + I(cs) + "_";
+                            for (int c = 0; c < pl.nclass; ++c) {
+                                if (pl.need[c] & 1) emit("      double " + w + "r" + I(c) + " = 0.0;\n");
+                                if (pl.need[c] & 2) emit("      double " + w + "i" + I(c) + " = 0.0;\n");
+                            }
+                        }
+                    }
                 for (int i = 0; i < R; ++i) {
                     if (i & mask) continue;
                     const int cs = cstat(i);
@@ -2412,10 +2643,26 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
                     if (!gpre) emit(mv_code("vf", idx, D, mexpr(op.mat, cs), mcls(op.mat, cs), fl));
                     for (int p = 0; p < op.np; ++p) {
                         const unsigned dof = op.mat_d + (unsigned)(p * nsub * dd);
-                        emit(dot_code("acc_s" + I(op.slot + p), idx, D, mexpr(dof, cs), mcls(dof, cs), fl));
+                        auto it = plans.find({p, cs});
+                        if (it != plans.end() && it->second.ok)
+                            emit(dot_plan_group(it->second, "w" + I(p) + "_" + I(cs) + "_", idx, D, fl));
+                        else
+                            emit(dot_code("acc_s" + I(op.slot + p), idx, D, mexpr(dof, cs), mcls(dof, cs), fl));
                     }
                     if (gpre) emit(mv_code("vf", idx, D, mexpr(op.mat, cs), mcls(op.mat, cs), fl));
                     emit(mv_code("vg", idx, D, mexpr(op.mat, cs), mcls(op.mat, cs), fl));
+                }
+                for (const auto &kv : plans) {
+                    const DotPlan &pl = kv.second;
+                    if (!pl.ok) continue;
+                    const int p = kv.first.first, cs = kv.first.second;
+                    const unsigned dof = op.mat_d + (unsigned)(p * nsub * dd);
+                    const std::string w = "w" + I(p) + "_" + I(cs) + "_", acc = "acc_s" + I(op.slot + p);
+                    for (int c = 0; c < pl.nclass; ++c) {
+                        const std::string m = mexpr(dof, cs)(pl.ref[c]);
+                        if (pl.need[c] & 1) { emit("      " + acc + " = fma(" + m + ".x, " + w + "r" + I(c) + ", " + acc + ");\n"); fl += 2; }
+                        if (pl.need[c] & 2) { emit("      " + acc + " = fma(-" + m + ".y, " + w + "i" + I(c) + ", " + acc + ");\n"); fl += 2; }
+                    }
                 }
                 for (int p = 0; p < op.np; ++p) open_slots.push_back(op.slot + p);
             }
@@ -2558,7 +2805,10 @@ std::string shape_key(const RParams &P, bool rev) {
             cls[(size_t)i >> 1] = (char)(cls[(size_t)i >> 1] | (pool_ucls(P, (unsigned)i, 1, 0) << (4 * (i & 1))));
         key += cls;
     }
-    for (const char *e : {"VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_WIDE_REGS", "VQB_JIT_GDIFF", "VQB_JIT_SHUFFLE", "VQB_JIT_REDLANES", "VQB_JIT_DIRECT", "VQB_JIT_FACTOR", "VQB_JIT_CHECK", "VQB_JIT_PBANK"}) {
+    // partitions of the derivative matrices (DotPlan)
+    if (rev)
+        for (int i = 0; i < nops; ++i) key += dot_signature(P, P.ops[i]) + "/";
+    for (const char *e : {"VQB_JIT_DOTPLAN", "VQB_JIT_REDBATCH", "VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_WIDE_REGS", "VQB_JIT_GDIFF", "VQB_JIT_SHUFFLE", "VQB_JIT_REDLANES", "VQB_JIT_DIRECT", "VQB_JIT_FACTOR", "VQB_JIT_CHECK", "VQB_JIT_PBANK"}) {
         const char *v = std::getenv(e);
         key += '|';
         if (v) key += v;

@@ -1,0 +1,5 @@
+# full ncu captures of one heavy adjoint launch per gradient config (current generator)
+mkdir -p gpurun_out/s12
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:vqb_rev -s 34 -c 2 -o gpurun_out/s12/qaoa_rev python bench.py --config qaoa30 --no-extra --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/s12/ncu_qaoa.log 2>&1; echo "ncu qaoa rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:vqb_rev -s 40 -c 2 -o gpurun_out/s12/noisy_rev python bench.py --config noisy15 --no-extra --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/s12/ncu_noisy.log 2>&1; echo "ncu noisy rc=$?"
+ls -la gpurun_out/s12
