@@ -55,8 +55,22 @@ struct Error : std::runtime_error {
 
 [[noreturn]] inline void raise(int code, const std::string &msg) { throw Error(code, msg); }
 
+// Planning-only mode for development on a host without a GPU (VQB_DRYRUN=1):
+// CUDA runtime calls and kernel launches are skipped, so the host side --
+// reverse programs, stage planning, lowering, kernel generation and
+// VQB_JIT_DUMP -- runs to completion and can be inspected; every result read
+// back from the "device" is garbage. Never set in production.
+inline bool dry_run() {
+    static const bool on = [] {
+        const char *v = std::getenv("VQB_DRYRUN");
+        return v && *v == '1';
+    }();
+    return on;
+}
+
 #define VQB_CUDA(call)                                                                     \
     do {                                                                                   \
+        if (::vqb::dry_run()) break;                                                       \
         cudaError_t e_ = (call);                                                           \
         if (e_ != cudaSuccess)                                                             \
             ::vqb::raise(VQB_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \

@@ -156,6 +156,11 @@ int64_t compiles() { return g_compiles.load(); }
 
 std::vector<Kernel> get(const std::vector<std::string> &sources, const std::string &name) {
     std::vector<Kernel> out(sources.size());
+    if (dry_run()) { // planning only: no compilation, a placeholder handle
+        static Entry placeholder;
+        for (auto &k : out) k.e = &placeholder;
+        return out;
+    }
     std::vector<size_t> miss;
     {
         std::lock_guard<std::mutex> lk(g_mu);
@@ -208,6 +213,7 @@ std::vector<Kernel> get(const std::vector<std::string> &sources, const std::stri
 void launch(const Kernel &k, unsigned grid, unsigned block, size_t smem, cudaStream_t st,
             void **args) {
     Entry *e = static_cast<Entry *>(k.e);
+    if (dry_run()) return;
     {
         std::lock_guard<std::mutex> lk(g_mu);
         if (smem > e->max_smem) {
@@ -222,6 +228,7 @@ void launch(const Kernel &k, unsigned grid, unsigned block, size_t smem, cudaStr
 
 int blocks_per_sm(const Kernel &k, unsigned block, size_t smem) {
     Entry *e = static_cast<Entry *>(k.e);
+    if (dry_run()) return 4;
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = e->per_sm.find(smem);
     if (it != e->per_sm.end()) return it->second;

@@ -62,6 +62,7 @@ DevScope::~DevScope() {
 
 void *dev_alloc(size_t bytes, bool state, bool raise_on_fail) {
     void *p = nullptr;
+    if (dry_run()) return reinterpret_cast<void *>(uintptr_t(256)); // planning only: never dereferenced
     const cudaError_t e = cudaMalloc(&p, bytes);
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -75,7 +76,7 @@ void *dev_alloc(size_t bytes, bool state, bool raise_on_fail) {
 }
 
 void dev_free(void *p, size_t bytes, bool state) {
-    if (!p) return;
+    if (!p || dry_run()) return;
     cudaFree(p);
     g_live_bytes.fetch_sub(bytes);
     if (state) g_live_states.fetch_sub(1);

@@ -72,6 +72,7 @@ ProfMark prof_begin(cudaStream_t st) {
 void check_launch(const char *what, const ProfMark &m) {
     note_launch(1);
     const cudaError_t e = cudaGetLastError();
+    if (dry_run()) return;
     if (e != cudaSuccess) raise(VQB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
     if (m.slot >= 0) {
         std::lock_guard<std::mutex> lk(g_mu);

@@ -833,6 +833,62 @@ int env_int(const char *name, int dflt);
 // Lower as much of a stage's block list as fits one parameter block.
 // `remaining` (block indices, in a valid order) is consumed; what is left
 // must run in a following launch with the same tile bits.
+// Real scalar and rank-one form of one matrix of a channel step (D x D,
+// column-major): M = c (1 + e J_R) up to rounding with J_R the all-ones matrix
+// on the index set R (mask; |R| >= 2), or otherwise the real scalar that
+// leaves the cheapest M / c (best_scale); c = 1: leave M alone.
+struct PairForm {
+    double c = 1.0;
+    unsigned mask = 0;
+    double e = 0.0;
+};
+PairForm pair_form(const cvec &M, int nt) {
+    PairForm pf;
+    const int D = 1 << nt;
+    for (const cplx &v : M)
+        if (v.imag() != 0.0 || v != v) return pf;
+    auto at = [&](int r, int c) { return M[r + (size_t)c * D].real(); };
+    unsigned rmask = 0; // indices coupled to another one
+    for (int r = 0; r < D; ++r)
+        for (int c = 0; c < D; ++c)
+            if (r != c && at(r, c) != 0.0) rmask |= (1u << r) | (1u << c);
+    bool ok = true;
+    double c0 = 0, d = 0, e = 0;
+    bool have_c = false, have_d = false, have_e = false;
+    auto same = [](double x, double y) { return std::abs(x - y) <= 4e-16 * std::max(std::abs(x), std::abs(y)); };
+    for (int r = 0; r < D && ok; ++r) {
+        if (rmask >> r & 1) {
+            if (!have_d) d = at(r, r), have_d = true;
+            else ok = same(at(r, r), d);
+            for (int c = 0; c < D && ok; ++c) {
+                if (c == r || !(rmask >> c & 1)) continue;
+                if (!have_e) e = at(r, c), have_e = true;
+                else ok = same(at(r, c), e);
+            }
+        } else {
+            if (!have_c) c0 = at(r, r), have_c = true;
+            else ok = same(at(r, r), c0);
+        }
+    }
+    if (ok && rmask == 0 && have_c && c0 != 0.0) { // c * identity
+        pf.c = c0;
+        return pf;
+    }
+    if (ok && have_d && have_e && __builtin_popcount(rmask) >= 2) {
+        const double c = have_c ? c0 : d - e;
+        if (c != 0.0 && std::abs(d - e - c) <= 1e-14 * std::abs(c)) {
+            pf.c = c;
+            pf.mask = rmask;
+            pf.e = e / c;
+            return pf;
+        }
+    }
+    double cost = 0;
+    const cplx sc = best_scale(M.data(), nt, 0, &cost);
+    if (sc.imag() == 0.0 && sc.real() != 0.0) pf.c = sc.real();
+    return pf;
+}
+
 void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks,
                      std::vector<int> &remaining, int pn, bool rev, RParams &P, SlotMap &slots,
                      bool regwide = false, bool gdiff = false, bool factor = false) {
@@ -848,9 +904,18 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
     // contribution is taken before its update (derivative generator G_p),
     // and that contribution is rescaled by |c|^2 through its slot scale;
     // the launch ends with both states multiplied by c.
+    // Channel steps (pair ops: S^-1 on Phi, S^dag on Psi) are factored per
+    // state by real scalars ra (Phi) and rb (Psi): Phi runs as true / (c ra),
+    // Psi as true / (c rb), later contributions are rescaled by |c|^2 ra rb.
+    // A depolarizing superoperator and its inverse are c (1 + e J_R) with J_R
+    // the all-ones matrix on the basis states R with equal ket and bra bits:
+    // x_i += e * sum_R x for i in R, nothing else (rank_one below; flagged in
+    // ROp::unit bits 2 (Phi) and 3 (Psi), R in ROp::slot, e at ROp::mat_d /
+    // ROp::mat_e -- fields a non-parametric step does not otherwise use).
     cplx scale = 1.0;
+    double ra = 1.0, rb = 1.0;
     const int ops_cap = factor ? kMaxOps - 1 : kMaxOps;
-    const int pool_cap = factor ? kMaxPool - 1 : kMaxPool;
+    const int pool_cap = factor ? kMaxPool - 2 : kMaxPool;
     std::memset(&P, 0, sizeof P);
     for (int j = 0; j < K; ++j) P.bits[j] = sg.bits[j];
     P.ntiles = 1ull << (pn - K);
@@ -885,9 +950,10 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
     };
     auto pool_need = [&](const FusedOp &f) {
         if (f.nt >= 3) // XOR-term form: |X| * D entries per sub-matrix
-            return (count_x(f) * (1 << f.nt) << f.nc) * (1 + (f.pair ? 1 : 0));
+            return (count_x(f) * (1 << f.nt) << f.nc) * (1 + (f.pair ? 1 : 0)) + (f.pair ? 2 : 0);
         const int dd = (1 << (2 * f.nt)) << f.nc;
-        return dd * (1 + (f.pair ? 1 : 0) + (rev ? f.np : 0)) + (rev && f.nt == 0 ? f.np << f.nc : 0);
+        return dd * (1 + (f.pair ? 1 : 0) + (rev ? f.np : 0)) + (rev && f.nt == 0 ? f.np << f.nc : 0) +
+               (f.pair ? 2 : 0);
     };
     int nops = 0, npool = 0, nslots = 0;
     while (!remaining.empty()) {
@@ -1029,6 +1095,29 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
                 }
                 return off;
             };
+            // channel steps: per-state real scalars and the rank-one form
+            // (detected on the matrices in the op's final bit order)
+            cvec pair_phi, pair_psi;
+            const cvec *src_phi = &f.sub_phi, *src_psi = &f.sub_psi;
+            PairForm fa, fb;
+            if (factor && rev && f.pair && f.np == 0 && f.nc == 0 && f.nt >= 1 &&
+                (f.nt <= 2 || wide_in_regs(f)) && env_int("VQB_JIT_PAIRFACTOR", 1) != 0) {
+                fa = pair_form(f.nt > 1 ? permute_matrix(f.sub_phi, f.nt, order) : f.sub_phi, f.nt);
+                fb = pair_form(f.nt > 1 ? permute_matrix(f.sub_psi, f.nt, order) : f.sub_psi, f.nt);
+                pair_phi = f.sub_phi;
+                pair_psi = f.sub_psi;
+                if (fa.c != 1.0) divide_by(pair_phi.data(), pair_phi.size(), cplx(fa.c));
+                if (fb.c != 1.0) divide_by(pair_psi.data(), pair_psi.size(), cplx(fb.c));
+                ra *= fa.c;
+                rb *= fb.c;
+                src_phi = &pair_phi;
+                src_psi = &pair_psi;
+                if (fa.mask && fb.mask && fa.mask != fb.mask) fb.mask = 0;
+                if (env_int("VQB_JIT_RANKONE", 1) == 0) fa.mask = fb.mask = 0;
+                if (fa.mask) o.unit |= 4;
+                if (fb.mask) o.unit |= 8;
+                o.slot = (int)(fa.mask ? fa.mask : fb.mask);
+            }
             if (f.nt >= 3) {
                 // wide ops run in smem_op as sum_k diag(d_k) P_{x_k}: store the
                 // XOR patterns x_k and, per sub-matrix, d_k[r] = S[r, r ^ x_k]
@@ -1050,8 +1139,8 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
                         }
                     }
                 };
-                scan(f.sub_phi);
-                if (f.pair) scan(f.sub_psi);
+                scan(*src_phi);
+                if (f.pair) scan(*src_psi);
                 std::sort(X.begin(), X.end());
                 o.xoff = P.nxpat;
                 o.nx = (int)X.size();
@@ -1073,8 +1162,8 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
                     }
                     return off;
                 };
-                o.mat = pushx(f.sub_phi, &o.ident);
-                if (f.pair) o.mat_psi = pushx(f.sub_psi, &o.ident_psi);
+                o.mat = pushx(*src_phi, &o.ident);
+                if (f.pair) o.mat_psi = pushx(*src_psi, &o.ident_psi);
             } else if (factor && !f.pair && (!rev || f.np == 0 || use_g)) {
                 cvec sub = f.sub_phi;
                 double c = 0;
@@ -1086,8 +1175,15 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
                 }
                 o.mat = push(sub, 0, &o.ident);
             } else {
-                o.mat = push(f.sub_phi, 0, &o.ident);
-                if (f.pair) o.mat_psi = push(f.sub_psi, 0, &o.ident_psi);
+                o.mat = push(*src_phi, 0, &o.ident);
+                if (f.pair) o.mat_psi = push(*src_psi, 0, &o.ident_psi);
+            }
+            if (o.unit & (4 | 8)) {
+                // rank-one coefficients e (Phi at mat_d, Psi at mat_e)
+                o.mat_d = (unsigned)npool;
+                P.pool[npool++] = make_double2(fa.e, 0.0);
+                o.mat_e = (unsigned)npool;
+                P.pool[npool++] = make_double2(fb.e, 0.0);
             }
             if (rev && f.nt == 0 && !f.pair) {
                 o.unit = 1;
@@ -1109,7 +1205,7 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
                 o.ident = 0;
                 o.slot = nslots;
                 // contributions of the scaled states: <psi/c|G|phi/c> = |1/c|^2 <psi|G|phi>
-                const double corr = std::norm(scale_before);
+                const double corr = std::norm(scale_before) * ra * rb;
                 for (int p = 0; p < f.np; ++p) {
                     slots.scale.push_back(f.scale * corr);
                     slots.dst.push_back(f.grad_base + p);
@@ -1146,12 +1242,18 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
         sb.op_count = nops - sb.op_begin;
         remaining.swap(deferred);
     }
-    if (factor && scale != cplx(1) && P.nsubs > 0) {
+    if (factor && (scale != cplx(1) || ra != 1.0 || rb != 1.0) && P.nsubs > 0) {
         // the factored scalars, once per amplitude, in the last sub-stage
         ROp &o = P.ops[nops++];
         o.tab = o.tab_psi = -1;
         o.mat = (unsigned)npool;
-        P.pool[npool++] = make_double2(scale.real(), scale.imag());
+        const cplx sa = scale * ra, sb2 = scale * rb;
+        P.pool[npool++] = make_double2(sa.real(), sa.imag());
+        if (ra != rb) {
+            o.pair = 1;
+            o.mat_psi = (unsigned)npool;
+            P.pool[npool++] = make_double2(sb2.real(), sb2.imag());
+        }
         P.fast[nops - 1] = 0;
         ++P.subs[P.nsubs - 1].op_count;
     }
@@ -1503,6 +1605,23 @@ std::string dot_plan_group(const DotPlan &pl, const std::string &wname, const in
             }
         }
     return e;
+}
+
+// v[i] += e * sum_{j in R} v[j] for i in R (real e): the rank-one form of a
+// depolarizing superoperator (or its inverse) after its scalar is factored
+std::string rank_one_code(const std::string &v, const int *ridx, int nr, const std::string &e, double &fl) {
+    auto el = [&](int k) { return v + "[" + std::to_string(ridx[k]) + "]"; };
+    std::string c = "      {\n        double2 tsum = " + el(0) + ";\n";
+    for (int k = 1; k < nr; ++k) {
+        c += "        tsum.x += " + el(k) + ".x; tsum.y += " + el(k) + ".y;\n";
+        fl += 2;
+    }
+    for (int k = 0; k < nr; ++k) {
+        c += "        " + el(k) + ".x = fma(" + e + ".x, tsum.x, " + el(k) + ".x); " + el(k) + ".y = fma(" + e +
+             ".x, tsum.y, " + el(k) + ".y);\n";
+        fl += 4;
+    }
+    return c + "      }\n";
 }
 
 // register indices of the matrix rows of group i (Pos<NT, P0, P1>::off)
@@ -2527,9 +2646,31 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
                     spool = true;
                 }
                 auto pe = [&](unsigned off) { return "P.pool[" + I(off) + "]"; };
-                emit(jit_wide_regs(P, op, "vf", op.mat, op.ident, dyn, pe, fl));
-                emit(jit_wide_regs(P, op, "vg", op.pair ? op.mat_psi : op.mat, op.pair ? op.ident_psi : op.ident,
-                                   dyn, pe, fl));
+                for (int st2 = 0; st2 < 2; ++st2) {
+                    const char *v = st2 ? "vg" : "vf";
+                    if (dyn.empty() && op.pair && op.np == 0 && (op.unit & (st2 ? 8 : 4))) {
+                        if (((st2 ? op.ident_psi : op.ident) & 1)) continue;
+                        int rmask = 0;
+                        for (int q = 0; q < op.nt; ++q) rmask |= 1 << op.lb[q];
+                        for (int i0 = 0; i0 < R; ++i0) {
+                            if (i0 & rmask) continue;
+                            int ridx[16], nr = 0;
+                            for (int r = 0; r < (1 << op.nt); ++r) {
+                                if (!((op.slot >> r) & 1)) continue;
+                                int x = i0;
+                                for (int q = 0; q < op.nt; ++q)
+                                    if ((r >> q) & 1) x |= 1 << op.lb[q];
+                                ridx[nr++] = x;
+                            }
+                            emit(rank_one_code(v, ridx, nr, "P.pool[" + I(st2 ? op.mat_e : op.mat_d) + "]", fl));
+                        }
+                        continue;
+                    }
+                    if (st2 == 0) emit(jit_wide_regs(P, op, "vf", op.mat, op.ident, dyn, pe, fl));
+                    else
+                        emit(jit_wide_regs(P, op, "vg", op.pair ? op.mat_psi : op.mat,
+                                           op.pair ? op.ident_psi : op.ident, dyn, pe, fl));
+                }
                 continue;
             }
             if (op.nt >= 3) {
@@ -2599,12 +2740,20 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
                     const char *v = st2 ? "vg" : "vf";
                     const unsigned m = st2 ? mpsi : op.mat;
                     const unsigned long long id = st2 ? ipsi : op.ident;
+                    const bool r1 = !dynamic && op.pair && (op.unit & (st2 ? 8 : 4));
                     for (int i = 0; i < R; ++i) {
                         if (i & mask) continue;
                         const int cs = cstat(i);
                         int idx[4];
                         group_idx(op.nt, op.code, i, idx);
                         if (!dynamic && ((id >> cs) & 1)) continue;
+                        if (r1) {
+                            int ridx[16], nr = 0;
+                            for (int r = 0; r < D; ++r)
+                                if ((op.slot >> r) & 1) ridx[nr++] = idx[r];
+                            emit(rank_one_code(v, ridx, nr, "P.pool[" + I(st2 ? op.mat_e : op.mat_d) + "]", fl));
+                            continue;
+                        }
                         if (dynamic) emit("      if (!((" + num(id) + " >> (cd | " + I(cs) + ")) & 1))\n");
                         emit(mv_code(v, idx, D, mexpr(m, cs), mcls(m, cs), fl));
                     }
@@ -2808,7 +2957,7 @@ std::string shape_key(const RParams &P, bool rev) {
     // partitions of the derivative matrices (DotPlan)
     if (rev)
         for (int i = 0; i < nops; ++i) key += dot_signature(P, P.ops[i]) + "/";
-    for (const char *e : {"VQB_JIT_DOTPLAN", "VQB_JIT_REDBATCH", "VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_WIDE_REGS", "VQB_JIT_GDIFF", "VQB_JIT_SHUFFLE", "VQB_JIT_REDLANES", "VQB_JIT_DIRECT", "VQB_JIT_FACTOR", "VQB_JIT_CHECK", "VQB_JIT_PBANK"}) {
+    for (const char *e : {"VQB_JIT_DOTPLAN", "VQB_JIT_REDBATCH", "VQB_JIT_PAIRFACTOR", "VQB_JIT_RANKONE", "VQB_JIT_POOL", "VQB_JIT_BLOCKS", "VQB_JIT_MODE", "VQB_JIT_REV_BLOCKS", "VQB_JIT_DIAGRUN", "VQB_JIT_ACC", "VQB_JIT_WIDE2", "VQB_JIT_LAZY", "VQB_WIDE_REGS", "VQB_JIT_GDIFF", "VQB_JIT_SHUFFLE", "VQB_JIT_REDLANES", "VQB_JIT_DIRECT", "VQB_JIT_FACTOR", "VQB_JIT_CHECK", "VQB_JIT_PBANK"}) {
         const char *v = std::getenv(e);
         key += '|';
         if (v) key += v;
