@@ -333,6 +333,8 @@ GradientOut gradient_pure(const vqb_op *ops, int64_t count, const vqb_pauli_term
     DevBuf dbuf(gbytes + sizeof(double2));
     double *dgrads = dbuf.as<double>();
     double2 *dloss = reinterpret_cast<double2 *>(dbuf.as<char>() + gbytes);
+    // every writer accumulates (steps may share a gradient entry)
+    VQB_CUDA(cudaMemsetAsync(dgrads, 0, gbytes, phi->stream));
     auto sweep = [&] {
         HostTimer ht("gradient_pure reverse");
         std::vector<RevOp> rprog;
@@ -421,6 +423,8 @@ GradientOut gradient_mixed(const vqb_op *ops, int64_t count, const vqb_pauli_ter
     DevBuf dbuf(gbytes + sizeof(double2));
     double *dgrads = dbuf.as<double>();
     double2 *dloss = reinterpret_cast<double2 *>(dbuf.as<char>() + gbytes);
+    // every writer accumulates: the ket and bra halves of a gate share its entries
+    VQB_CUDA(cudaMemsetAsync(dgrads, 0, gbytes, phi->stream));
     auto sweep = [&] {
         run_reverse(phi, psi, mixed_reverse_program(es, n, base, chan_inv, chan_adj), dgrads, fused);
     };

@@ -109,6 +109,43 @@ std::vector<RevOp> mixed_reverse_program(const std::vector<Element> &es, int n,
             prog.push_back(std::move(bra));
             continue;
         }
+        // The superoperator conj(U) (x) U is the product of its ket half and its
+        // bra half, which act on different bits: the step splits into two, each
+        // with the derivative of its own factor, both adding into the gate's
+        // gradient entries. dS S^-1 = (dU U^-1) (x) 1 + 1 (x) conj(dU U^-1) and the
+        // halves commute, so the two contributions sum to the reference's
+        // Re<<psi| dS |S^-1 phi>> (autodiff.hpp:297-322) while each half costs a
+        // 2^m x 2^m product instead of one 4^m x 4^m. VQB_MIXED_SPLIT=0 keeps
+        // the single step.
+        static const bool split = [] {
+            const char *v = std::getenv("VQB_MIXED_SPLIT");
+            return !(v && *v == '0');
+        }();
+        // (a diagonal gate stays one step: the ket and bra phases cancel on
+        // half of the entries, which the single diagonal superoperator skips)
+        bool diagonal = true;
+        for (int r = 0; r < g.dim() && diagonal; ++r)
+            for (int c = 0; c < g.dim(); ++c)
+                if (r != c && inv.mat[r + (size_t)c * g.dim()] != cplx(0)) {
+                    diagonal = false;
+                    break;
+                }
+        if (split && !diagonal) {
+            RevOp ket, bra;
+            ket.phi_op = ket.psi_op = inv;
+            bra.phi_op = bra.psi_op = bra_side(inv, n);
+            for (int p = 0; p < g.np; ++p) {
+                if (!g.is_param[p]) continue;
+                const cvec du = gate_derivative(g, p);
+                bra.dmats.push_back(conjugated(du));
+                ket.dmats.push_back(du);
+            }
+            ket.grad_base = bra.grad_base = base[i];
+            ket.scale = bra.scale = 1.0; // grads = Re(acc) (autodiff.hpp:320-322)
+            prog.push_back(std::move(ket));
+            prog.push_back(std::move(bra));
+            continue;
+        }
         const int d = g.dim();
         int pos[6];
         for (int k = 0; k < g.m; ++k) {

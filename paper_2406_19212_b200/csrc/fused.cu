@@ -497,15 +497,22 @@ __global__ void __launch_bounds__(kT, 2) k_stage(double2 *__restrict__ phi, doub
     }
 }
 
-// grads[j] = scale[j] * sum_b partial[b][j] (fixed block order)
+// grads[dst] += sum over the slots of that destination (chained in slot order
+// by slot_links) of scale[j] * sum_b partial[b][j] (fixed block order): one
+// thread per destination, deterministic
 __global__ void k_reduce_grads(const double *__restrict__ partial, int nblocks, int ld,
                                const double *__restrict__ scale, const long long *__restrict__ dst,
-                               int ncols, double *__restrict__ grads) {
+                               const long long *__restrict__ link, int ncols,
+                               double *__restrict__ grads) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= ncols) return;
-    double v = 0;
-    for (int b = 0; b < nblocks; ++b) v += partial[(size_t)b * ld + j];
-    grads[dst[j]] = scale[j] * v;
+    if (j >= ncols || !(link[j] & 1)) return;
+    double acc = 0;
+    for (long long k = j; k >= 0; k = link[k] >> 1) {
+        double v = 0;
+        for (int b = 0; b < nblocks; ++b) v += partial[(size_t)b * ld + k];
+        acc += scale[k] * v;
+    }
+    grads[dst[j]] += acc;
 }
 
 bool is_identity(const cplx *m, int d) {
@@ -708,11 +715,16 @@ void execute(DeviceState *sphi, DeviceState *spsi, const std::vector<FusedOp> &f
     const int grid = (int)std::min<unsigned long long>((unsigned long long)nsm * per_sm, max_tiles);
     if (REV && nslots_total > 0) {
         m_partial.ensure(sizeof(double) * (size_t)grid * nslots_total);
-        m_slots.ensure((sizeof(double) + sizeof(long long)) * nslots_total);
+        m_slots.ensure((sizeof(double) + 2 * sizeof(long long)) * nslots_total);
+        const std::vector<long long> links = slot_links(slot_dst);
         VQB_CUDA(cudaMemcpyAsync(m_slots.p, slot_scale.data(), sizeof(double) * nslots_total,
                                  cudaMemcpyHostToDevice, st));
         VQB_CUDA(cudaMemcpyAsync(static_cast<char *>(m_slots.p) + sizeof(double) * nslots_total,
                                  slot_dst.data(), sizeof(long long) * nslots_total,
+                                 cudaMemcpyHostToDevice, st));
+        VQB_CUDA(cudaMemcpyAsync(static_cast<char *>(m_slots.p) +
+                                     (sizeof(double) + sizeof(long long)) * nslots_total,
+                                 links.data(), sizeof(long long) * nslots_total,
                                  cudaMemcpyHostToDevice, st));
     }
     for (size_t i = 0; i < stages.size(); ++i) {
@@ -739,6 +751,8 @@ void execute(DeviceState *sphi, DeviceState *spsi, const std::vector<FusedOp> &f
             static_cast<const double *>(m_slots.p),
             reinterpret_cast<const long long *>(static_cast<char *>(m_slots.p) +
                                                 sizeof(double) * nslots_total),
+            reinterpret_cast<const long long *>(static_cast<char *>(m_slots.p) +
+                                                (sizeof(double) + sizeof(long long)) * nslots_total),
             nslots_total, dgrads);
         check_launch("k_reduce_grads", pf_);
     }

@@ -290,6 +290,7 @@ struct Epilogue {
     double2 *out_c;   // complex results [ns] (nullable)
     double *out_r;    // real_scale * Re(result) [ns] (nullable)
     double real_scale;
+    bool accumulate = false; // out_r[s] += ... (gradient vectors: several steps may share an entry)
 };
 
 // Block-reduce NS complex values, store the block partial, and let the last
@@ -341,7 +342,7 @@ __device__ void reduce_epilogue(double2 (&v)[NS], int ns, double2 *partials, uns
             w = warp_sum(w);
             if (lane == 0) {
                 if (ep.out_c) ep.out_c[s] = w;
-                if (ep.out_r) ep.out_r[s] = ep.real_scale * w.x;
+                if (ep.out_r) ep.out_r[s] = (ep.accumulate ? ep.out_r[s] : 0.0) + ep.real_scale * w.x;
             }
         }
     }
@@ -976,7 +977,7 @@ static void reverse_m(double2 *phi, double2 *psi, int pn, const int *pos1, const
     const uint64_t groups = 1ull << (pn - M);
     const ProfMark pf_ = prof_begin(w->stream);
     k_reverse_step<M><<<reduce_grid(groups), kThreads, 0, w->stream>>>(
-        phi, psi, groups, A, w->ws.partials, w->ws.counter, Epilogue{out_c, out_r, scale});
+        phi, psi, groups, A, w->ws.partials, w->ws.counter, Epilogue{out_c, out_r, scale, true});
     check_launch("k_reverse_step", pf_);
 }
 

@@ -1,6 +1,8 @@
 // Operation analysis and greedy stage packing (see plan.hpp).
 #include "plan.hpp"
 
+#include <unordered_map>
+
 #include <algorithm>
 #include <deque>
 
@@ -72,6 +74,24 @@ FusedOp analyse(const int *pos1, int m, const std::vector<const cvec *> &mats) {
 }
 
 } // namespace
+
+std::vector<long long> slot_links(const std::vector<long long> &dst) {
+    std::vector<long long> link(dst.size(), -1 * 2);
+    std::unordered_map<long long, long long> last;
+    for (size_t j = 0; j < dst.size(); ++j) {
+        auto it = last.find(dst[j]);
+        if (it == last.end()) {
+            link[j] = -1 * 2 + 1; // first slot of its destination, end of chain
+            last[dst[j]] = (long long)j;
+        } else {
+            // append to the chain, keeping the predecessor's leader bit
+            link[it->second] = (long long)j * 2 + (link[it->second] & 1);
+            link[j] = -1 * 2;
+            it->second = (long long)j;
+        }
+    }
+    return link;
+}
 
 int entry_class(const cplx &v) {
     const double re = v.real(), im = v.imag();

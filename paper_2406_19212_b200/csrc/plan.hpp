@@ -73,6 +73,9 @@ std::vector<const FusedOp *> fuse_blocks_ref(const std::vector<FusedOp> &ops, co
 // Entry class: 0 zero, 1 real, 2 imaginary, 3 complex, 4 exactly +1,
 // 5 exactly -1, 6 exactly +i, 7 exactly -i.
 int entry_class(const cplx &v);
+// Gradient slots that share a destination, chained in slot order:
+// link[j] = (next slot of dst[j], or -1) * 2 + (1 if j is its destination's first slot)
+std::vector<long long> slot_links(const std::vector<long long> &dst);
 // FP64 instructions per amplitude of an op's register code: per output row
 // a unit entry is emitted first and costs nothing (a copy), every other term
 // 2 (unit, real, imaginary) or 4 (complex); identity sub-matrices cost

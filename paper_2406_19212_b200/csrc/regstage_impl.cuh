@@ -730,15 +730,22 @@ __global__ void __launch_bounds__(T, (kBlocksPerSm<REV, WIDE>))
     }
 }
 
-// grads[dst[j]] = scale[j] * sum_b partial[b][j] (fixed block order)
+// grads[dst] += sum over the slots of that destination (chained in slot order,
+// slot_links) of scale[j] * (sum_b partial[b][j] + extra[j]), blocks in fixed
+// order: one thread per destination, deterministic
 __global__ void k_grads(const double *__restrict__ partial, int nblocks, int ld,
                         const double *__restrict__ scale, const long long *__restrict__ dst,
-                        int ncols, const double *__restrict__ extra, double *__restrict__ grads) {
+                        const long long *__restrict__ link, int ncols,
+                        const double *__restrict__ extra, double *__restrict__ grads) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= ncols) return;
-    double v = 0;
-    for (int b = 0; b < nblocks; ++b) v += partial[(size_t)b * ld + j];
-    grads[dst[j]] = scale[j] * (v + extra[j]);
+    if (j >= ncols || !(link[j] & 1)) return;
+    double acc = 0;
+    for (long long k = j; k >= 0; k = link[k] >> 1) {
+        double v = 0;
+        for (int b = 0; b < nblocks; ++b) v += partial[(size_t)b * ld + k];
+        acc += scale[k] * (v + extra[k]);
+    }
+    grads[dst[j]] += acc;
 }
 
 // Specialised adjoint launches write one partial per (slot, tile); this sums a
@@ -1198,7 +1205,11 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
                     o.mat_e = (unsigned)npool;
                     for (int p = 0; p < f.np; ++p)
                         for (int c = 0; c < (1 << f.nc); ++c) {
-                            const cplx e = f.sub_d[(size_t(p) << f.nc) + c] * f.sub_phi[c];
+                            cplx e = f.sub_d[(size_t(p) << f.nc) + c] * f.sub_phi[c];
+                            // parts at rounding level of an exact zero are zero (a
+                            // rotation's e is -i/2 times a sign: imaginary)
+                            if (std::abs(e.real()) < 4e-15) e.real(0.0);
+                            if (std::abs(e.imag()) < 4e-15) e.imag(0.0);
                             P.pool[npool++] = make_double2(e.real(), e.imag());
                         }
                 }
@@ -1554,6 +1565,12 @@ std::vector<int> dot_selectable(const ROp &op, int cs) {
         if (dynamic ? (cc & rmask) == cs : cc == cs) sel.push_back(cc);
     return sel;
 }
+// matrices the contraction of a parametric step uses: D_p (with the updated
+// Phi), G_p (ROp::unit bit 1, old Phi), or for a unit-modulus diagonal step
+// the table e_p = D_p M at mat_e (old Phi: conj(psi) phi is invariant under
+// the step, autodiff contribution Re(conj(psi) e phi))
+unsigned dot_base(const ROp &op) { return op.nt == 0 && (op.unit & 1) ? op.mat_e : op.mat_d; }
+
 // every plan a parametric 0..2-bit step's code depends on (kernel key)
 std::string dot_signature(const RParams &P, const ROp &op) {
     if (op.np <= 0 || op.nt >= 3) return "";
@@ -1565,7 +1582,7 @@ std::string dot_signature(const RParams &P, const ROp &op) {
     for (int p = 0; p < op.np; ++p)
         for (int cs = 0; cs < nsub; ++cs) {
             if (cs & ~rmask) continue;
-            s += dot_plan_sig(dot_plan(P, op.mat_d + (unsigned)(p * nsub * dd), dd, dot_selectable(op, cs)), dd);
+            s += dot_plan_sig(dot_plan(P, dot_base(op) + (unsigned)(p * nsub * dd), dd, dot_selectable(op, cs)), dd);
             s += ';';
         }
     return s;
@@ -2773,7 +2790,7 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
                         for (int p = 0; p < op.np; ++p) {
                             if (plans.count({p, cs})) continue;
                             const DotPlan pl =
-                                dot_plan(P, op.mat_d + (unsigned)(p * nsub * dd), dd, dot_selectable(op, cs));
+                                dot_plan(P, dot_base(op) + (unsigned)(p * nsub * dd), dd, dot_selectable(op, cs));
                             plans[{p, cs}] = pl;
                             if (!pl.ok) continue;
                             const std::string w = "w" + I(p) + "_" + I(cs) + "_";
@@ -2788,10 +2805,11 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
                     const int cs = cstat(i);
                     int idx[4];
                     group_idx(op.nt, op.code, i, idx);
-                    const bool gpre = (op.unit & 2) != 0; // G_p = D_p inv on the old Phi
+                    // G_p = D_p inv, or e_p of a unit-modulus diagonal step, on the old Phi
+                    const bool gpre = (op.unit & 2) != 0 || dot_base(op) != op.mat_d;
                     if (!gpre) emit(mv_code("vf", idx, D, mexpr(op.mat, cs), mcls(op.mat, cs), fl));
                     for (int p = 0; p < op.np; ++p) {
-                        const unsigned dof = op.mat_d + (unsigned)(p * nsub * dd);
+                        const unsigned dof = dot_base(op) + (unsigned)(p * nsub * dd);
                         auto it = plans.find({p, cs});
                         if (it != plans.end() && it->second.ok)
                             emit(dot_plan_group(it->second, "w" + I(p) + "_" + I(cs) + "_", idx, D, fl));
@@ -2805,7 +2823,7 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
                     const DotPlan &pl = kv.second;
                     if (!pl.ok) continue;
                     const int p = kv.first.first, cs = kv.first.second;
-                    const unsigned dof = op.mat_d + (unsigned)(p * nsub * dd);
+                    const unsigned dof = dot_base(op) + (unsigned)(p * nsub * dd);
                     const std::string w = "w" + I(p) + "_" + I(cs) + "_", acc = "acc_s" + I(op.slot + p);
                     for (int c = 0; c < pl.nclass; ++c) {
                         const std::string m = mexpr(dof, cs)(pl.ref[c]);
@@ -3258,18 +3276,24 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
     if (REV && total_slots > 0) {
         wait_issue_gate();
         if ((int)slots.scale.size() != total_slots) raise(VQB_ERR_INTERNAL, "gradient slot mismatch");
-        m_slots.ensure((sizeof(double) + sizeof(long long)) * total_slots);
+        m_slots.ensure((sizeof(double) + 2 * sizeof(long long)) * total_slots);
+        const std::vector<long long> links = slot_links(slots.dst);
         VQB_CUDA(cudaMemcpyAsync(m_slots.p, slots.scale.data(), sizeof(double) * total_slots,
                                  cudaMemcpyHostToDevice, st));
         VQB_CUDA(cudaMemcpyAsync(static_cast<char *>(m_slots.p) + sizeof(double) * total_slots,
                                  slots.dst.data(), sizeof(long long) * total_slots,
                                  cudaMemcpyHostToDevice, st));
+        VQB_CUDA(cudaMemcpyAsync(static_cast<char *>(m_slots.p) +
+                                     (sizeof(double) + sizeof(long long)) * total_slots,
+                                 links.data(), sizeof(long long) * total_slots, cudaMemcpyHostToDevice, st));
         const ProfMark pf_ = prof_begin(st);
         k_grads<<<(total_slots + 127) / 128, 128, 0, st>>>(
             static_cast<const double *>(m_partial.p), grid, total_slots,
             static_cast<const double *>(m_slots.p),
             reinterpret_cast<const long long *>(static_cast<char *>(m_slots.p) +
                                                 sizeof(double) * total_slots),
+            reinterpret_cast<const long long *>(static_cast<char *>(m_slots.p) +
+                                                (sizeof(double) + sizeof(long long)) * total_slots),
             total_slots, static_cast<const double *>(m_slotsum.p), dgrads);
         check_launch("k_grads", pf_);
     }
