@@ -701,7 +701,7 @@ def measure(wl: Workload, args, eng, world, rank, local, dist, steps=None, warmu
         h_in[0] = 1.0
         from paper_2406_19212_b200.abi import c128_p
         pin = ct.cast(ct.c_void_p(h_in.data_ptr()), c128_p)
-        up = eng._fn("state_upload")
+        up = eng._fn("state_upload_async")  # ordered on the state's stream; the gradient call synchronises
 
         # gradient_pure / gradient_mixed (autodiff.hpp:95-98,184-188): the
         # input is s0 (uploaded from pinned host memory every step), the
@@ -733,7 +733,7 @@ def measure(wl: Workload, args, eng, world, rank, local, dist, steps=None, warmu
         e2e = {"value": wl.job_units(steps) / (ems / 1e3), "unit": wl.unit,
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": 8 * (1 + nparams),
                "ms_per_step": ems / steps, "loss": last["loss"],
-               "path": "vqb_state_upload (s0 from pinned host memory) -> vqb_gradient_"
+               "path": "vqb_state_upload_async (s0 from pinned host memory) -> vqb_gradient_"
                        + ("pure" if wl.kind == "grad_pure" else "mixed") + " (loss + gradients to host)"}
         del h_in
 

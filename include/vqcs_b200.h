@@ -191,6 +191,13 @@ VQB_API int vqb_state_set_zero(vqb_state *st); /* back to |0...0> */
  * buffer may be pageable or pinned. */
 VQB_API int vqb_state_upload(vqb_state *st, const vqb_c128 *host, uint64_t count);
 VQB_API int vqb_state_download(const vqb_state *st, vqb_c128 *host, uint64_t count);
+/* Upload without waiting: `host` must be page-locked and stay unchanged until
+ * the next call on this state that returns a result to the host (every such
+ * call synchronises the state's stream, on which the copy is ordered). Lets
+ * the host-side planning of the following call overlap the transfer.
+ * VQB_ERR_USAGE for pageable memory. No reference counterpart (the
+ * reference's states live in host memory, state.hpp:175-256). */
+VQB_API int vqb_state_upload_async(vqb_state *st, const vqb_c128 *host, uint64_t count);
 VQB_API int vqb_state_copy(vqb_state *dst, const vqb_state *src);
 /* Amplitudes [offset, offset + count) in canonical order (the host-side view
  * of a slice of state.hpp's amplitude vector, state.hpp:222-226) — for states

@@ -391,6 +391,7 @@ def bind_abi(lib: ct.CDLL, prefix: str) -> None:
         "state_destroy": (ct.c_int, [vp]),
         "state_info": (ct.c_int, [vp, ct.POINTER(i32), ct.POINTER(i32), ct.POINTER(u64)]),
         "state_upload": (ct.c_int, [vp, c128_p, u64]),
+        "state_upload_async": (ct.c_int, [vp, c128_p, u64]),
         "state_download": (ct.c_int, [vp, c128_p, u64]),
         "state_copy": (ct.c_int, [vp, vp]),
         "state_download_range": (ct.c_int, [vp, u64, u64, c128_p]),

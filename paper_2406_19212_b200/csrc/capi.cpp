@@ -218,6 +218,24 @@ VQB_API int vqb_state_upload(vqb_state *s, const vqb_c128 *host, uint64_t count)
     });
 }
 
+VQB_API int vqb_state_upload_async(vqb_state *s, const vqb_c128 *host, uint64_t count) {
+    return guard([&] {
+        DeviceState *d = ds(s);
+        DevScope on_(d->device);
+        need(host, "host");
+        check_count(d, count, "state_upload_async");
+        cudaPointerAttributes attr{};
+        if (!dry_run() && (cudaPointerGetAttributes(&attr, host) != cudaSuccess ||
+                           attr.type != cudaMemoryTypeHost)) {
+            cudaGetLastError();
+            raise(VQB_ERR_USAGE, "state_upload_async: the host buffer must be page-locked "
+                                 "(cudaMallocHost / cudaHostRegister); use vqb_state_upload");
+        }
+        VQB_CUDA(cudaMemcpyAsync(d->amps, host, sizeof(double2) * count, cudaMemcpyHostToDevice,
+                                 d->stream));
+    });
+}
+
 VQB_API int vqb_state_download(const vqb_state *s, vqb_c128 *host, uint64_t count) {
     return guard([&] {
         DeviceState *d = ds(s);

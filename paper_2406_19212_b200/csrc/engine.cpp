@@ -1,5 +1,6 @@
 // Lowering of circuits to gate programs and the element-by-element executor.
 #include "engine.hpp"
+#include "plan.hpp"
 
 #include <algorithm>
 #include <cstdlib>
@@ -68,20 +69,23 @@ std::vector<Gate> mixed_forward_program(const std::vector<Element> &es, int n) {
 // gradient_pure reverse loop (autodiff.hpp:130-150)
 std::vector<RevOp> pure_reverse_program(const std::vector<Element> &es,
                                         const std::vector<int64_t> &base) {
-    std::vector<RevOp> prog;
-    for (size_t i = es.size(); i-- > 0;) {
-        const Gate &g = es[i].gate;
-        RevOp r;
-        r.phi_op = gate_inverse(g);
-        r.psi_op = r.phi_op;
-        if (g.has_active()) {
-            for (int p = 0; p < g.np; ++p)
-                if (g.is_param[p]) r.dmats.push_back(gate_derivative(g, p));
-            r.grad_base = base[i];
-            r.scale = 2.0; // grads = 2 Re(acc) (autodiff.hpp:147-149)
+    const size_t n = es.size();
+    std::vector<RevOp> prog(n);
+    parallel_chunks(n, 96, [&](size_t b, size_t e) {
+        for (size_t k = b; k < e; ++k) {
+            const size_t i = n - 1 - k; // reverse order
+            const Gate &g = es[i].gate;
+            RevOp &r = prog[k];
+            r.phi_op = gate_inverse(g);
+            r.psi_op = r.phi_op;
+            if (g.has_active()) {
+                for (int p = 0; p < g.np; ++p)
+                    if (g.is_param[p]) r.dmats.push_back(gate_derivative(g, p));
+                r.grad_base = base[i];
+                r.scale = 2.0; // grads = 2 Re(acc) (autodiff.hpp:147-149)
+            }
         }
-        prog.push_back(std::move(r));
-    }
+    });
     return prog;
 }
 
@@ -117,10 +121,8 @@ std::vector<RevOp> mixed_reverse_program(const std::vector<Element> &es, int n,
         // Re<<psi| dS |S^-1 phi>> (autodiff.hpp:297-322) while each half costs a
         // 2^m x 2^m product instead of one 4^m x 4^m. VQB_MIXED_SPLIT=0 keeps
         // the single step.
-        static const bool split = [] {
-            const char *v = std::getenv("VQB_MIXED_SPLIT");
-            return !(v && *v == '0');
-        }();
+        const char *split_env = std::getenv("VQB_MIXED_SPLIT");
+        const bool split = !(split_env && *split_env == '0');
         // (a diagonal gate stays one step: the ket and bra phases cancel on
         // half of the entries, which the single diagonal superoperator skips)
         bool diagonal = true;

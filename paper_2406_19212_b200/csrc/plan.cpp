@@ -1,6 +1,11 @@
 // Operation analysis and greedy stage packing (see plan.hpp).
 #include "plan.hpp"
 
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <mutex>
+#include <thread>
 #include <unordered_map>
 
 #include <algorithm>
@@ -74,6 +79,136 @@ FusedOp analyse(const int *pos1, int m, const std::vector<const cvec *> &mats) {
 }
 
 } // namespace
+
+// ---- StageJob: ordered-consumption parallel for over a persistent pool ----
+struct StageJob::Impl {
+    size_t n = 0;
+    std::function<void(size_t)> fn;
+    std::atomic<size_t> next{0};
+    std::unique_ptr<std::atomic<int>[]> state; // 0 pending, 1 running, 2 done, 3 cancelled
+    std::mutex mu;
+    std::condition_variable cv;
+    // run one index if any is left; false when none
+    bool help() {
+        const size_t i = next.fetch_add(1);
+        if (i >= n) return false;
+        int expect = 0;
+        if (!state[i].compare_exchange_strong(expect, 1)) return true; // cancelled by the owner
+        fn(i); // fn reports its own errors through its captures
+        state[i].store(2);
+        {
+            std::lock_guard<std::mutex> lk(mu);
+        }
+        cv.notify_all();
+        return true;
+    }
+};
+
+namespace {
+class PlanPool {
+  public:
+    PlanPool() {
+        const char *v = std::getenv("VQB_PLAN_THREADS");
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        int nt = v && *v ? std::atoi(v) : (int)std::min(4u, hw > 2 ? (hw - 2) / 2 : 0u);
+        for (int t = 0; t < nt; ++t) threads_.emplace_back([this] { loop(); });
+    }
+    ~PlanPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto &t : threads_) t.join();
+    }
+    void add(const std::shared_ptr<StageJob::Impl> &job) {
+        if (threads_.empty()) return;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            jobs_.push_back(job);
+        }
+        cv_.notify_all();
+    }
+
+  private:
+    void loop() {
+        for (;;) {
+            std::shared_ptr<StageJob::Impl> job;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || !jobs_.empty(); });
+                if (stop_) return;
+                job = jobs_.front();
+                if (job->next.load() >= job->n) {
+                    jobs_.pop_front();
+                    continue;
+                }
+            }
+            while (job->help()) {
+            }
+        }
+    }
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<std::shared_ptr<StageJob::Impl>> jobs_;
+    std::vector<std::thread> threads_;
+    bool stop_ = false;
+};
+PlanPool &plan_pool() {
+    static PlanPool *p = new PlanPool; // never destroyed: workers may outlive static teardown
+    return *p;
+}
+} // namespace
+
+StageJob::StageJob(size_t n, std::function<void(size_t)> fn) : impl_(std::make_shared<Impl>()) {
+    impl_->n = n;
+    impl_->fn = std::move(fn);
+    impl_->state.reset(new std::atomic<int>[n ? n : 1]);
+    for (size_t i = 0; i < n; ++i) impl_->state[i].store(0);
+    if (n > 1) plan_pool().add(impl_);
+}
+
+void StageJob::wait_for(size_t i) {
+    Impl &J = *impl_;
+    while (J.state[i].load() != 2) {
+        if (J.help()) continue; // take part instead of sleeping
+        std::unique_lock<std::mutex> lk(J.mu);
+        J.cv.wait_for(lk, std::chrono::microseconds(50), [&] { return J.state[i].load() == 2; });
+    }
+}
+
+StageJob::~StageJob() {
+    Impl &J = *impl_;
+    // nothing may start after this point, and whatever runs must finish (fn
+    // references the caller's frame)
+    J.next.store(J.n);
+    for (size_t i = 0; i < J.n; ++i) {
+        int expect = 0;
+        if (J.state[i].compare_exchange_strong(expect, 3)) continue; // never started: cancelled
+        while (J.state[i].load() == 1) std::this_thread::yield();
+    }
+}
+
+void parallel_chunks(size_t n, size_t chunk, const std::function<void(size_t, size_t)> &fn) {
+    if (n <= chunk) {
+        if (n) fn(0, n);
+        return;
+    }
+    const size_t nchunks = (n + chunk - 1) / chunk;
+    std::vector<std::exception_ptr> errs(nchunks);
+    {
+        StageJob job(nchunks, [&](size_t c) {
+            try {
+                fn(c * chunk, std::min(n, (c + 1) * chunk));
+            } catch (...) {
+                errs[c] = std::current_exception();
+            }
+        });
+        for (size_t c = 0; c < nchunks; ++c) job.wait_for(c);
+    }
+    for (auto &e : errs)
+        if (e) std::rethrow_exception(e);
+}
 
 std::vector<long long> slot_links(const std::vector<long long> &dst) {
     std::vector<long long> link(dst.size(), -1 * 2);

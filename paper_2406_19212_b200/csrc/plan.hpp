@@ -13,6 +13,8 @@
 // disjoint (they commute), so the stage order reproduces the program exactly.
 #pragma once
 #include <deque>
+#include <functional>
+#include <memory>
 
 #include "engine.hpp"
 
@@ -73,6 +75,25 @@ std::vector<const FusedOp *> fuse_blocks_ref(const std::vector<FusedOp> &ops, co
 // Entry class: 0 zero, 1 real, 2 imaginary, 3 complex, 4 exactly +1,
 // 5 exactly -1, 6 exactly +i, 7 exactly -i.
 int entry_class(const cplx &v);
+// Host planning in parallel: fn(0..n-1) on a small persistent pool (the caller
+// takes part; several callers may overlap). done(i) is polled by consumers
+// that need results in order: wait_for(i) returns once fn(i) has finished,
+// running other indices of the job meanwhile.
+class StageJob {
+  public:
+    StageJob(size_t n, std::function<void(size_t)> fn);
+    ~StageJob(); // waits for indices still running
+    void wait_for(size_t i);
+    struct Impl;
+
+  private:
+    std::shared_ptr<Impl> impl_;
+};
+
+// fn(begin, end) over [0, n) in chunks on the planning pool; returns when all
+// chunks are done. Small n runs inline.
+void parallel_chunks(size_t n, size_t chunk, const std::function<void(size_t, size_t)> &fn);
+
 // Gradient slots that share a destination, chained in slot order:
 // link[j] = (next slot of dst[j], or -1) * 2 + (1 if j is its destination's first slot)
 std::vector<long long> slot_links(const std::vector<long long> &dst);

@@ -2629,9 +2629,15 @@ std::string jit_reverse_source(const RParams &P, bool *uses_spool, double *flops
                     flush_slots(acc_budget);
                 }
                 // every element: the product of its phase products
+                // (innermost product from the masks with the fewest classes: the
+                // partial products shared between elements are then the small ones)
+                std::vector<int> by_size(masks);
+                std::stable_sort(by_size.begin(), by_size.end(), [](int a, int b) {
+                    return __builtin_popcount(a) < __builtin_popcount(b);
+                });
                 for (int i = 0; i < R; ++i) {
                     std::string ph;
-                    for (int m : masks) {
+                    for (int m : by_size) {
                         const int g = extract(i, m);
                         if (!ph_set[{m, g}]) continue;
                         const std::string t2 = "PH" + I(m) + "_" + I(g);
@@ -2958,7 +2964,7 @@ std::string shape_key(const RParams &P, bool rev) {
     auto add = [&](const void *p, size_t n) { key.append(static_cast<const char *>(p), n); };
     add(P.bits, sizeof P.bits);
     add(&P.ntiles, sizeof P.ntiles);
-    add(&P.nsubs, 4 * sizeof(int)); // nsubs, nslots, slot_begin, partial_ld
+    add(&P.nsubs, 2 * sizeof(int)); // nsubs, nslots (slot_begin and partial_ld do not shape the code)
     add(P.subs, sizeof(RSub) * (size_t)P.nsubs);
     add(P.ops, sizeof(ROp) * (size_t)nops);
     add(&P.ntab, 3 * sizeof(int)); // ntab, nxpat, npool
@@ -3027,7 +3033,6 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
         VQB_CUDA(cudaMemsetAsync(m_partial.p, 0, sizeof(double) * (size_t)grid * total_slots, st));
     }
     SlotMap slots;
-    std::deque<FusedOp> fused_store; // merged blocks of every stage (stable addresses)
     // Actions (a launch, or an unfusable op) are lowered in program order and
     // issued as soon as their kernel is known, so the host's planning of later
     // stages overlaps the device's work on earlier ones. The first
@@ -3141,71 +3146,97 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
         }
         check_launch(REV ? "k_regstage_rev" : "k_regstage", pf_);
     };
-    auto submit = [&](Action &&act) {
-        if (use_jit && act.P) {
-            HostAcc ha(&t_key);
-            act.key = shape_key(*act.P, REV);
-            act.hash = fnv1a(act.key);
-            act.jit = find_shape(act.key, act.hash);
-            if (!act.jit) batching = true; // compile later, with the other misses
-        }
-        if (batching) pending.push_back(std::move(act));
-        else {
-            HostAcc ha(&t_issue);
-            issue(act);
+    // Per stage: block fusion, lowering (one or more launches) and the kernel
+    // lookup. Stages are independent once planned, so they are prepared in
+    // parallel on the planning pool (plan.hpp StageJob) and issued in program
+    // order as they complete; gradient slots are numbered per stage and
+    // shifted to their place in the sweep afterwards.
+    struct StageOut {
+        std::vector<Action> acts;
+        SlotMap slots;
+        std::exception_ptr err;
+    };
+    std::vector<StageOut> outs(stages.size());
+    auto prepare = [&](size_t si) {
+        StageOut &so = outs[si];
+        try {
+            const Stage &sg = stages[si];
+            if (!sg.fused) {
+                Action a;
+                a.fallback_op = sg.ops[0];
+                so.acts.push_back(std::move(a));
+                return;
+            }
+            std::deque<FusedOp> store; // merged blocks (stable addresses)
+            std::vector<const FusedOp *> blocks;
+            if (max_support > 0) blocks = fuse_blocks_ref(fops, sg.ops, max_support, store, cost_fusion);
+            else
+                for (int idx : sg.ops) blocks.push_back(&fops[idx]);
+            std::vector<int> remaining(blocks.size());
+            for (size_t i = 0; i < blocks.size(); ++i) remaining[i] = (int)i;
+            while (!remaining.empty()) {
+                Action act;
+                act.P = std::make_unique<RParams>();
+                RParams &P = *act.P;
+                lower_stage_reg(sg, blocks, remaining, pn, REV, P, so.slots, regwide,
+                                use_jit && env_int("VQB_JIT_GDIFF", 1) != 0, factor_on);
+                P.partial_ld = total_slots;
+                if (stats) {
+                    int nt_hist[5] = {0, 0, 0, 0, 0}, nops = 0;
+                    for (int i = 0; i < P.nsubs; ++i) nops += P.subs[i].op_count;
+                    for (int i = 0; i < nops; ++i) nt_hist[std::min(P.ops[i].nt, 4)]++;
+                    std::fprintf(stderr, "[regstage%s] gates %zu blocks %zu subs %d ops nt0..4 %d %d %d %d %d slots %d\n",
+                                 REV ? "-rev" : "", sg.ops.size(), blocks.size(), P.nsubs, nt_hist[0],
+                                 nt_hist[1], nt_hist[2], nt_hist[3], nt_hist[4], P.nslots);
+                }
+                {
+                    // algorithmic FP64 flops of this launch: a dense 2^nt x 2^nt
+                    // complex matrix costs 8 * 2^nt flops per amplitude per state;
+                    // a parametric step adds the np derivative contractions
+                    double per_amp = 0;
+                    int nops = 0;
+                    for (int i = 0; i < P.nsubs; ++i) nops += P.subs[i].op_count;
+                    for (int i = 0; i < nops; ++i) {
+                        const ROp &o = P.ops[i];
+                        const double mv = o.nt == 0 ? 6.0 : 8.0 * (1 << o.nt);
+                        per_amp += (REV ? 2.0 : 1.0) * mv + (REV ? o.np * (mv + 2.0) : 0.0);
+                    }
+                    act.dense_flops_per_amp = per_amp;
+                }
+                for (int i = 0; i < P.nsubs; ++i)
+                    for (int o = 0; o < P.subs[i].op_count; ++o)
+                        act.has_wide = act.has_wide || P.ops[P.subs[i].op_begin + o].nt >= 3;
+                act.wide = REV || act.has_wide;
+                if (use_jit) {
+                    act.key = shape_key(P, REV);
+                    act.hash = fnv1a(act.key);
+                    act.jit = find_shape(act.key, act.hash);
+                }
+                so.acts.push_back(std::move(act));
+            }
+        } catch (...) {
+            so.err = std::current_exception();
         }
     };
-    for (const Stage &sg : stages) {
-        if (!sg.fused) {
-            Action a;
-            a.fallback_op = sg.ops[0];
-            submit(std::move(a));
-            continue;
-        }
-        std::vector<const FusedOp *> blocks;
-        HostAcc ha_f(&t_fuse);
-        if (max_support > 0) blocks = fuse_blocks_ref(fops, sg.ops, max_support, fused_store, cost_fusion);
-        else
-            for (int idx : sg.ops) blocks.push_back(&fops[idx]);
-        std::vector<int> remaining(blocks.size());
-        for (size_t i = 0; i < blocks.size(); ++i) remaining[i] = (int)i;
-        while (!remaining.empty()) {
-            Action act;
-            act.P = std::make_unique<RParams>();
-            RParams &P = *act.P;
-            {
-                HostAcc ha(&t_lower);
-                lower_stage_reg(sg, blocks, remaining, pn, REV, P, slots, regwide,
-                                use_jit && env_int("VQB_JIT_GDIFF", 1) != 0, factor_on);
-            }
-            P.partial_ld = total_slots;
-            if (stats) {
-                int nt_hist[5] = {0, 0, 0, 0, 0}, nops = 0;
-                for (int i = 0; i < P.nsubs; ++i) nops += P.subs[i].op_count;
-                for (int i = 0; i < nops; ++i) nt_hist[std::min(P.ops[i].nt, 4)]++;
-                std::fprintf(stderr, "[regstage%s] gates %zu blocks %zu subs %d ops nt0..4 %d %d %d %d %d slots %d\n",
-                             REV ? "-rev" : "", sg.ops.size(), blocks.size(), P.nsubs, nt_hist[0],
-                             nt_hist[1], nt_hist[2], nt_hist[3], nt_hist[4], P.nslots);
-            }
-            {
-                // algorithmic FP64 flops of this launch: a dense 2^nt x 2^nt
-                // complex matrix costs 8 * 2^nt flops per amplitude per state;
-                // a parametric step adds the np derivative contractions
-                double per_amp = 0;
-                int nops = 0;
-                for (int i = 0; i < P.nsubs; ++i) nops += P.subs[i].op_count;
-                for (int i = 0; i < nops; ++i) {
-                    const ROp &o = P.ops[i];
-                    const double mv = o.nt == 0 ? 6.0 : 8.0 * (1 << o.nt);
-                    per_amp += (REV ? 2.0 : 1.0) * mv + (REV ? o.np * (mv + 2.0) : 0.0);
+    {
+        HostAcc ha_f(&t_fuse); // fuse + lower + key, wall time of the pipeline
+        StageJob job(stages.size(), prepare);
+        for (size_t si = 0; si < stages.size(); ++si) {
+            job.wait_for(si);
+            StageOut &so = outs[si];
+            if (so.err) std::rethrow_exception(so.err);
+            const int shift = (int)slots.scale.size();
+            slots.scale.insert(slots.scale.end(), so.slots.scale.begin(), so.slots.scale.end());
+            slots.dst.insert(slots.dst.end(), so.slots.dst.begin(), so.slots.dst.end());
+            for (Action &act : so.acts) {
+                if (act.P) act.P->slot_begin += shift;
+                if (use_jit && act.P && !act.jit) batching = true; // compile later, with the other misses
+                if (batching) pending.push_back(std::move(act));
+                else {
+                    HostAcc ha(&t_issue);
+                    issue(act);
                 }
-                act.dense_flops_per_amp = per_amp;
             }
-            for (int i = 0; i < P.nsubs; ++i)
-                for (int o = 0; o < P.subs[i].op_count; ++o)
-                    act.has_wide = act.has_wide || P.ops[P.subs[i].op_begin + o].nt >= 3;
-            act.wide = REV || act.has_wide;
-            submit(std::move(act));
         }
     }
     if (!pending.empty()) {
@@ -3320,7 +3351,10 @@ void run_program_reg(DeviceState *s, const std::vector<Gate> &prog) {
     fops.reserve(prog.size());
     {
         HostTimer ht("analyse_gate x n");
-        for (const auto &g : prog) fops.push_back(analyse_gate(g));
+        fops.resize(prog.size());
+        parallel_chunks(prog.size(), 96, [&](size_t b, size_t e) {
+            for (size_t i = b; i < e; ++i) fops[i] = analyse_gate(prog[i]);
+        });
     }
     run_reg<false>(s, nullptr, fops, nullptr, [&](const FusedOp &f) {
         apply_gate_fast(s->amps, s->pn, f.gate, s->stream);
@@ -3332,10 +3366,13 @@ void run_reverse_reg(DeviceState *phi, DeviceState *psi, const std::vector<RevOp
     HostTimer ht("run_reverse_reg (analyse+run)");
     std::vector<FusedOp> fops;
     fops.reserve(prog.size());
-    for (const auto &r : prog) {
-        fops.push_back(analyse_rev(r));
-        if (fops.back().np > 0 && fops.back().nt > 2) fops.back().fusable = false;
-    }
+    fops.resize(prog.size());
+    parallel_chunks(prog.size(), 96, [&](size_t b, size_t e) {
+        for (size_t i = b; i < e; ++i) {
+            fops[i] = analyse_rev(prog[i]);
+            if (fops[i].np > 0 && fops[i].nt > 2) fops[i].fusable = false;
+        }
+    });
     run_reg<true>(phi, psi, fops, dgrads, [&](const FusedOp &f) {
         const RevOp &r = *f.rev;
         if (r.dmats.empty()) {

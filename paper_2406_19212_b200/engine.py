@@ -225,6 +225,13 @@ class Engine:
         self.check(self._fn("state_upload")(s.handle, amps.ctypes.data_as(c128_p),
                                             ct.c_uint64(amps.size)))
 
+    def upload_async(self, s: State, pinned_ptr: int, count: int) -> None:
+        """vqb_state_upload_async: `pinned_ptr` addresses page-locked host
+        memory that stays unchanged until the next result-returning call on `s`
+        (product only; the CPU checkers have no such entry point)."""
+        self.check(self._fn("state_upload_async")(s.handle, ct.cast(ct.c_void_p(pinned_ptr), c128_p),
+                                                  ct.c_uint64(count)))
+
     def download(self, s: State, out: Optional[np.ndarray] = None) -> np.ndarray:
         if out is None:
             out = np.empty(s.size, dtype=np.complex128)

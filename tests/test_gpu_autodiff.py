@@ -286,7 +286,13 @@ def test_specialised_adjoint_matches_reference(dev, ref, monkeypatch, regs):
                                      {"VQB_JIT_GDIFF": "0"}, {"VQB_JIT_FACTOR": "1"},
                                      {"VQB_JIT_FACTOR": "1", "VQB_JIT_GDIFF": "0"},
                                      {"VQB_JIT_REDLANES": "1"}, {"VQB_JIT_REDLANES": "8"},
-                                     {"VQB_JIT_DIRECT": "0"}])
+                                     {"VQB_JIT_DIRECT": "0"}, {"VQB_JIT_DOTPLAN": "0"},
+                                     {"VQB_JIT_REDBATCH": "1"}, {"VQB_JIT_REDBATCH": "2"},
+                                     {"VQB_MIXED_SPLIT": "0"},
+                                     {"VQB_JIT_FACTOR": "1", "VQB_MIXED_SPLIT": "0"},
+                                     {"VQB_JIT_FACTOR": "1", "VQB_JIT_RANKONE": "0"},
+                                     {"VQB_JIT_FACTOR": "1", "VQB_JIT_PAIRFACTOR": "0"},
+                                     {"VQB_JIT_FACTOR": "1", "VQB_JIT_DOTPLAN": "0"}])
 def test_structure_classes_and_generator_variants(dev, ref, monkeypatch, variant):
     """Specialised kernels key on which matrix entries are exactly zero, real or
     imaginary (structure-aware emission): angles that make entries vanish
@@ -295,7 +301,10 @@ def test_structure_classes_and_generator_variants(dev, ref, monkeypatch, variant
     adjoint, in every generator variant (diagonal runs off, no accumulator
     budget, eager relayouts, serial host planning, no derivative generators,
     scalar factoring and cost-model fusion forced on at this size (they
-    switch on by themselves at >= 2^22 amplitudes), partial-lane reductions)."""
+    switch on by themselves at >= 2^22 amplitudes), partial-lane reductions,
+    row-wise derivative contractions, unbatched slot reductions, unsplit
+    superoperator steps, channel steps without the rank-one form or without
+    per-state scalars)."""
     monkeypatch.setenv("VQB_JIT", "1")
     for k, v in variant.items():
         monkeypatch.setenv(k, v)
@@ -328,3 +337,38 @@ def test_structure_classes_and_generator_variants(dev, ref, monkeypatch, variant
     loss, g = dev.gradient_mixed(w.observable, w.circuit, dev.mixed_state(6))
     rloss, rg = ref.gradient_mixed(w.observable, w.circuit, ref.mixed_state(6))
     assert abs(loss - rloss) <= RTOL * abs(rloss) and rel_err(g, rg) <= RTOL
+
+
+@pytest.mark.parametrize("factor", ["0", "1"])
+def test_mixed_gradient_channel_forms(dev, ref, monkeypatch, factor):
+    """Channel steps of the density-matrix adjoint in every form the lowering
+    picks: depolarizing (rank-one, c (1 + e J)), amplitude and phase damping
+    (real scalar only), a Generic two-Kraus channel, a 2-qubit parametric gate
+    (fSim: ket and bra half steps on two bits each, five shared gradient
+    entries) and tied single-qubit rotations, against the reference's
+    gradient_mixed (autodiff.hpp:184-329)."""
+    from paper_2406_19212_b200.abi import ChannelKind, make_channel, standard_channel
+    monkeypatch.setenv("VQB_JIT", "1")
+    monkeypatch.setenv("VQB_JIT_FACTOR", factor)
+    n = 7
+    c = Circuit()
+    for q in range(1, n + 1):
+        c.push_back(standard_gate(GateKind.H, [q]))
+        c.push_back(parametric_gate(GateKind.Ry, [q], 0.3 + 0.1 * q, True))
+        c.push_back(standard_channel(ChannelKind.Depolarizing, q, 0.02))
+        c.push_back(parametric_gate(GateKind.Rz, [q], -0.2 + 0.05 * q, True))
+        c.push_back(standard_channel(ChannelKind.PhaseDamping, q, 0.03))
+    for q in range(1, n):
+        c.push_back(parametric_gate(GateKind.Fsim, [q, q + 1], [0.4, -0.3, 0.2, 0.7, -0.5], [True] * 5))
+        c.push_back(standard_channel(ChannelKind.AmplitudeDamping, q, 0.05))
+    g = 0.1
+    k0 = np.array([[1, 0], [0, math.sqrt(1 - g)]], dtype=complex)
+    k1 = np.array([[0, math.sqrt(g) * 0.6], [0, 0.8j * math.sqrt(g)]], dtype=complex)
+    c.push_back(make_channel([3], [k0, k1]))
+    for q in range(1, n + 1):
+        c.push_back(parametric_gate(GateKind.Rx, [q], 0.15 * q, True))
+    op = sum_z(n)
+    loss, gr = dev.gradient_mixed(op, c, dev.mixed_state(n))
+    rloss, rg = ref.gradient_mixed(op, c, ref.mixed_state(n))
+    assert abs(loss - rloss) <= RTOL * abs(rloss)
+    assert rel_err(gr, rg) <= RTOL

@@ -118,3 +118,28 @@ def test_bounds_checked_kernels(dev, ref, monkeypatch, variant):
     loss, g = dev.gradient_mixed(d.observable, d.circuit, dev.mixed_state(6))
     rl, rg = ref.gradient_mixed(d.observable, d.circuit, ref.mixed_state(6))
     assert abs(loss - rl) <= 1e-10 * max(1.0, abs(rl)) and rel_err(g, rg) <= 1e-10
+
+
+def test_async_upload_from_pinned_memory(dev):
+    """vqb_state_upload_async: ordered on the state's stream (the following
+    gradient sees the uploaded state), pageable memory is refused."""
+    import torch
+    from paper_2406_19212_b200.abi import UsageError
+    n = 14
+    w = circuits.config0(n=n, layers=2)
+    rng = np.random.default_rng(5)
+    amps = random_state(n, rng)
+    s_sync = dev.pure_state(n)
+    dev.upload(s_sync, amps)
+    want = dev.gradient_pure(w.observable, w.circuit, s_sync)
+    pinned = torch.zeros(2 << n, dtype=torch.float64, pin_memory=True)
+    pinned.numpy().view(np.complex128)[:] = amps
+    s = dev.pure_state(n)
+    dev.upload_async(s, pinned.data_ptr(), 1 << n)
+    got = dev.gradient_pure(w.observable, w.circuit, s)
+    assert got[0] == want[0] and np.array_equal(got[1], want[1])
+    pageable = np.ascontiguousarray(amps)
+    with pytest.raises(UsageError):
+        dev.upload_async(s, pageable.ctypes.data, 1 << n)
+    s.free()
+    s_sync.free()
