@@ -241,6 +241,14 @@ DeviceState *clone(const DeviceState *src) {
     return d;
 }
 
+// The reverse steps after the last parametric one only bring Phi back to the
+// initial state (autodiff.hpp:151-154 reports max |Phi_end - s0|): without a
+// residual request nothing reads their result, so they are not run.
+void drop_dead_tail(std::vector<RevOp> &rprog, bool want_residual) {
+    if (want_residual) return;
+    while (!rprog.empty() && rprog.back().dmats.empty()) rprog.pop_back();
+}
+
 void check_operator(const PauliPack &op, int n, const char *what) {
     if (op.max_qubit > n)
         raise(VQB_ERR_INDEX, std::string(what) + ": operator acts on qubit " +
@@ -341,6 +349,7 @@ GradientOut gradient_pure(const vqb_op *ops, int64_t count, const vqb_pauli_term
         {
             HostTimer ht2("reverse program");
             rprog = pure_reverse_program(es, base);
+            drop_dead_tail(rprog, want_residual);
         }
         run_reverse(phi, psi, rprog, dgrads, fused);
     };
@@ -426,7 +435,9 @@ GradientOut gradient_mixed(const vqb_op *ops, int64_t count, const vqb_pauli_ter
     // every writer accumulates: the ket and bra halves of a gate share its entries
     VQB_CUDA(cudaMemsetAsync(dgrads, 0, gbytes, phi->stream));
     auto sweep = [&] {
-        run_reverse(phi, psi, mixed_reverse_program(es, n, base, chan_inv, chan_adj), dgrads, fused);
+        std::vector<RevOp> rprog = mixed_reverse_program(es, n, base, chan_inv, chan_adj);
+        drop_dead_tail(rprog, want_residual);
+        run_reverse(phi, psi, rprog, dgrads, fused);
     };
     std::unique_ptr<GatedSweep> gs;
     if (total > 0 && parallel_adjoint()) gs = std::make_unique<GatedSweep>(sweep);
