@@ -150,7 +150,7 @@ class Workload:
 # ------------------------------------------------------------------ clocks sampler
 class ClockSampler:
     """SM clocks and clock-event (throttle) reasons sampled through NVML every
-    10 ms while the timed region runs (plus one sample at entry and exit, so
+    20 ms while the timed region runs (plus one sample at entry and exit, so
     short regions are covered); falls back to `nvidia-smi -lms 200`."""
     NAMES = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
              "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
@@ -163,17 +163,20 @@ class ClockSampler:
         self.stop = threading.Event()
         self.nv = None
         self.proc = None
+        self.mx = None
 
     def _sample(self):
         nv = self.nv
         sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
-        mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        if self.mx is None:  # constant: asked once (every NVML query takes driver locks the launches need too)
+            self.mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        mx = self.mx
         r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
         reasons = {k for k, attr in self.NAMES.items() if r & getattr(nv, attr, 0)}
         self.samples.append((float(sm), float(mx), reasons))
 
     def _poll(self):
-        while not self.stop.wait(0.01):
+        while not self.stop.wait(0.02):
             try:
                 self._sample()
             except Exception:

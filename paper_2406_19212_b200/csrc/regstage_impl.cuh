@@ -3028,10 +3028,16 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
     if (REV)
         for (const auto &f : fops) total_slots += f.np;
     static thread_local DevMem m_partial, m_slots;
-    if (REV && total_slots > 0) {
-        m_partial.ensure(sizeof(double) * (size_t)grid * total_slots);
+    // per-block partial rows of the interpreter's launches: zeroed at its first
+    // use; a sweep run entirely by specialised kernels (per-slot sums in
+    // m_slotsum) leaves them out of the final reduction
+    bool partial_rows_used = false;
+    auto use_partial_rows = [&] {
+        if (partial_rows_used || !REV || total_slots == 0) return;
         VQB_CUDA(cudaMemsetAsync(m_partial.p, 0, sizeof(double) * (size_t)grid * total_slots, st));
-    }
+        partial_rows_used = true;
+    };
+    if (REV && total_slots > 0) m_partial.ensure(sizeof(double) * (size_t)grid * total_slots);
     SlotMap slots;
     // Actions (a launch, or an unfusable op) are lowered in program order and
     // issued as soon as their kernel is known, so the host's planning of later
@@ -3051,8 +3057,15 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
     };
     // adjoint specialisation: per-(slot, tile) partials, summed per launch
     static thread_local DevMem m_jpartial, m_slotsum, m_slotsplit;
-    const size_t jpartial_bytes = sizeof(double) * (size_t)kMaxSlots * ntiles;
+    // Small sweeps (config 0: 2^10 tiles, 600 slots) keep every slot's tile
+    // partials of the whole sweep and sum them in one launch at the end
+    // instead of one small launch behind every stage.
+    const bool merged_sums = REV && total_slots > 0 && (size_t)total_slots * ntiles <= (size_t(1) << 23) &&
+                             ntiles < (1ull << 16);
+    const size_t jpartial_bytes =
+        sizeof(double) * (size_t)(merged_sums ? std::max(total_slots, kMaxSlots) : kMaxSlots) * ntiles;
     const bool use_jit = jit::enabled(pn) && (!REV || jpartial_bytes <= (size_t(1) << 30));
+    bool any_jit_slots = false;
     // wide operations on register bits need the specialised kernels (the
     // interpreter runs them through shared memory only)
     const bool regwide = use_jit && RB >= 4 && env_int("VQB_WIDE_REGS", 1) != 0;
@@ -3060,6 +3073,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
         m_slotsum.ensure(sizeof(double) * total_slots);
         VQB_CUDA(cudaMemsetAsync(m_slotsum.p, 0, sizeof(double) * total_slots, st));
         if (use_jit) m_jpartial.ensure(jpartial_bytes);
+        if (use_jit && merged_sums) VQB_CUDA(cudaMemsetAsync(m_jpartial.p, 0, jpartial_bytes, st));
     }
     // structure-aware kernels: merge blocks only where the emitted cost does
     // not grow, factor scalars out of the forward matrices (VQB_JIT_FACTOR=0:
@@ -3098,10 +3112,13 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             const size_t sm = (size_t)(sh.xtiles * TS + (sh.spool ? P.npool : 0)) * sizeof(double2) +
                               sizeof(double) * (size_t)P.nslots * NW * red_lanes_of();
             void *a0 = sphi->amps, *a1 = spsi->amps, *pp = m_jpartial.p;
+            if (merged_sums) pp = static_cast<double *>(m_jpartial.p) + (size_t)P.slot_begin * ntiles;
             void *args[4] = {&a0, &a1, &pp, P.pool};
             jit::launch(sh.k, (unsigned)ntiles, T, sm, st, args);
             check_launch("k_regstage_rev_jit", pf_);
-            if (P.nslots > 0) {
+            if (P.nslots > 0 && merged_sums) {
+                any_jit_slots = true; // summed after the last launch
+            } else if (P.nslots > 0) {
                 const ProfMark pf2 = prof_begin(st);
                 // small sweeps (few tiles): one block per slot, straight to the sums
                 double *slot_out = static_cast<double *>(m_slotsum.p) + P.slot_begin;
@@ -3135,6 +3152,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             check_launch("k_regstage_jit", pf_);
             return;
         }
+        use_partial_rows();
         if (act.wide) {
             const size_t sm = smem_bytes<REV>(P.npool);
             k_regstage<REV, true><<<grid_size<REV, true>(ntiles, sm), T, sm, st>>>(
@@ -3304,6 +3322,14 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             issue(act);
         }
     }
+    if (merged_sums && any_jit_slots) {
+        // slots of interpreter launches or fallback steps have no tile partials:
+        // their rows were zeroed with the buffer and add nothing
+        const ProfMark pf2 = prof_begin(st);
+        k_slot_sums<<<dim3(total_slots, 1), 256, 0, st>>>(static_cast<const double *>(m_jpartial.p), ntiles,
+                                                         static_cast<double *>(m_slotsum.p));
+        check_launch("k_slot_sums", pf2);
+    }
     if (REV && total_slots > 0) {
         wait_issue_gate();
         if ((int)slots.scale.size() != total_slots) raise(VQB_ERR_INTERNAL, "gradient slot mismatch");
@@ -3319,7 +3345,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
                                  links.data(), sizeof(long long) * total_slots, cudaMemcpyHostToDevice, st));
         const ProfMark pf_ = prof_begin(st);
         k_grads<<<(total_slots + 127) / 128, 128, 0, st>>>(
-            static_cast<const double *>(m_partial.p), grid, total_slots,
+            static_cast<const double *>(m_partial.p), partial_rows_used ? grid : 0, total_slots,
             static_cast<const double *>(m_slots.p),
             reinterpret_cast<const long long *>(static_cast<char *>(m_slots.p) +
                                                 sizeof(double) * total_slots),
