@@ -166,6 +166,11 @@ class DeviceState {
     void upload(std::span<const std::complex<double>> a) {
         check(vqb_state_upload(s_, reinterpret_cast<const vqb_c128 *>(a.data()), a.size()));
     }
+    // `a` must be page-locked and unchanged until the next call on this state
+    // that returns a result (vqb_state_upload_async)
+    void upload_async(std::span<const std::complex<double>> a) {
+        check(vqb_state_upload_async(s_, reinterpret_cast<const vqb_c128 *>(a.data()), a.size()));
+    }
     void download(std::span<std::complex<double>> a) const {
         check(vqb_state_download(s_, reinterpret_cast<vqb_c128 *>(a.data()), a.size()));
     }
