@@ -957,10 +957,10 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
     };
     auto pool_need = [&](const FusedOp &f) {
         if (f.nt >= 3) // XOR-term form: |X| * D entries per sub-matrix
-            return (count_x(f) * (1 << f.nt) << f.nc) * (1 + (f.pair ? 1 : 0)) + (f.pair ? 2 : 0);
+            return (count_x(f) * (1 << f.nt) << f.nc) * (1 + (f.pair ? 1 : 0)) + 2;
         const int dd = (1 << (2 * f.nt)) << f.nc;
         return dd * (1 + (f.pair ? 1 : 0) + (rev ? f.np : 0)) + (rev && f.nt == 0 ? f.np << f.nc : 0) +
-               (f.pair ? 2 : 0);
+               2; // + rank-one coefficients
     };
     int nops = 0, npool = 0, nslots = 0;
     while (!remaining.empty()) {
@@ -1125,6 +1125,27 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
                 if (fb.mask) o.unit |= 8;
                 o.slot = (int)(fa.mask ? fa.mask : fb.mask);
             }
+            // forward channel superoperators (non-parametric, no conditions): the
+            // same scalar / rank-one form, the scalar joins the launch's product
+            bool fwd_form = false;
+            if (factor && !rev && !f.pair && f.np == 0 && f.nc == 0 && f.nt >= 2 &&
+                (f.nt <= 2 || wide_in_regs(f)) && env_int("VQB_JIT_PAIRFACTOR", 1) != 0) {
+                fa = pair_form(f.nt > 1 ? permute_matrix(f.sub_phi, f.nt, order) : f.sub_phi, f.nt);
+                // register ops keep best_scale's (possibly complex) scalar unless
+                // the rank-one form applies; wide ops had no factoring at all
+                if (fa.mask || f.nt >= 3) {
+                    pair_phi = f.sub_phi;
+                    if (fa.c != 1.0) divide_by(pair_phi.data(), pair_phi.size(), cplx(fa.c));
+                    scale *= fa.c;
+                    src_phi = &pair_phi;
+                    if (env_int("VQB_JIT_RANKONE", 1) == 0) fa.mask = 0;
+                    if (fa.mask) {
+                        o.unit |= 4;
+                        o.slot = (int)fa.mask;
+                    }
+                    fwd_form = true;
+                }
+            }
             if (f.nt >= 3) {
                 // wide ops run in smem_op as sum_k diag(d_k) P_{x_k}: store the
                 // XOR patterns x_k and, per sub-matrix, d_k[r] = S[r, r ^ x_k]
@@ -1171,6 +1192,8 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
                 };
                 o.mat = pushx(*src_phi, &o.ident);
                 if (f.pair) o.mat_psi = pushx(*src_psi, &o.ident_psi);
+            } else if (fwd_form) {
+                o.mat = push(*src_phi, 0, &o.ident);
             } else if (factor && !f.pair && (!rev || f.np == 0 || use_g)) {
                 cvec sub = f.sub_phi;
                 double c = 0;
@@ -1977,6 +2000,24 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
                     dyn = "(0" + dyn + ")";
                     spool = true;
                 }
+                if (dyn.empty() && (op.unit & 4)) { // rank-one form (channel superoperators)
+                    if (op.ident & 1) continue;
+                    int rm = 0;
+                    for (int q = 0; q < op.nt; ++q) rm |= 1 << op.lb[q];
+                    for (int i0 = 0; i0 < R; ++i0) {
+                        if (i0 & rm) continue;
+                        int ridx[16], nr = 0;
+                        for (int r = 0; r < (1 << op.nt); ++r) {
+                            if (!((op.slot >> r) & 1)) continue;
+                            int x = i0;
+                            for (int q = 0; q < op.nt; ++q)
+                                if ((r >> q) & 1) x |= 1 << op.lb[q];
+                            ridx[nr++] = x;
+                        }
+                        emit(rank_one_code("v", ridx, nr, MP + "[" + std::to_string(op.mat_d) + "]", fl));
+                    }
+                    continue;
+                }
                 emit(jit_wide_regs(P, op, "v", op.mat, op.ident, dyn,
                                    [&](unsigned off) { return MP + "[" + std::to_string(off) + "]"; }, fl));
                 continue;
@@ -2141,6 +2182,13 @@ std::string jit_forward_source_rs16(const RParams &P, bool *uses_spool, bool *pe
                     if ((op.ident >> c) & 1) continue;
                     int idx[4];
                     group_idx(op.nt, op.code, i, idx);
+                    if (op.unit & 4) { // rank-one form (channel superoperators)
+                        int ridx[16], nr = 0;
+                        for (int r = 0; r < D; ++r)
+                            if ((op.slot >> r) & 1) ridx[nr++] = idx[r];
+                        emit(rank_one_code("v", ridx, nr, MP + "[" + std::to_string(op.mat_d) + "]", fl));
+                        continue;
+                    }
                     const unsigned base_off = op.mat + (unsigned)(c * dd);
                     emit(mv_code(
                         "v", idx, D, [&](int k) { return MP + "[" + std::to_string(base_off + (unsigned)k) + "]"; },
