@@ -567,9 +567,30 @@ std::vector<FusedOp> fuse_blocks(const std::vector<FusedOp> &ops, const std::vec
     return out;
 }
 
+// The greedy packing is sensitive to which low bits every tile is made to hold
+// (config 1 at 28 qubits: 35 stages with bits 0-2, 29 with bits 0-3; the QAOA
+// and noisy sweeps the other way round), and 256-byte runs move ~8 % faster
+// than 128-byte ones (64-byte runs are far slower: VQB_LOW_BITS=2 costs 25 %
+// per launch). Large states are planned both ways and the plan with the
+// smaller estimated time (stages x relative time per stage) runs; planning
+// costs tens of microseconds per hundred operations.
 std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k) {
+    const char *v = std::getenv("VQB_LOW_BITS");
+    if (v && *v) return plan_stages(ops, pn, k, std::max(0, std::min(6, std::atoi(v))));
+    std::vector<Stage> a = plan_stages(ops, pn, k, kLowBits);
+    if (pn < 22 || k < kLowBits + 4) return a; // small states are launch-bound: fewest stages of the default
+    std::vector<Stage> b = plan_stages(ops, pn, k, kLowBits + 1);
+    auto fused = [](const std::vector<Stage> &st) {
+        size_t n = 0;
+        for (const Stage &s : st) n += s.fused ? 1 : 0;
+        return (double)n;
+    };
+    return 0.92 * fused(b) < fused(a) ? b : a;
+}
+
+std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, int low_bits) {
     k = std::min(k, pn);
-    const int low = std::min(kLowBits, pn);
+    const int low = std::min(low_bits, pn);
     uint64_t lowmask = 0;
     for (int b = 0; b < low; ++b) lowmask |= 1ull << b;
 

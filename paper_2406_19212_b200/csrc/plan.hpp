@@ -53,6 +53,8 @@ struct Stage {
 FusedOp analyse_gate(const Gate &g);
 FusedOp analyse_rev(const RevOp &r);
 std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k);
+// with the lowest `low_bits` bits in every tile (contiguous runs of 16 * 2^low_bits bytes)
+std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, int low_bits);
 
 // Within one stage, multiply runs of non-parametric operations into dense
 // blocks on at most `max_support` qubits (an operation is moved only past

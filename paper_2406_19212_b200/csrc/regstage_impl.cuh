@@ -3251,9 +3251,11 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
                     int nt_hist[5] = {0, 0, 0, 0, 0}, nops = 0;
                     for (int i = 0; i < P.nsubs; ++i) nops += P.subs[i].op_count;
                     for (int i = 0; i < nops; ++i) nt_hist[std::min(P.ops[i].nt, 4)]++;
-                    std::fprintf(stderr, "[regstage%s] gates %zu blocks %zu subs %d ops nt0..4 %d %d %d %d %d slots %d\n",
+                    std::string tb;
+                    for (int j = 0; j < K; ++j) tb += (j ? "," : "") + std::to_string(sg.bits[j]);
+                    std::fprintf(stderr, "[regstage%s] gates %zu blocks %zu subs %d ops nt0..4 %d %d %d %d %d slots %d tile %s\n",
                                  REV ? "-rev" : "", sg.ops.size(), blocks.size(), P.nsubs, nt_hist[0],
-                                 nt_hist[1], nt_hist[2], nt_hist[3], nt_hist[4], P.nslots);
+                                 nt_hist[1], nt_hist[2], nt_hist[3], nt_hist[4], P.nslots, tb.c_str());
                 }
                 {
                     // algorithmic FP64 flops of this launch: a dense 2^nt x 2^nt
