@@ -574,11 +574,25 @@ std::vector<FusedOp> fuse_blocks(const std::vector<FusedOp> &ops, const std::vec
 // per launch). Large states are planned both ways and the plan with the
 // smaller estimated time (stages x relative time per stage) runs; planning
 // costs tens of microseconds per hundred operations.
-std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k) {
+//
+// A plan depends on the program's structure only (which bits every operation
+// touches and mixes), not on matrix values: plans are cached by that
+// structure, so a variational loop or a benchmark plans once per circuit
+// shape (the search costs ~5 ms for 800 operations).
+namespace {
+struct PlanCache {
+    std::mutex mu;
+    std::unordered_map<uint64_t, std::pair<std::vector<uint64_t>, std::vector<Stage>>> map;
+};
+PlanCache &plan_cache() {
+    static PlanCache *c = new PlanCache;
+    return *c;
+}
+std::vector<Stage> plan_stages_uncached(const std::vector<FusedOp> &ops, int pn, int k) {
     const char *v = std::getenv("VQB_LOW_BITS");
     if (v && *v) return plan_stages(ops, pn, k, std::max(0, std::min(6, std::atoi(v))));
     std::vector<Stage> a = plan_stages(ops, pn, k, kLowBits);
-    if (pn < 22 || k < kLowBits + 4) return a; // small states are launch-bound: fewest stages of the default
+    if (pn < 22 || k < kLowBits + 4) return a; // small states are launch-bound: 128-byte runs suffice
     std::vector<Stage> b = plan_stages(ops, pn, k, kLowBits + 1);
     auto fused = [](const std::vector<Stage> &st) {
         size_t n = 0;
@@ -586,6 +600,38 @@ std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k) {
         return (double)n;
     };
     return 0.92 * fused(b) < fused(a) ? b : a;
+}
+} // namespace
+
+std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k) {
+    std::vector<uint64_t> key;
+    key.reserve(2 * ops.size() + 2);
+    key.push_back((uint64_t)pn);
+    key.push_back((uint64_t)k);
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&](uint64_t w) {
+        key.push_back(w);
+        h = (h ^ w) * 1099511628211ull;
+        h ^= h >> 29;
+    };
+    for (const FusedOp &f : ops) {
+        mix(f.support);
+        mix(f.mixmask ^ (f.fusable ? 0 : 1ull << 63));
+    }
+    h ^= (uint64_t)pn * 0x9e3779b97f4a7c15ull + (uint64_t)k;
+    PlanCache &pc = plan_cache();
+    {
+        std::lock_guard<std::mutex> lk(pc.mu);
+        auto it = pc.map.find(h);
+        if (it != pc.map.end() && it->second.first == key) return it->second.second;
+    }
+    std::vector<Stage> st = plan_stages_uncached(ops, pn, k);
+    {
+        std::lock_guard<std::mutex> lk(pc.mu);
+        if (pc.map.size() >= 64) pc.map.clear();
+        pc.map[h] = {std::move(key), st};
+    }
+    return st;
 }
 
 std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, int low_bits) {
@@ -627,6 +673,58 @@ std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, i
             if (ops[i].fusable && (ops[i].mixmask & ~S) && __builtin_popcountll(need) <= k) S = need;
         }
         for (int b = 0; b < pn && __builtin_popcountll(S) < k; ++b) S |= 1ull << b;
+        // Hill climbing on the tile: swap one free tile bit for a bit a pending
+        // operation mixes while the stage would take more operations (mixing
+        // operations weigh 4, diagonal ones 1: the latter ride along anyway).
+        // First-fit alone packs config 1 into 29-35 stages and config 4 into
+        // 28-30; the climbed tiles need 24 and 18 (VQB_PLAN_SEARCH=0: first fit).
+        static const bool search = [] {
+            const char *v = std::getenv("VQB_PLAN_SEARCH");
+            return !(v && *v == '0');
+        }();
+        if (search) {
+            const uint64_t all = pn >= 64 ? ~0ull : (1ull << pn) - 1;
+            auto taken = [&](uint64_t T) {
+                uint64_t bl = 0;
+                int n = 0, w = 0, seen = 0;
+                for (int i : remaining) {
+                    const FusedOp &op = ops[i];
+                    if (n < kMaxPlanOps && !(op.support & bl) && op.fusable && (op.mixmask & ~T) == 0) {
+                        ++n;
+                        w += op.mixmask ? 4 : 1;
+                    } else {
+                        bl |= op.support;
+                        if ((bl & all) == all) break; // every qubit is behind a deferred operation
+                    }
+                    if (++seen >= 512) break;
+                }
+                return w;
+            };
+            uint64_t cand = 0;
+            int seen = 0;
+            for (int i : remaining) {
+                cand |= ops[i].mixmask;
+                if (++seen >= 160) break;
+            }
+            int best = taken(S);
+            for (int iter = 0; iter < 12; ++iter) {
+                uint64_t bestS = S;
+                for (int bo = 0; bo < pn; ++bo) {
+                    if (!(S >> bo & 1) || (lowmask >> bo & 1)) continue;
+                    for (int bi = 0; bi < pn; ++bi) {
+                        if ((S >> bi & 1) || !(cand >> bi & 1)) continue;
+                        const uint64_t T = (S & ~(1ull << bo)) | (1ull << bi);
+                        const int sc = taken(T);
+                        if (sc > best) {
+                            best = sc;
+                            bestS = T;
+                        }
+                    }
+                }
+                if (bestS == S) break;
+                S = bestS;
+            }
+        }
         // Pass 2: with the tile fixed, take every op that fits and is not
         // ordered behind a deferred op sharing a qubit.
         Stage st;
