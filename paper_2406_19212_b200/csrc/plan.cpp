@@ -2,6 +2,7 @@
 #include "plan.hpp"
 
 #include <atomic>
+#include <cstring>
 #include <chrono>
 #include <condition_variable>
 #include <mutex>
@@ -588,18 +589,61 @@ PlanCache &plan_cache() {
     static PlanCache *c = new PlanCache;
     return *c;
 }
+// Estimated time of a plan in units of one HBM pass with 128-byte runs: a
+// stage costs the larger of its pass (0.92 with 256-byte runs) and its emitted
+// FP64 work (config 1: a launch turns FP64-bound at ~127 executed flops per
+// amplitude, about 70 op_cost units).
+double plan_estimate(const std::vector<Stage> &st, const std::vector<FusedOp> &ops, int low_bits) {
+    const double pass = low_bits > kLowBits ? 0.92 : 1.0;
+    double t = 0;
+    for (const Stage &s : st) {
+        if (!s.fused) {
+            t += 1.0;
+            continue;
+        }
+        double c = 0;
+        for (int i : s.ops) c += op_cost(ops[i]);
+        t += std::max(pass, c / 70.0);
+    }
+    return t;
+}
+
+// The packing is greedy and sensitive to its knobs -- which low bits every
+// tile holds, how much the tile search favours the operations at the front of
+// the program (a ragged frontier leaves a tail of nearly empty stages) -- so a
+// small portfolio of settings is planned and the plan with the smallest
+// estimate runs. Paid once per circuit structure (plan cache).
 std::vector<Stage> plan_stages_uncached(const std::vector<FusedOp> &ops, int pn, int k) {
     const char *v = std::getenv("VQB_LOW_BITS");
-    if (v && *v) return plan_stages(ops, pn, k, std::max(0, std::min(6, std::atoi(v))));
-    std::vector<Stage> a = plan_stages(ops, pn, k, kLowBits);
-    if (pn < 22 || k < kLowBits + 4) return a; // small states are launch-bound: 128-byte runs suffice
-    std::vector<Stage> b = plan_stages(ops, pn, k, kLowBits + 1);
-    auto fused = [](const std::vector<Stage> &st) {
-        size_t n = 0;
-        for (const Stage &s : st) n += s.fused ? 1 : 0;
-        return (double)n;
-    };
-    return 0.92 * fused(b) < fused(a) ? b : a;
+    std::vector<int> lows;
+    if (v && *v) lows = {std::max(0, std::min(6, std::atoi(v)))};
+    else if (pn < 22 || k < kLowBits + 4) lows = {kLowBits}; // small states are launch-bound: 128-byte runs suffice
+    else lows = {kLowBits, kLowBits + 1};
+    static const int portfolio = [] {
+        const char *e = std::getenv("VQB_PLAN_PORTFOLIO");
+        return e && *e ? std::atoi(e) : 3;
+    }();
+    static const int front[3][2] = {{0, 128}, {32, 64}, {128, 200}};
+    std::vector<Stage> best;
+    double best_t = 0;
+    for (int low : lows)
+        for (int f = 0; f < std::max(1, std::min(3, portfolio)); ++f) {
+            std::vector<Stage> cand = plan_stages(ops, pn, k, PlanKnobs{low, front[f][0], front[f][1]});
+            static const bool by_count = [] {
+                const char *e = std::getenv("VQB_PLAN_PICK");
+                return e && std::strcmp(e, "count") == 0;
+            }();
+            double t = plan_estimate(cand, ops, low);
+            if (by_count) {
+                t = 0;
+                for (const Stage &sx : cand) t += sx.fused && low > kLowBits ? 0.92 : 1.0;
+            }
+            if (best.empty() || t < best_t - 1e-9) {
+                best = std::move(cand);
+                best_t = t;
+            }
+        }
+    return best;
 }
 } // namespace
 
@@ -635,8 +679,12 @@ std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k) {
 }
 
 std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, int low_bits) {
+    return plan_stages(ops, pn, k, PlanKnobs{low_bits, 0, 128});
+}
+
+std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, const PlanKnobs &knobs) {
     k = std::min(k, pn);
-    const int low = std::min(low_bits, pn);
+    const int low = std::min(knobs.low_bits, pn);
     uint64_t lowmask = 0;
     for (int b = 0; b < low; ++b) lowmask |= 1ull << b;
 
@@ -683,6 +731,7 @@ std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, i
             return !(v && *v == '0');
         }();
         if (search) {
+            const int gamma = knobs.gamma, gamma_window = std::max(1, knobs.window);
             const uint64_t all = pn >= 64 ? ~0ull : (1ull << pn) - 1;
             auto taken = [&](uint64_t T) {
                 uint64_t bl = 0;
@@ -691,7 +740,7 @@ std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, i
                     const FusedOp &op = ops[i];
                     if (n < kMaxPlanOps && !(op.support & bl) && op.fusable && (op.mixmask & ~T) == 0) {
                         ++n;
-                        w += op.mixmask ? 4 : 1;
+                        w += (op.mixmask ? 64 : 16) + (seen < gamma_window ? gamma * (gamma_window - seen) / gamma_window : 0);
                     } else {
                         bl |= op.support;
                         if ((bl & all) == all) break; // every qubit is behind a deferred operation

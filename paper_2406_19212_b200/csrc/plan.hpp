@@ -55,6 +55,13 @@ FusedOp analyse_rev(const RevOp &r);
 std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k);
 // with the lowest `low_bits` bits in every tile (contiguous runs of 16 * 2^low_bits bytes)
 std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, int low_bits);
+// low_bits + how the tile search weighs the front of the program: an operation
+// among the first `window` pending ones scores up to `gamma`/64 of a mixing
+// operation extra, falling linearly with its position
+struct PlanKnobs {
+    int low_bits, gamma, window;
+};
+std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, const PlanKnobs &knobs);
 
 // Within one stage, multiply runs of non-parametric operations into dense
 // blocks on at most `max_support` qubits (an operation is moved only past
