@@ -963,6 +963,7 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
                2; // + rank-one coefficients
     };
     int nops = 0, npool = 0, nslots = 0;
+    const bool sub_search = env_int("VQB_SUB_SEARCH", 1) != 0;
     while (!remaining.empty()) {
         if (P.nsubs >= kMaxSubs) break;
         unsigned rset = 0;
@@ -995,6 +996,58 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
             if (__builtin_popcount(rset | mix) <= RB) rset |= mix;
         }
         for (int j = K - 1; j >= 0 && __builtin_popcount(rset) < RB; --j) rset |= 1u << j;
+        // Hill climbing on the register set, as the stage planner does on tiles:
+        // swap one register bit for another tile bit while the sub-stage takes
+        // more operations (every sub-stage saved is one relayout of the tile
+        // through shared memory). VQB_SUB_SEARCH=0: first fit.
+        if (sub_search) {
+            auto pack = [&](unsigned rs, std::vector<int> *tk, std::vector<int> *df) {
+                uint64_t bl = 0;
+                int pool_u = 0, ops_u = 0, slots_u = 0, xp_u = 0, score = 0;
+                for (int i : remaining) {
+                    const FusedOp &f = *blocks[i];
+                    const unsigned mix = mixmask(f);
+                    const int nx = count_x(f);
+                    const bool fits_res = nops + ops_u < ops_cap && npool + pool_u + pool_need(f) <= pool_cap &&
+                                          nslots + slots_u + (rev ? f.np : 0) <= kMaxSlots &&
+                                          P.nxpat + xp_u + nx <= 256;
+                    if ((f.support & bl) || (mix & ~rs) || !fits_res) {
+                        if (df) df->push_back(i);
+                        bl |= f.support;
+                        continue;
+                    }
+                    if (tk) tk->push_back(i);
+                    pool_u += pool_need(f);
+                    xp_u += nx;
+                    ++ops_u;
+                    slots_u += rev ? f.np : 0;
+                    score += mix ? 4 : 1;
+                }
+                return score;
+            };
+            int best = pack(rset, nullptr, nullptr);
+            for (int iter = 0; iter < 6; ++iter) {
+                unsigned best_rs = rset;
+                for (int bo = 0; bo < K; ++bo) {
+                    if (!(rset >> bo & 1)) continue;
+                    for (int bi = 0; bi < K; ++bi) {
+                        if (rset >> bi & 1) continue;
+                        const unsigned rs = (rset & ~(1u << bo)) | (1u << bi);
+                        const int sc = pack(rs, nullptr, nullptr);
+                        if (sc > best) {
+                            best = sc;
+                            best_rs = rs;
+                        }
+                    }
+                }
+                if (best_rs == rset) break;
+                rset = best_rs;
+            }
+            taken.clear();
+            deferred.clear();
+            pack(rset, &taken, &deferred);
+            if (taken.empty()) break;
+        }
         RSub &sb = P.subs[P.nsubs++];
         {
             int nr = 0;
