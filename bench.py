@@ -486,9 +486,12 @@ def roofline_of(eng, wl, prof, launch_recs, step_flops, world):
     avg_s = tot_ms / cnt / 1e3
     achieved = bytes_per_launch / avg_s / 1e9
     traffic = None
+    fp64_pipe = None
     try:
         with open(TRAFFIC_PATH) as f:
-            traffic = json.load(f).get(wl.name, {}).get(name)
+            rec = json.load(f).get(wl.name, {})
+        traffic = rec.get(name)
+        fp64_pipe = rec.get("fp64_pipe_active_pct", {}).get(name)
     except Exception:
         pass
     step_ms = sum(v[1] for v in prof.values())
@@ -497,6 +500,10 @@ def roofline_of(eng, wl, prof, launch_recs, step_flops, world):
             "peak_source": peak_kind, "launches_per_step": cnt,
             "avg_launch_us": 1e6 * avg_s, "share_of_step": tot_ms / step_ms if step_ms else None,
             "algorithmic_bytes_per_launch": bytes_per_launch}
+    if fp64_pipe:
+        # from the committed ncu capture of this kernel (like `traffic`): how
+        # busy the FP64 pipe is, [min, max] % over the captured launches
+        roof["fp64_pipe_active_pct_ncu"] = fp64_pipe
     dfma, dfma_kind = dfma_peak()
     fused_ms = sum(v[1] for k, v in prof.items() if k.startswith("k_regstage") or k.startswith("k_stage"))
     if step_flops > 0 and fused_ms > 0:

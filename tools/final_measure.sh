@@ -10,6 +10,7 @@ for c in rqc28 hea20 qaoa30 noisy15 rqc33; do
 done
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/final/launches_rqc28.csv \
     python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/final/ncu_launch.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:vqb_stage --launch-skip 120 --launch-count 3 \
-    -o gpurun_out/final/ncu_full_rqc28 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/final/ncu_full.log 2>&1
+# three consecutive stage launches of the headline config (after its warm-up steps)
+ncu --set full --import-source on --clock-control none -k regex:vqb_stage --launch-skip 70 --launch-count 4 \
+    -o gpurun_out/final/ncu_full_rqc28 python bench.py --config rqc28 --no-extra --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/final/ncu_full.log 2>&1
 echo done
