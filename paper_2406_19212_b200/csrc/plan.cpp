@@ -662,6 +662,13 @@ std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k) {
         mix(f.support);
         mix(f.mixmask ^ (f.fusable ? 0 : 1ull << 63));
     }
+    // the planner's switches are part of the key (tests flip them in one process)
+    for (const char *e : {"VQB_LOW_BITS", "VQB_PLAN_PORTFOLIO", "VQB_PLAN_SEARCH", "VQB_PLAN_PICK"}) {
+        const char *v = std::getenv(e);
+        uint64_t w = 0xcbf29ce484222325ull;
+        for (; v && *v; ++v) w = (w ^ (unsigned char)*v) * 1099511628211ull;
+        mix(w);
+    }
     h ^= (uint64_t)pn * 0x9e3779b97f4a7c15ull + (uint64_t)k;
     PlanCache &pc = plan_cache();
     {

@@ -64,3 +64,26 @@ def test_parallel_planning_generates_the_same_kernels(tmp_path):
     assert na == nb and na
     for n in na:
         assert open(a / n, "rb").read() == open(b / n, "rb").read(), n
+
+
+def stage_count(tmp_path, config, **env_extra):
+    out = tmp_path / ("plan_" + config + "_" + "_".join(f"{k}{v}" for k, v in env_extra.items()))
+    env = dict(os.environ, VQB_PLAN_STATS="1", VQB_PLAN_THREADS="0", **env_extra)
+    env.pop("VQB_JIT", None)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "dryrun_dump.py"), config, str(out)],
+                       capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return len(re.findall(r"^\[regstage\] ", r.stderr, re.M)), len(re.findall(r"^\[regstage-rev\] ", r.stderr, re.M))
+
+
+def test_searched_plan_needs_fewer_launches_than_first_fit(tmp_path):
+    """Config 1 at its full size (host side only): the hill-climbed tiles pack
+    the 785 gates into far fewer stages (HBM passes) than first fit -- 35 with
+    3 forced low bits, 29 with 4 -- and the QAOA gradient of config 2 needs
+    fewer forward and adjoint launches too."""
+    first_fit, _ = stage_count(tmp_path, "rqc28", VQB_PLAN_SEARCH="0")
+    searched, _ = stage_count(tmp_path, "rqc28")
+    assert first_fit >= 29 and searched <= 24 and searched < first_fit, (first_fit, searched)
+    f0, r0 = stage_count(tmp_path, "qaoa30", VQB_PLAN_SEARCH="0")
+    f1, r1 = stage_count(tmp_path, "qaoa30")
+    assert f1 <= f0 and r1 <= r0 and f1 + r1 < f0 + r0, (f0, r0, f1, r1)
