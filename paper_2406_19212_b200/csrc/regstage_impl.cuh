@@ -963,7 +963,17 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
                2; // + rank-one coefficients
     };
     int nops = 0, npool = 0, nslots = 0;
-    const bool sub_search = env_int("VQB_SUB_SEARCH", 1) != 0;
+    // (states below 2^22 amplitudes are host-bound: their relayouts are cheap
+    // and the search's host time is not)
+    const bool sub_search = env_int("VQB_SUB_SEARCH", pn >= 22 ? 1 : 0) != 0;
+    // per-block figures the packing loops below read many times
+    std::vector<unsigned> mix_of(blocks.size());
+    std::vector<int> nx_of(blocks.size()), need_of(blocks.size());
+    for (int i : remaining) {
+        mix_of[i] = mixmask(*blocks[i]);
+        nx_of[i] = count_x(*blocks[i]);
+        need_of[i] = pool_need(*blocks[i]);
+    }
     while (!remaining.empty()) {
         if (P.nsubs >= kMaxSubs) break;
         unsigned rset = 0;
@@ -972,10 +982,10 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
         int pool_used = 0, ops_used = 0, slots_used = 0, xp_used = 0;
         for (int i : remaining) {
             const FusedOp &f = *blocks[i];
-            const unsigned mix = mixmask(f);
-            const int nx = count_x(f);
+            const unsigned mix = mix_of[i];
+            const int nx = nx_of[i];
             const bool fits_res = nops + ops_used < ops_cap &&
-                                  npool + pool_used + pool_need(f) <= pool_cap &&
+                                  npool + pool_used + need_of[i] <= pool_cap &&
                                   nslots + slots_used + (rev ? f.np : 0) <= kMaxSlots &&
                                   P.nxpat + xp_used + nx <= 256;
             if ((f.support & blocked) || __builtin_popcount(rset | mix) > RB || !fits_res) {
@@ -985,14 +995,14 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
             }
             rset |= mix;
             taken.push_back(i);
-            pool_used += pool_need(f);
+            pool_used += need_of[i];
             xp_used += nx;
             ++ops_used;
             slots_used += rev ? f.np : 0;
         }
         if (taken.empty()) break; // parameter block full: continue in the next launch
         for (int i : deferred) {
-            const unsigned mix = mixmask(*blocks[i]);
+            const unsigned mix = mix_of[i];
             if (__builtin_popcount(rset | mix) <= RB) rset |= mix;
         }
         for (int j = K - 1; j >= 0 && __builtin_popcount(rset) < RB; --j) rset |= 1u << j;
@@ -1006,9 +1016,9 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
                 int pool_u = 0, ops_u = 0, slots_u = 0, xp_u = 0, score = 0;
                 for (int i : remaining) {
                     const FusedOp &f = *blocks[i];
-                    const unsigned mix = mixmask(f);
-                    const int nx = count_x(f);
-                    const bool fits_res = nops + ops_u < ops_cap && npool + pool_u + pool_need(f) <= pool_cap &&
+                    const unsigned mix = mix_of[i];
+                    const int nx = nx_of[i];
+                    const bool fits_res = nops + ops_u < ops_cap && npool + pool_u + need_of[i] <= pool_cap &&
                                           nslots + slots_u + (rev ? f.np : 0) <= kMaxSlots &&
                                           P.nxpat + xp_u + nx <= 256;
                     if ((f.support & bl) || (mix & ~rs) || !fits_res) {
@@ -1017,7 +1027,7 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
                         continue;
                     }
                     if (tk) tk->push_back(i);
-                    pool_u += pool_need(f);
+                    pool_u += need_of[i];
                     xp_u += nx;
                     ++ops_u;
                     slots_u += rev ? f.np : 0;
