@@ -78,7 +78,7 @@ constexpr int NPART = NW * (32 / LANES_PER_PART);
 constexpr int B3 = RB > 3 ? 3 : 0;
 
 constexpr int kMaxSubs = 32;
-constexpr int kMaxOps = 56;
+constexpr int kMaxOps = 84; // (ROp is 112 bytes: the parameter block stays under 32 KB)
 constexpr int kMaxSlots = 64;
 constexpr int kMaxPool = 1072; // double2 entries
 constexpr int kMaxTab = 192;   // per-element diagonal tables, copied to shared memory
@@ -94,14 +94,14 @@ struct ROp {
     int per_group;        // condition depends on register bits
     int pair;             // psi has its own matrices (channel steps)
     int slot;             // first gradient slot (param ops)
-    int ck[kMaxCond];     // 0: outside tile, 1: thread bit, 2: register bit
-    int cp[kMaxCond];     // global bit / thread bit / register bit
+    signed char ck[kMaxCond]; // 0: outside tile, 1: thread bit, 2: register bit
+    signed char cp[kMaxCond]; // global bit / thread bit / register bit
     unsigned mat, mat_psi, mat_d; // pool offsets (2^nc sub-matrices each, ascending order)
     unsigned long long ident, ident_psi;
-    int rw[RB];           // condition-index bits contributed by register bit b
+    unsigned char rw[RB]; // condition-index bits contributed by register bit b
     int tab, tab_psi;     // nt = 0 with register conditions: shared-memory tables
     int xoff, nx;         // nt >= 3: XOR patterns of the diagonal-times-permutation terms
-    int lb[kMaxMix];      // nt >= 3: tile-local mixing bits in matrix bit order
+    signed char lb[kMaxMix]; // nt >= 3: tile-local mixing bits in matrix bit order
     // nt = 0 adjoint steps: every phase has modulus 1 (conj(psi) phi is then
     // invariant under the step) and, for parametric ones, the tables
     // e_p[c] = D_p[c] * M[c] at pool offset mat_e
@@ -969,10 +969,31 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
     // per-block figures the packing loops below read many times
     std::vector<unsigned> mix_of(blocks.size());
     std::vector<int> nx_of(blocks.size()), need_of(blocks.size());
+    // Channel steps that run in rank-one form (both states of an adjoint pair
+    // step, or a forward superoperator) read one coefficient each and no
+    // matrix: their matrices and XOR patterns are left out of the parameter
+    // block, which is what a launch's capacity is mostly spent on in the
+    // density-matrix sweeps (130 pool entries per 2-qubit channel otherwise).
+    // Such a launch has no interpreter form (ROp::unit bit 4).
+    std::vector<char> r1_of(blocks.size(), 0);
+    const bool r1_allowed = factor && env_int("VQB_JIT_PAIRFACTOR", 1) != 0 && env_int("VQB_JIT_RANKONE", 1) != 0 &&
+                            env_int("VQB_JIT_R1_OMIT", 1) != 0;
     for (int i : remaining) {
-        mix_of[i] = mixmask(*blocks[i]);
-        nx_of[i] = count_x(*blocks[i]);
-        need_of[i] = pool_need(*blocks[i]);
+        const FusedOp &f = *blocks[i];
+        mix_of[i] = mixmask(f);
+        nx_of[i] = count_x(f);
+        need_of[i] = pool_need(f);
+        if (!r1_allowed || f.np != 0 || f.nc != 0 || !(f.nt <= 2 || wide_in_regs(f))) continue;
+        if (rev && f.pair && f.nt >= 1) {
+            const PairForm a = pair_form(f.sub_phi, f.nt), b = pair_form(f.sub_psi, f.nt);
+            r1_of[i] = a.mask && a.mask == b.mask;
+        } else if (!rev && !f.pair && f.nt >= 2) {
+            r1_of[i] = pair_form(f.sub_phi, f.nt).mask != 0;
+        }
+        if (r1_of[i]) {
+            need_of[i] = 2;
+            nx_of[i] = 0;
+        }
     }
     while (!remaining.empty()) {
         if (P.nsubs >= kMaxSubs) break;
@@ -1209,7 +1230,12 @@ void lower_stage_reg(const Stage &sg, const std::vector<const FusedOp *> &blocks
                     fwd_form = true;
                 }
             }
-            if (f.nt >= 3) {
+            const bool omit = r1_of[i] && (o.unit & 4) && (!f.pair || (o.unit & 8));
+            if (omit) {
+                o.unit |= 16; // rank-one form only: no matrices in the block
+                o.xoff = P.nxpat;
+                o.nx = 0;
+            } else if (f.nt >= 3) {
                 // wide ops run in smem_op as sum_k diag(d_k) P_{x_k}: store the
                 // XOR patterns x_k and, per sub-matrix, d_k[r] = S[r, r ^ x_k]
                 auto permuted = [&](const cvec &src, int c) {
@@ -3209,7 +3235,7 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
             int nops = 0;
             for (int i = 0; i < P.nsubs; ++i) nops = std::max(nops, P.subs[i].op_begin + P.subs[i].op_count);
             for (int i = 0; i < nops; ++i)
-                if (P.ops[i].inreg || (P.ops[i].nt > 0 && (P.ops[i].unit & 2)))
+                if (P.ops[i].inreg || (P.ops[i].nt > 0 && (P.ops[i].unit & 2)) || (P.ops[i].unit & 16))
                     raise(VQB_ERR_INTERNAL, "stage program with register-resident wide operations has no "
                                             "specialised kernel (set VQB_WIDE_REGS=0)");
         }
