@@ -613,7 +613,7 @@ double plan_estimate(const std::vector<Stage> &st, const std::vector<FusedOp> &o
 // the program (a ragged frontier leaves a tail of nearly empty stages) -- so a
 // small portfolio of settings is planned and the plan with the smallest
 // estimate runs. Paid once per circuit structure (plan cache).
-std::vector<Stage> plan_stages_uncached(const std::vector<FusedOp> &ops, int pn, int k) {
+std::vector<Stage> plan_stages_uncached(const std::vector<FusedOp> &ops, int pn, int k, int max_ops) {
     const char *v = std::getenv("VQB_LOW_BITS");
     std::vector<int> lows;
     if (v && *v) lows = {std::max(0, std::min(6, std::atoi(v)))};
@@ -628,7 +628,7 @@ std::vector<Stage> plan_stages_uncached(const std::vector<FusedOp> &ops, int pn,
     double best_t = 0;
     for (int low : lows)
         for (int f = 0; f < std::max(1, std::min(3, portfolio)); ++f) {
-            std::vector<Stage> cand = plan_stages(ops, pn, k, PlanKnobs{low, front[f][0], front[f][1]});
+            std::vector<Stage> cand = plan_stages(ops, pn, k, PlanKnobs{low, front[f][0], front[f][1], max_ops});
             static const bool by_count = [] {
                 const char *e = std::getenv("VQB_PLAN_PICK");
                 return e && std::strcmp(e, "count") == 0;
@@ -647,12 +647,12 @@ std::vector<Stage> plan_stages_uncached(const std::vector<FusedOp> &ops, int pn,
 }
 } // namespace
 
-std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k) {
+std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, int max_ops) {
     std::vector<uint64_t> key;
     key.reserve(2 * ops.size() + 2);
     key.push_back((uint64_t)pn);
-    key.push_back((uint64_t)k);
-    uint64_t h = 1469598103934665603ull;
+    key.push_back((uint64_t)k | (uint64_t)max_ops << 32);
+    uint64_t h = 1469598103934665603ull ^ (uint64_t)max_ops;
     auto mix = [&](uint64_t w) {
         key.push_back(w);
         h = (h ^ w) * 1099511628211ull;
@@ -676,17 +676,13 @@ std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k) {
         auto it = pc.map.find(h);
         if (it != pc.map.end() && it->second.first == key) return it->second.second;
     }
-    std::vector<Stage> st = plan_stages_uncached(ops, pn, k);
+    std::vector<Stage> st = plan_stages_uncached(ops, pn, k, max_ops);
     {
         std::lock_guard<std::mutex> lk(pc.mu);
         if (pc.map.size() >= 64) pc.map.clear();
         pc.map[h] = {std::move(key), st};
     }
     return st;
-}
-
-std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, int low_bits) {
-    return plan_stages(ops, pn, k, PlanKnobs{low_bits, 0, 128});
 }
 
 std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, const PlanKnobs &knobs) {
@@ -745,7 +741,7 @@ std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, c
                 int n = 0, w = 0, seen = 0;
                 for (int i : remaining) {
                     const FusedOp &op = ops[i];
-                    if (n < kMaxPlanOps && !(op.support & bl) && op.fusable && (op.mixmask & ~T) == 0) {
+                    if (n < knobs.max_ops && !(op.support & bl) && op.fusable && (op.mixmask & ~T) == 0) {
                         ++n;
                         w += (op.mixmask ? 64 : 16) + (seen < gamma_window ? gamma * (gamma_window - seen) / gamma_window : 0);
                     } else {
@@ -792,7 +788,7 @@ std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, c
         blocked = 0;
         for (int i : remaining) {
             const FusedOp &op = ops[i];
-            if ((int)st.ops.size() < kMaxPlanOps && !(op.support & blocked) && op.fusable &&
+            if ((int)st.ops.size() < knobs.max_ops && !(op.support & blocked) && op.fusable &&
                 (op.mixmask & ~S) == 0) {
                 st.ops.push_back(i);
             } else {

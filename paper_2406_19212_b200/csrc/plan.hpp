@@ -52,14 +52,14 @@ struct Stage {
 
 FusedOp analyse_gate(const Gate &g);
 FusedOp analyse_rev(const RevOp &r);
-std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k);
-// with the lowest `low_bits` bits in every tile (contiguous runs of 16 * 2^low_bits bytes)
-std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, int low_bits);
-// low_bits + how the tile search weighs the front of the program: an operation
+std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, int max_ops = kMaxPlanOps);
+// one setting of the greedy packing: the lowest `low_bits` bits are in every
+// tile (contiguous runs of 16 * 2^low_bits bytes) + how the tile search weighs the front of the program: an operation
 // among the first `window` pending ones scores up to `gamma`/64 of a mixing
 // operation extra, falling linearly with its position
 struct PlanKnobs {
     int low_bits, gamma, window;
+    int max_ops = kMaxPlanOps; // operations per stage (the register executor splits a stage into launches itself)
 };
 std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, const PlanKnobs &knobs);
 

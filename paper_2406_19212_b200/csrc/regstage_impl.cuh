@@ -3152,7 +3152,10 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
     std::vector<Stage> stages;
     {
         HostTimer ht(REV ? "plan_stages (rev)" : "plan_stages (fwd)");
-        stages = plan_stages(fops, pn, K);
+        // the executor splits a stage into launches itself (kMaxOps blocks each),
+        // and block fusion shrinks runs of gates: stages may hold more operations
+        // than the shared-memory interpreter's limit
+        stages = plan_stages(fops, pn, K, env_int("VQB_STAGE_OPS", 192));
     }
     const int max_support = env_int("VQB_FUSE_QUBITS", 2);
     const bool stats = std::getenv("VQB_PLAN_STATS") != nullptr;
