@@ -624,11 +624,20 @@ std::vector<Stage> plan_stages_uncached(const std::vector<FusedOp> &ops, int pn,
         return e && *e ? std::atoi(e) : 3;
     }();
     static const int front[3][2] = {{0, 128}, {32, 64}, {128, 200}};
+    // starting points of the tile search per stage: 12 for large states (config
+    // 3's adjoint: 27 launches without, 23 with, 21 with 24 of them, which
+    // costs config 1 two launches: profiles/r2_ab_plan_seeds.txt), 6 for the
+    // small, host-bound ones
+    std::vector<int> seed_counts;
+    if (const char *e = std::getenv("VQB_PLAN_SEEDS"); e && *e) seed_counts = {std::atoi(e)};
+    else seed_counts = {pn < 22 ? 6 : 12};
     std::vector<Stage> best;
     double best_t = 0;
+    for (int seeds : seed_counts)
     for (int low : lows)
         for (int f = 0; f < std::max(1, std::min(3, portfolio)); ++f) {
-            std::vector<Stage> cand = plan_stages(ops, pn, k, PlanKnobs{low, front[f][0], front[f][1], max_ops});
+            std::vector<Stage> cand =
+                plan_stages(ops, pn, k, PlanKnobs{low, front[f][0], front[f][1], max_ops, seeds});
             static const bool by_count = [] {
                 const char *e = std::getenv("VQB_PLAN_PICK");
                 return e && std::strcmp(e, "count") == 0;
@@ -663,7 +672,7 @@ std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, i
         mix(f.mixmask ^ (f.fusable ? 0 : 1ull << 63));
     }
     // the planner's switches are part of the key (tests flip them in one process)
-    for (const char *e : {"VQB_LOW_BITS", "VQB_PLAN_PORTFOLIO", "VQB_PLAN_SEARCH", "VQB_PLAN_PICK"}) {
+    for (const char *e : {"VQB_LOW_BITS", "VQB_PLAN_PORTFOLIO", "VQB_PLAN_SEARCH", "VQB_PLAN_PICK", "VQB_PLAN_SEEDS"}) {
         const char *v = std::getenv(e);
         uint64_t w = 0xcbf29ce484222325ull;
         for (; v && *v; ++v) w = (w ^ (unsigned char)*v) * 1099511628211ull;
@@ -704,8 +713,12 @@ std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, c
             remaining.erase(remaining.begin());
             continue;
         }
-        // Pass 1: greedy tile selection in program order.
-        uint64_t S = lowmask, blocked = 0;
+        // Pass 1: greedy tile selection in program order, from the tile bits
+        // `seed` (the forced low bits, or those plus one pending operation's
+        // mixing bits: several starting points are tried below).
+        int tile_score = 0;
+        auto build_tile = [&](uint64_t seed) {
+        uint64_t S = seed, blocked = 0;
         for (int i : remaining) {
             const FusedOp &op = ops[i];
             if ((op.support & blocked) || !op.fusable) {
@@ -776,7 +789,35 @@ std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, c
                 if (bestS == S) break;
                 S = bestS;
             }
+            tile_score = best;
         }
+        return S;
+        };
+        uint64_t S = build_tile(lowmask);
+        // Other starting points: the tile seeded with one pending operation's
+        // mixing bits. The first pending operations may be stragglers (config
+        // 3's reverse sweep starts with one channel per qubit, and a tile grown
+        // from four of them takes those four and nothing else); a tile grown
+        // from an operation further along may take a whole chain, and the
+        // stragglers ride with a later stage that holds their qubits anyway.
+        if (knobs.seeds > 0 && tile_score > 0) {
+            int best_score = tile_score, tried = 0;
+            uint64_t seen_seed = 0;
+            for (int i : remaining) {
+                if (tried >= knobs.seeds) break;
+                const uint64_t m = ops[i].mixmask & ~lowmask;
+                if (!ops[i].fusable || !m || (m & ~seen_seed) == 0) continue;
+                seen_seed |= m;
+                if (__builtin_popcountll(lowmask | m) > k) continue;
+                ++tried;
+                const uint64_t T = build_tile(lowmask | m);
+                if (tile_score > best_score) {
+                    best_score = tile_score;
+                    S = T;
+                }
+            }
+        }
+        uint64_t blocked = 0;
         // Pass 2: with the tile fixed, take every op that fits and is not
         // ordered behind a deferred op sharing a qubit.
         Stage st;
@@ -785,7 +826,6 @@ std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, c
         for (int b = 0; b < pn; ++b)
             if (S >> b & 1) st.bits[nb++] = b;
         std::vector<int> deferred;
-        blocked = 0;
         for (int i : remaining) {
             const FusedOp &op = ops[i];
             if ((int)st.ops.size() < knobs.max_ops && !(op.support & blocked) && op.fusable &&

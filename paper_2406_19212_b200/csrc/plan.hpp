@@ -60,6 +60,7 @@ std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, i
 struct PlanKnobs {
     int low_bits, gamma, window;
     int max_ops = kMaxPlanOps; // operations per stage (the register executor splits a stage into launches itself)
+    int seeds = 0;             // extra starting points of the tile search (pending operations' mixing bits)
 };
 std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, const PlanKnobs &knobs);
 
