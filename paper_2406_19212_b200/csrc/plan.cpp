@@ -631,11 +631,15 @@ std::vector<Stage> plan_stages_uncached(const std::vector<FusedOp> &ops, int pn,
     std::vector<int> seed_counts;
     if (const char *e = std::getenv("VQB_PLAN_SEEDS"); e && *e) seed_counts = {std::atoi(e)};
     else seed_counts = {pn < 22 ? 6 : 12};
+    // very long programs: the search is linear in the operation count (~0.2 ms
+    // per operation with the whole portfolio); keep the one-time cost bounded
+    const bool huge = ops.size() > 4000;
+    if (huge && seed_counts[0] > 4) seed_counts[0] = 4;
     std::vector<Stage> best;
     double best_t = 0;
     for (int seeds : seed_counts)
     for (int low : lows)
-        for (int f = 0; f < std::max(1, std::min(3, portfolio)); ++f) {
+        for (int f = 0; f < std::max(1, std::min(huge ? 1 : 3, portfolio)); ++f) {
             std::vector<Stage> cand =
                 plan_stages(ops, pn, k, PlanKnobs{low, front[f][0], front[f][1], max_ops, seeds});
             static const bool by_count = [] {
