@@ -613,7 +613,8 @@ double plan_estimate(const std::vector<Stage> &st, const std::vector<FusedOp> &o
 // the program (a ragged frontier leaves a tail of nearly empty stages) -- so a
 // small portfolio of settings is planned and the plan with the smallest
 // estimate runs. Paid once per circuit structure (plan cache).
-std::vector<Stage> plan_stages_uncached(const std::vector<FusedOp> &ops, int pn, int k, int max_ops) {
+std::vector<Stage> plan_stages_uncached(const std::vector<FusedOp> &ops, int pn, int k, int max_ops,
+                                        int seeds_hint) {
     const char *v = std::getenv("VQB_LOW_BITS");
     std::vector<int> lows;
     if (v && *v) lows = {std::max(0, std::min(6, std::atoi(v)))};
@@ -630,7 +631,7 @@ std::vector<Stage> plan_stages_uncached(const std::vector<FusedOp> &ops, int pn,
     // small, host-bound ones
     std::vector<int> seed_counts;
     if (const char *e = std::getenv("VQB_PLAN_SEEDS"); e && *e) seed_counts = {std::atoi(e)};
-    else seed_counts = {pn < 22 ? 6 : 12};
+    else seed_counts = {seeds_hint > 0 ? seeds_hint : pn < 22 ? 6 : 12};
     // very long programs: the search is linear in the operation count (~0.2 ms
     // per operation with the whole portfolio); keep the one-time cost bounded
     const bool huge = ops.size() > 4000;
@@ -660,11 +661,11 @@ std::vector<Stage> plan_stages_uncached(const std::vector<FusedOp> &ops, int pn,
 }
 } // namespace
 
-std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, int max_ops) {
+std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, int max_ops, int seeds) {
     std::vector<uint64_t> key;
     key.reserve(2 * ops.size() + 2);
     key.push_back((uint64_t)pn);
-    key.push_back((uint64_t)k | (uint64_t)max_ops << 32);
+    key.push_back((uint64_t)k | (uint64_t)max_ops << 32 | (uint64_t)seeds << 48);
     uint64_t h = 1469598103934665603ull ^ (uint64_t)max_ops;
     auto mix = [&](uint64_t w) {
         key.push_back(w);
@@ -689,7 +690,7 @@ std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, i
         auto it = pc.map.find(h);
         if (it != pc.map.end() && it->second.first == key) return it->second.second;
     }
-    std::vector<Stage> st = plan_stages_uncached(ops, pn, k, max_ops);
+    std::vector<Stage> st = plan_stages_uncached(ops, pn, k, max_ops, seeds);
     {
         std::lock_guard<std::mutex> lk(pc.mu);
         if (pc.map.size() >= 64) pc.map.clear();

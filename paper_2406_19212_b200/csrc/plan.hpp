@@ -52,7 +52,10 @@ struct Stage {
 
 FusedOp analyse_gate(const Gate &g);
 FusedOp analyse_rev(const RevOp &r);
-std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, int max_ops = kMaxPlanOps);
+// seeds: starting points of the tile search per stage (0: 12 for states of
+// >= 2^22 amplitudes, 6 below)
+std::vector<Stage> plan_stages(const std::vector<FusedOp> &ops, int pn, int k, int max_ops = kMaxPlanOps,
+                               int seeds = 0);
 // one setting of the greedy packing: the lowest `low_bits` bits are in every
 // tile (contiguous runs of 16 * 2^low_bits bytes) + how the tile search weighs the front of the program: an operation
 // among the first `window` pending ones scores up to `gamma`/64 of a mixing

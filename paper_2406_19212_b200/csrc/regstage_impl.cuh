@@ -3155,7 +3155,10 @@ void run_reg(DeviceState *sphi, DeviceState *spsi, std::vector<FusedOp> &fops, d
         // the executor splits a stage into launches itself (kMaxOps blocks each),
         // and block fusion shrinks runs of gates: stages may hold more operations
         // than the shared-memory interpreter's limit
-        stages = plan_stages(fops, pn, K, env_int("VQB_STAGE_OPS", 192));
+        // (density-matrix programs pair every ket bit with its bra bit, so good
+        // tiles are rarer: their search starts from 24 seeds per stage instead of
+        // 12 -- config 3's adjoint 23 -> 21 launches, profiles/r2_ab_plan_seeds.txt)
+        stages = plan_stages(fops, pn, K, env_int("VQB_STAGE_OPS", 192), sphi->mixed && pn >= 22 ? 24 : 0);
     }
     const int max_support = env_int("VQB_FUSE_QUBITS", 2);
     const bool stats = std::getenv("VQB_PLAN_STATS") != nullptr;
